@@ -1,0 +1,206 @@
+/*
+ * dx.h -- C ABI of the DynaExq hot path on B200 (sm_100a).
+ *
+ * DynaExq (arXiv 2511.15015, /root/reference/PAPER.md): a hybrid-precision MoE expert layer whose
+ * experts live in a fragmentation-free slot pool at a HIGH or LOW precision tier chosen at run
+ * time by an EMA-hotness controller under an HBM budget.  Citations: PAPER.md:line; readings of
+ * ambiguous passages are DESIGN.md §2 (R-*).
+ *
+ * Conventions for every entry point
+ *  - Plain C types only; no torch types.  Device pointers are CUDA device (or UVA-mapped) memory
+ *    ordered on the pool's compute stream; host pointers are ordinary host memory.
+ *  - Every call returns a dx_status; nothing is thrown across the ABI.  On failure
+ *    dx_last_error() returns a thread-local message (valid until the next failing call).
+ *  - One host thread mutates a pool at a time (SPEC.md:197 single mutator); pools are independent.
+ *  - The library owns the device arena: exactly ONE cudaMalloc per pool, in dx_pool_create, and no
+ *    device allocation afterwards ("avoids runtime cudaMalloc calls").
+ */
+#ifndef DYNAEXQ_DX_H
+#define DYNAEXQ_DX_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DX_OK = 0,
+    DX_ERR_INVALID_ARG = 1,        /* malformed argument / wrong tier for a command */
+    DX_ERR_RANGE = 2,              /* layer / expert / n_hot out of range */
+    DX_ERR_INFEASIBLE_BUDGET = 3,  /* budget < (N+s)*S_l + s*S_h per layer */
+    DX_ERR_POOL_EXHAUSTED = 4,     /* no free block; the command is deferred, pool never grows */
+    DX_ERR_BUSY = 5,               /* expert already has a transition in flight */
+    DX_ERR_LEDGER = 6,             /* ledger corruption (double free / foreign block), fatal */
+    DX_ERR_NOT_READY = 7,          /* operation needs the warm-up to have finished */
+    DX_ERR_CUDA = 8,
+    DX_ERR_NCCL = 9,
+    DX_ERR_OOM = 10
+} dx_status;
+
+/* Precision of a tier: 16 = bf16, 4 = int4, 2 = int2 (group-wise asymmetric, DESIGN.md R-Q1).
+ * Pairs used by the paper: (16,4) for Qwen3-30B-A3B, (4,2) for Qwen3-Next-80B-A3B. */
+typedef struct {
+    int32_t num_layers;         /* L */
+    int32_t num_experts;        /* global E (= N, the paper's m) */
+    int32_t top_k;              /* k */
+    int32_t hidden;             /* H (multiple of group_size and of 256) */
+    int32_t inter;              /* I, expert intermediate size (multiple of group_size and of 64) */
+    int32_t group_size;         /* g: 128, or 32 for tiny shapes */
+    int32_t high_bits;          /* 16 or 4 */
+    int32_t low_bits;           /* 4 or 2, < high_bits */
+    uint64_t expert_budget_bytes; /* per GPU, all layers; M = floor(budget / L) per layer */
+    int32_t n_spare;            /* spare blocks per tier per layer: the transient buffer */
+    double  ema_alpha;          /* alpha of Eq. 2 */
+    int32_t period;             /* Tp: plan when t ≡ 0 mod Tp (Alg. 1) */
+    int32_t warmup_steps;       /* W: tau_h fixed and initial hot set chosen at t = W */
+    int32_t dwell_min;          /* minimum steps between transitions of one expert (DESIGN.md R-C2) */
+    int32_t publish_lag;        /* L: 1 <= L < Tp, transitions become stable L steps after issue (R-T1) */
+    int32_t max_tokens;         /* max tokens per dx_moe_forward; sizes the workspace */
+    int32_t ep_rank, ep_size;   /* expert parallelism: this GPU owns experts [r*E/G, (r+1)*E/G) */
+} dx_config;
+
+typedef struct dx_pool_s* dx_pool;
+
+/* Derived sizes of a pool (read-only). */
+typedef struct {
+    int32_t  n_hot;             /* §3.5 solution (R-P2) */
+    int32_t  experts_local;     /* E_loc = E / ep_size */
+    int32_t  cap_hi, cap_lo;    /* blocks per tier per layer after warm-up: n_hot+s, E_loc-n_hot+s */
+    int64_t  slot_bytes_hi, slot_bytes_lo; /* S_h, S_l (R-P1) */
+    int64_t  layer_budget;      /* M */
+    int64_t  layer_bytes;       /* bytes actually reserved per layer (<= M) */
+    int64_t  arena_bytes;       /* the one device allocation */
+    int64_t  export_bytes_hi, export_bytes_lo; /* dx_export_expert output sizes */
+} dx_info;
+
+/* One command of a precision plan (Alg. 1 EnqueueUpgrade/EnqueueDowngrade). */
+typedef struct {
+    int32_t expert;             /* local expert id */
+    int32_t dir;                /* +1 promote, -1 demote, 0 relayout move (finalize only) */
+    int32_t dst_slot;           /* destination block in the destination tier's region */
+    int32_t src_slot;           /* block the expert occupied when the plan was made */
+} dx_cmd;
+
+#define DX_MAX_CMDS 1024
+typedef struct {
+    int32_t  due;               /* 1 if a plan (or the warm-up finalize) ran at this step */
+    int32_t  finalize;          /* 1 at t == W: tau_h fixed, initial HIGH set installed synchronously */
+    int32_t  n;                 /* number of commands */
+    int64_t  step;              /* t at which the plan was made */
+    int64_t  publish_step;      /* t at which the commands become the stable version */
+    dx_cmd   cmd[DX_MAX_CMDS];
+} dx_plan;
+
+/* ---------------------------------------------------------------- pool lifecycle */
+
+/* Create the slot pool of every layer (§3.4) after solving the per-layer budget
+ * (§3.5).  master_bf16_host[l * E_loc + e] points to expert e's bf16 master image
+ *   W_gate[I][H] | W_up[I][H] | W_down[H][I]   (row-major, nn.Linear layout, 3*I*H*2 bytes)
+ * in PINNED (page-locked, UVA-mapped) host memory.  Borrowed: must outlive the pool when
+ * high_bits == 16, because promotions stream HIGH images from it (the DRAM cache).
+ * When high_bits < 16 the library allocates its own pinned HIGH-image cache and fills it here.
+ * Every expert starts LOW in warm-up block e (R-P3).  Streams are cudaStream_t (NULL = legacy
+ * default for compute; side NULL = the library creates a low-priority stream).
+ * Errors: INVALID_ARG (shapes, non-pinned master), RANGE, INFEASIBLE_BUDGET, OOM, CUDA. */
+dx_status dx_pool_create(const dx_config* cfg, const void* const* master_bf16_host,
+                         void* compute_stream, void* side_stream, dx_pool* out);
+dx_status dx_pool_destroy(dx_pool pool);
+dx_status dx_pool_info(dx_pool pool, dx_info* out);
+
+/* ---------------------------------------------------------------- the MoE layer (Eq. 1) */
+
+/* y = sum_{j in topk} g_j(x) E_j(x) for T tokens of one layer, each expert
+ * read at its last stable version and tier.
+ *   x_bf16      [T][H] bf16, device.
+ *   router_w    [E][H] bf16, device, and router_bias [E] fp32 (may be NULL): router mode,
+ *               logits = x W_r^T + b in fp32 (the router stays full precision);
+ *   logits      [T][E] fp32, device: trace mode (router_w must be NULL).  Exactly one of the two.
+ *   y_bf16      [T][H] bf16, device (output).
+ *   topk_idx    [T][k] int32 and topk_gate [T][k] fp32, device, optional outputs.
+ * Also accumulates the hotness counters cnt/mass of the layer.
+ * 0 <= T <= max_tokens; T = 0 is a no-op.  Asynchronous on the compute stream. */
+dx_status dx_moe_forward(dx_pool pool, int32_t layer, const void* x_bf16, int32_t T,
+                         const void* router_w_bf16, const float* router_bias, const float* logits,
+                         void* y_bf16, int32_t* topk_idx, float* topk_gate);
+
+/* Fold the counters accumulated since the last fold into the EMA scores (Eq. 2, PAPER.md:226,
+ * with Alg. 1's passive decay, R-H2); step t += 1; publish transitions due at the new t (R-T1).
+ * Asynchronous on the compute stream (waits on the side stream only when a publish is due). */
+dx_status dx_hotness_update(dx_pool pool, int32_t layer);
+/* Trace mode: accumulate counters from given routing (device idx [T][k] int32 global expert ids,
+ * gate [T][k] fp32; B_tot = T) and fold.  INVALID_ARG on a duplicate expert within a token. */
+dx_status dx_hotness_update_from(dx_pool pool, int32_t layer, const int32_t* topk_idx,
+                                 const float* topk_gate, int32_t T);
+
+/* Alg. 1 PrecisionSchedule at the current step t of `layer`:
+ *  t == W: finalize the warm-up (tau_h, initial HIGH set, synchronous relayout, R-P3);
+ *  t > W, t ≡ 0 mod Tp: compute the plan on the device (R-C1..C4), reserve destination blocks and
+ *  issue promotions (H2D of the HIGH image) and demotions (on-device group quantisation) on the
+ *  side stream; they become stable at t + L.
+ * out == NULL: fully asynchronous.  out != NULL: synchronises and reports the plan (tests). */
+dx_status dx_plan_precision(dx_pool pool, int32_t layer, dx_plan* out);
+
+/* Manual commands (EnqueueUpgrade / EnqueueDowngrade for host-chosen experts), issued like a plan.
+ * Per expert: RANGE, NOT_READY (before warm-up end), INVALID_ARG (already at that tier),
+ * BUSY (in flight), POOL_EXHAUSTED (no free block: deferred, nothing issued).  Synchronising. */
+dx_status dx_promote(dx_pool pool, int32_t layer, const int32_t* experts, int32_t n);
+dx_status dx_demote(dx_pool pool, int32_t layer, const int32_t* experts, int32_t n);
+
+/* Wait for all compute- and side-stream work of the pool (does not move the publish schedule). */
+dx_status dx_sync(dx_pool pool);
+
+/* ---------------------------------------------------------------- inspection (synchronising) */
+dx_status dx_query_expert(dx_pool pool, int32_t layer, int32_t e, int32_t* tier, int32_t* slot,
+                          uint32_t* version, int32_t* in_flight);
+/* Bulk table: arrays of E_loc entries each (any may be NULL).  tier: 1 HIGH 0 LOW;
+ * in_flight: +1/-1 pending direction, 0 none. */
+dx_status dx_get_table(dx_pool pool, int32_t layer, int32_t* tier, int32_t* slot, uint32_t* version,
+                       int32_t* in_flight);
+dx_status dx_occupancy(dx_pool pool, int32_t layer, int32_t* used_hi, int32_t* cap_hi,
+                       int32_t* used_lo, int32_t* cap_lo);
+/* S[E_loc] fp64 scores, cnt/mass[E_loc] counters not yet folded, tau_h, n_hot, t. */
+dx_status dx_get_hotness(dx_pool pool, int32_t layer, double* S, uint32_t* cnt, uint64_t* mass,
+                         double* tau_h, int32_t* n_hot, int64_t* step);
+/* Canonical image of expert e at its stable tier into host memory (DESIGN.md R-Q1 export):
+ * bf16 tier: 3*I*H bf16 (master layout); quantised tier: codes u8 [3*I*H] unpacked | scales bf16
+ * [3*I*H/g] | zeros u8 [3*I*H/g], matrices in the order gate, up, down. */
+dx_status dx_export_expert(dx_pool pool, int32_t layer, int32_t e, void* host_out, int64_t cap_bytes,
+                           int64_t* written);
+
+/* ---------------------------------------------------------------- standalone group quantiser */
+/* On-device group quantisation of a bf16 matrix [N][K] (row-major, groups of g along K), R-Q1:
+ * codes packed little-endian along K (int4: c[k] | c[k+1]<<4; int2: 4 per byte), scales bf16
+ * [N][K/g], zeros u8 [N][K/g].  All device pointers; asynchronous on `stream`. */
+dx_status dx_quantize(const void* w_bf16, int64_t N, int64_t K, int32_t g, int32_t bits,
+                      void* codes_packed, void* scales_bf16, void* zeros_u8, void* stream);
+/* w_hat = bf16_rn((q - z) * s) into w_bf16 [N][K]. */
+dx_status dx_dequantize(const void* codes_packed, const void* scales_bf16, const void* zeros_u8,
+                        int64_t N, int64_t K, int32_t g, int32_t bits, void* w_bf16, void* stream);
+
+/* Sizes in bytes of one expert slot at `bits` (R-P1), and the per-layer n_hot (R-P2); -1 if infeasible. */
+int64_t dx_slot_bytes(int32_t H, int32_t I, int32_t g, int32_t bits);
+int64_t dx_solve_n_hot(int64_t layer_budget, int32_t n_experts, int64_t S_h, int64_t S_l, int32_t n_spare);
+
+/* ---------------------------------------------------------------- profiling for benches */
+typedef struct {
+    int64_t  forwards;          /* dx_moe_forward calls (T > 0) since the last read */
+    double   fwd_ms;            /* summed device time of whole forwards (CUDA events on the compute stream) */
+    double   ffn_ms[2];         /* summed device time of the gate/up (0) and down (1) expert kernels */
+    uint64_t weight_bytes[2];   /* algorithmic expert-weight bytes those kernels must read: every touched
+                                   expert's gate+up (0) / down (1) codes+scales+zeros at its stable tier */
+    uint64_t active_experts;    /* touched experts summed over forwards */
+} dx_profile_t;
+/* Enable/disable per-forward CUDA-event timing (weight-byte counters always run, on the device). */
+dx_status dx_profile_enable(dx_pool pool, int32_t enable);
+/* Synchronising; returns and resets the accumulated profile. */
+dx_status dx_profile_read(dx_pool pool, dx_profile_t* out);
+
+/* Number of kernels this library launched since pool creation (all streams). */
+int64_t dx_kernel_launches(dx_pool pool);
+const char* dx_last_error(void);
+const char* dx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

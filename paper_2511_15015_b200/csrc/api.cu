@@ -1,0 +1,734 @@
+// api.cu -- the C ABI (include/dx.h): pool lifecycle, the MoE layer forward, the controller
+// schedule and inspection.  Host logic only; all arithmetic of the path runs in the kernels.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+#include <cmath>
+#include <cuda_runtime.h>
+#include "dx_common.cuh"
+
+void launch_manual(const Ctrl& c, int layer, const int2* cmds, int n, int32_t* status, cudaStream_t st);
+
+static thread_local char g_err[1024] = "";
+void dx_set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+extern "C" const char* dx_last_error(void) { return g_err; }
+extern "C" const char* dx_version(void) { return "dynaexq-b200 0.1 (sm_100a)"; }
+
+#define DX_CHECK(cond, code, ...)      \
+    do {                               \
+        if (!(cond)) {                 \
+            dx_set_error(__VA_ARGS__); \
+            return code;               \
+        }                              \
+    } while (0)
+
+struct dx_pool_s {
+    dx_config cfg;
+    dx_info info;
+    int E, E_loc, e_lo, L, k, H, I, g;
+    SlotLayout hi, lo;
+    i64 layer_bytes, hi_base;
+    uint8_t* arena = nullptr;
+    uint8_t* weights = nullptr;
+    Ctrl ctrl;
+    RouteWs ws;
+    __nv_bfloat16* act = nullptr;
+    __nv_bfloat16* Y = nullptr;
+    int32_t* err_flag = nullptr;
+    int2* manual_cmds = nullptr;
+    int32_t* manual_status = nullptr;
+    const uint8_t** hi_img_dev = nullptr;   // [L * E_loc]
+    std::vector<const uint8_t*> hi_img_host;
+    uint8_t* hi_cache = nullptr;            // library-owned pinned HIGH images when high_bits < 16
+    cudaStream_t cs = nullptr, ss = nullptr;
+    bool own_ss = false;
+    std::vector<i64> t;                     // host mirror of the fold count per layer
+    std::vector<i64> publish_at;            // -1 none
+    std::vector<u64> pend_tokens;
+    std::vector<int> finalized;
+    std::vector<cudaEvent_t> ev_side;
+    cudaEvent_t ev_plan = nullptr;
+    i64 launches = 0;
+    u64 wbytes[2][2];                       // [tier][phase] algorithmic weight bytes per expert
+    bool profiling = false;
+    std::vector<cudaEvent_t> prof_ev;       // 4 per forward: start, after routing, between FFN phases, end
+    std::vector<cudaEvent_t> prof_free;
+    i64 prof_fwd = 0;
+};
+
+static u64 phase_bytes(const SlotLayout& L, int H, int I, int g, int nmat) {
+    const u64 n = (u64)I * H;
+    if (L.bits == 16) return nmat * n * 2;
+    return nmat * (n * L.bits / 8 + n / g * 3);
+}
+
+static int64_t slot_bytes_impl(int H, int I, int g, int bits) { return dx_slot_layout(H, I, g, bits).bytes; }
+
+extern "C" int64_t dx_slot_bytes(int32_t H, int32_t I, int32_t g, int32_t bits) {
+    if (H <= 0 || I <= 0 || g <= 0 || (bits != 16 && bits != 4 && bits != 2)) return -1;
+    return slot_bytes_impl(H, I, g, bits);
+}
+
+extern "C" int64_t dx_solve_n_hot(int64_t M, int32_t N, int64_t S_h, int64_t S_l, int32_t s) {
+    // largest n_hot with (n_hot+s) S_h + (N-n_hot+s) S_l <= M  (R-P2)
+    const int64_t num = M - (int64_t)N * S_l - (int64_t)s * (S_h + S_l);
+    if (num < 0 || S_h <= S_l) return -1;
+    const int64_t n = num / (S_h - S_l);
+    return n < N ? n : N;
+}
+
+template <typename T>
+static T* carve(uint8_t*& p, size_t count) {
+    uintptr_t a = ((uintptr_t)p + 255) & ~(uintptr_t)255;
+    T* r = reinterpret_cast<T*>(a);
+    p = reinterpret_cast<uint8_t*>(a + count * sizeof(T));
+    return r;
+}
+
+static dx_status validate(const dx_config* c) {
+    DX_CHECK(c, DX_ERR_INVALID_ARG, "null config");
+    DX_CHECK(c->num_layers >= 1 && c->num_experts >= 1, DX_ERR_INVALID_ARG, "num_layers/num_experts must be >= 1");
+    DX_CHECK(c->top_k >= 1 && c->top_k <= c->num_experts && c->top_k <= 16, DX_ERR_INVALID_ARG,
+             "top_k must be in [1, min(E, 16)]");
+    DX_CHECK(c->group_size == 32 || c->group_size == 64 || c->group_size == 128, DX_ERR_INVALID_ARG,
+             "group_size must be 32, 64 or 128");
+    DX_CHECK(c->hidden % 64 == 0 && c->inter % 64 == 0 && c->hidden % c->group_size == 0 &&
+             c->inter % c->group_size == 0 && c->hidden > 0 && c->inter > 0,
+             DX_ERR_INVALID_ARG, "hidden/inter must be positive multiples of 64 and of group_size");
+    DX_CHECK((c->high_bits == 16 && (c->low_bits == 4 || c->low_bits == 2)) || (c->high_bits == 4 && c->low_bits == 2),
+             DX_ERR_INVALID_ARG, "precision pair must be (16,4), (16,2) or (4,2)");
+    DX_CHECK(c->ema_alpha > 0.0 && c->ema_alpha < 1.0, DX_ERR_INVALID_ARG, "ema_alpha in (0,1)");
+    DX_CHECK(c->period >= 1 && c->warmup_steps >= 0 && c->dwell_min >= 0 && c->n_spare >= 0, DX_ERR_INVALID_ARG,
+             "period >= 1, warmup >= 0, dwell >= 0, n_spare >= 0");
+    DX_CHECK(c->publish_lag >= 1 && c->publish_lag < c->period, DX_ERR_INVALID_ARG, "1 <= publish_lag < period");
+    DX_CHECK(c->max_tokens >= 1, DX_ERR_INVALID_ARG, "max_tokens >= 1");
+    DX_CHECK(c->ep_size == 1 && c->ep_rank == 0, DX_ERR_INVALID_ARG,
+             "expert parallelism (ep_size > 1) is not available in this build");
+    DX_CHECK(c->num_experts <= 512 && c->num_experts + c->n_spare <= 1024, DX_ERR_INVALID_ARG,
+             "experts per GPU must be <= 512");
+    return DX_OK;
+}
+
+extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* master, void* compute_stream,
+                                    void* side_stream, dx_pool* out) {
+    dx_status st = validate(cfg);
+    if (st != DX_OK) return st;
+    DX_CHECK(master && out, DX_ERR_INVALID_ARG, "null master/out");
+    dx_pool p = new dx_pool_s();
+    p->cfg = *cfg;
+    p->L = cfg->num_layers;
+    p->E = cfg->num_experts;
+    p->E_loc = cfg->num_experts / cfg->ep_size;
+    p->e_lo = cfg->ep_rank * p->E_loc;
+    p->k = cfg->top_k;
+    p->H = cfg->hidden;
+    p->I = cfg->inter;
+    p->g = cfg->group_size;
+    p->hi = dx_slot_layout(p->H, p->I, p->g, cfg->high_bits);
+    p->lo = dx_slot_layout(p->H, p->I, p->g, cfg->low_bits);
+    const int E = p->E_loc, s = cfg->n_spare;
+    const i64 M = (i64)(cfg->expert_budget_bytes / (uint64_t)cfg->num_layers);
+    const i64 n_hot = dx_solve_n_hot(M, E, p->hi.bytes, p->lo.bytes, s);
+    if (n_hot < 0) {
+        dx_set_error("infeasible budget: per-layer %lld B < (N+s)*S_l + s*S_h = %lld B", (long long)M,
+                     (long long)((E + s) * p->lo.bytes + s * p->hi.bytes));
+        delete p;
+        return DX_ERR_INFEASIBLE_BUDGET;
+    }
+    const int cap_lo = E - (int)n_hot + s, cap_hi = (int)n_hot + s;
+    p->hi_base = (i64)cap_lo * p->lo.bytes;
+    i64 lb = p->hi_base + (i64)cap_hi * p->hi.bytes;
+    if ((i64)E * p->lo.bytes > lb) lb = (i64)E * p->lo.bytes;   // warm-up layout (R-P3)
+    p->layer_bytes = dx_up(lb, 1024);
+
+    // ---- the one device allocation: weights | controller | workspace | staging
+    const int T = cfg->max_tokens, k = p->k, L = p->L;
+    const int nblk = route_blocks(T);
+    const size_t Ek = (size_t)E;
+    size_t ctrl_bytes = 0;
+    {
+        const size_t LE = (size_t)L * Ek, LO = (size_t)L * (Ek + s);
+        ctrl_bytes = LE * (4 + 4 + 4 + 8 + 4 + 8 + 8 + 4 + 4 + 8 + 16) + LO * 8 + L * (8 + 8 + 4 * 3) + 64 * 256;
+    }
+    const size_t ws_bytes = (size_t)T * p->E * 4 + (size_t)T * k * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
+                            (size_t)(p->E + 1) * 8 + (size_t)T * k * (p->I + p->H) * 2 + 64 * 256 + 4096 * 8;
+    const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
+    const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
+    const size_t total = (size_t)L * p->layer_bytes + ctrl_bytes + ws_bytes + stage_bytes + ptr_bytes + 4096;
+    cudaError_t ce = cudaMalloc(&p->arena, total);
+    if (ce != cudaSuccess) {
+        dx_set_error("cudaMalloc(%zu) failed: %s", total, cudaGetErrorString(ce));
+        delete p;
+        return DX_ERR_OOM;
+    }
+    uint8_t* q = p->arena;
+    p->weights = q;
+    q += (size_t)L * p->layer_bytes;
+    Ctrl& c = p->ctrl;
+    const size_t LE = (size_t)L * E, LO = (size_t)L * (E + s);
+    c.tier = carve<int32_t>(q, LE);
+    c.slot = carve<int32_t>(q, LE);
+    c.version = carve<uint32_t>(q, LE);
+    c.S = carve<double>(q, LE);
+    c.cnt = carve<uint32_t>(q, LE);
+    c.mass = carve<u64>(q, LE);
+    c.last = carve<i64>(q, LE);
+    c.pend_dir = carve<int32_t>(q, LE);
+    c.pend_dst = carve<int32_t>(q, LE);
+    c.pend_at = carve<i64>(q, LE);
+    c.plan_cmd = carve<int4>(q, LE);
+    c.lo_owner = carve<int32_t>(q, LO);
+    c.hi_owner = carve<int32_t>(q, LO);
+    c.t = carve<i64>(q, L);
+    c.tau = carve<double>(q, L);
+    c.cap_lo = carve<int32_t>(q, L);
+    c.cap_hi = carve<int32_t>(q, L);
+    c.plan_n = carve<int32_t>(q, L);
+    c.E = E; c.s = s; c.n_hot = (int)n_hot; c.W = cfg->warmup_steps; c.Tp = cfg->period;
+    c.dwell = cfg->dwell_min; c.lag = cfg->publish_lag; c.alpha = cfg->ema_alpha;
+    RouteWs& w = p->ws;
+    w.logits = carve<float>(q, (size_t)T * p->E);
+    w.idx = carve<int32_t>(q, (size_t)T * k);
+    w.gate = carve<float>(q, (size_t)T * k);
+    w.hist = carve<int32_t>(q, (size_t)nblk * p->E);
+    w.base = carve<int32_t>(q, (size_t)nblk * p->E);
+    w.off = carve<int32_t>(q, p->E + 1);
+    w.act_e = carve<int32_t>(q, p->E);
+    w.n_act = carve<int32_t>(q, 1);
+    w.perm = carve<int32_t>(q, (size_t)T * k);
+    w.inv = carve<int32_t>(q, (size_t)T * k);
+    w.stats = carve<u64>(q, 4);
+    p->act = carve<__nv_bfloat16>(q, (size_t)T * k * p->I);
+    p->Y = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
+    p->err_flag = carve<int32_t>(q, 1);
+    p->manual_cmds = carve<int2>(q, 1024);
+    p->manual_status = carve<int32_t>(q, 1024);
+    uint8_t* stage_master = carve<uint8_t>(q, (size_t)3 * p->I * p->H * 2);
+    uint8_t* stage_high = carve<uint8_t>(q, (size_t)p->hi.bytes);
+    p->hi_img_dev = carve<const uint8_t*>(q, (size_t)L * E);
+    if ((size_t)(q - p->arena) > total) {
+        dx_set_error("internal: arena carve overflow");
+        cudaFree(p->arena);
+        delete p;
+        return DX_ERR_OOM;
+    }
+
+    // ---- streams / events
+    p->cs = (cudaStream_t)compute_stream;
+    if (side_stream) {
+        p->ss = (cudaStream_t)side_stream;
+    } else {
+        int lo_prio, hi_prio;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        cudaStreamCreateWithPriority(&p->ss, cudaStreamNonBlocking, lo_prio);
+        p->own_ss = true;
+    }
+    cudaEventCreateWithFlags(&p->ev_plan, cudaEventDisableTiming);
+    p->ev_side.resize(L);
+    for (int l = 0; l < L; ++l) cudaEventCreateWithFlags(&p->ev_side[l], cudaEventDisableTiming);
+    p->t.assign(L, 0);
+    p->publish_at.assign(L, -1);
+    p->pend_tokens.assign(L, 0);
+    p->finalized.assign(L, 0);
+
+    auto fail = [&](dx_status code) {
+        dx_pool_destroy(p);
+        return code;
+    };
+
+    // ---- HIGH image sources (the DRAM cache)
+    p->hi_img_host.resize((size_t)L * E);
+    if (cfg->high_bits < 16) {
+        ce = cudaHostAlloc((void**)&p->hi_cache, (size_t)L * E * p->hi.bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (ce != cudaSuccess) { dx_set_error("cudaHostAlloc HIGH cache: %s", cudaGetErrorString(ce)); return fail(DX_ERR_OOM); }
+    }
+    std::vector<const uint8_t*> img_dev((size_t)L * E);
+    for (int l = 0; l < L; ++l)
+        for (int e = 0; e < E; ++e) {
+            const void* m = master[(size_t)l * E + e];
+            if (!m) { dx_set_error("null master pointer (layer %d expert %d)", l, e); return fail(DX_ERR_INVALID_ARG); }
+            const uint8_t* src_host;
+            if (cfg->high_bits == 16) src_host = (const uint8_t*)m;
+            else src_host = p->hi_cache + ((size_t)l * E + e) * p->hi.bytes;
+            cudaPointerAttributes at;
+            ce = cudaPointerGetAttributes(&at, src_host);
+            if (ce != cudaSuccess || at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) {
+                cudaGetLastError();
+                dx_set_error("master image of layer %d expert %d is not pinned/mapped host memory", l, e);
+                return fail(DX_ERR_INVALID_ARG);
+            }
+            p->hi_img_host[(size_t)l * E + e] = src_host;
+            img_dev[(size_t)l * E + e] = (const uint8_t*)at.devicePointer;
+        }
+    DX_CUDA(cudaMemcpyAsync(p->hi_img_dev, img_dev.data(), img_dev.size() * sizeof(void*), cudaMemcpyHostToDevice, p->cs));
+
+    // ---- controller initial state: warm-up layout, all LOW, expert e in LOW block e (R-P3)
+    {
+        std::vector<int32_t> tier(LE, 0), slot(LE), pend(LE, 0), own_lo(LO, -1), own_hi(LO, -1);
+        std::vector<uint32_t> ver(LE, 0);
+        std::vector<double> S(LE, 0.0);
+        std::vector<i64> last(LE, DX_NEVER), at(LE, 0), tt(L, 0);
+        std::vector<double> tau(L, INFINITY);
+        std::vector<int32_t> clo(L, E), chi(L, 0), pn(L, 0);
+        for (int l = 0; l < L; ++l)
+            for (int e = 0; e < E; ++e) { slot[(size_t)l * E + e] = e; own_lo[(size_t)l * (E + s) + e] = e; }
+        DX_CUDA(cudaMemcpyAsync(c.tier, tier.data(), LE * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.slot, slot.data(), LE * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.version, ver.data(), LE * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.S, S.data(), LE * 8, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemsetAsync(c.cnt, 0, LE * 4, p->cs));
+        DX_CUDA(cudaMemsetAsync(c.mass, 0, LE * 8, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.last, last.data(), LE * 8, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.pend_dir, pend.data(), LE * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.pend_dst, pend.data(), LE * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.pend_at, at.data(), LE * 8, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.lo_owner, own_lo.data(), LO * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.hi_owner, own_hi.data(), LO * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.t, tt.data(), L * 8, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.tau, tau.data(), L * 8, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.cap_lo, clo.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.cap_hi, chi.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemcpyAsync(c.plan_n, pn.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
+        DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
+        DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
+        DX_CUDA(cudaStreamSynchronize(p->cs));
+    }
+    for (int ti = 0; ti < 2; ++ti) {
+        const SlotLayout& Ls = ti ? p->hi : p->lo;
+        p->wbytes[ti][0] = phase_bytes(Ls, p->H, p->I, p->g, 2);
+        p->wbytes[ti][1] = phase_bytes(Ls, p->H, p->I, p->g, 1);
+    }
+
+    // ---- initial images: LOW block e of every expert (and the HIGH image cache if quantised)
+    const size_t mbytes = (size_t)3 * p->I * p->H * 2;
+    SlotLayout bf = dx_slot_layout(p->H, p->I, p->g, 16);
+    for (int l = 0; l < L; ++l)
+        for (int e = 0; e < E; ++e) {
+            DX_CUDA(cudaMemcpyAsync(stage_master, master[(size_t)l * E + e], mbytes, cudaMemcpyHostToDevice, p->cs));
+            uint8_t* low = p->weights + (size_t)l * p->layer_bytes + (size_t)e * p->lo.bytes;
+            if (cfg->high_bits == 16) {
+                launch_quantize_slot(stage_master, bf, low, p->lo, p->H, p->I, p->g, p->cs);
+            } else {
+                launch_quantize_slot(stage_master, bf, stage_high, p->hi, p->H, p->I, p->g, p->cs);
+                DX_CUDA(cudaMemcpyAsync(p->hi_cache + ((size_t)l * E + e) * p->hi.bytes, stage_high, p->hi.bytes,
+                                        cudaMemcpyDeviceToHost, p->cs));
+                launch_quantize_slot(stage_high, p->hi, low, p->lo, p->H, p->I, p->g, p->cs);
+            }
+            p->launches += cfg->high_bits == 16 ? 3 : 6;
+        }
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    DX_CUDA(cudaGetLastError());
+
+    dx_info& inf = p->info;
+    inf.n_hot = (int)n_hot;
+    inf.experts_local = E;
+    inf.cap_hi = cap_hi;
+    inf.cap_lo = cap_lo;
+    inf.slot_bytes_hi = p->hi.bytes;
+    inf.slot_bytes_lo = p->lo.bytes;
+    inf.layer_budget = M;
+    inf.layer_bytes = p->layer_bytes;
+    inf.arena_bytes = (i64)total;
+    const i64 n3 = (i64)3 * p->I * p->H;
+    inf.export_bytes_hi = cfg->high_bits == 16 ? n3 * 2 : n3 + n3 / p->g * 3;
+    inf.export_bytes_lo = n3 + n3 / p->g * 3;
+    *out = p;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_pool_destroy(dx_pool p) {
+    if (!p) return DX_OK;
+    if (p->cs) cudaStreamSynchronize(p->cs);
+    if (p->ss) cudaStreamSynchronize(p->ss);
+    for (auto ev : p->ev_side) cudaEventDestroy(ev);
+    if (p->ev_plan) cudaEventDestroy(p->ev_plan);
+    if (p->own_ss && p->ss) cudaStreamDestroy(p->ss);
+    for (auto ev : p->prof_ev) cudaEventDestroy(ev);
+    for (auto ev : p->prof_free) cudaEventDestroy(ev);
+    if (p->hi_cache) cudaFreeHost(p->hi_cache);
+    if (p->arena) cudaFree(p->arena);
+    delete p;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_pool_info(dx_pool p, dx_info* out) {
+    DX_CHECK(p && out, DX_ERR_INVALID_ARG, "null pool/out");
+    *out = p->info;
+    return DX_OK;
+}
+
+extern "C" int64_t dx_kernel_launches(dx_pool p) { return p ? p->launches : 0; }
+
+extern "C" dx_status dx_profile_enable(dx_pool p, int32_t enable) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    p->profiling = enable != 0;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
+    DX_CHECK(p && out, DX_ERR_INVALID_ARG, "null pool/out");
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    memset(out, 0, sizeof(*out));
+    for (size_t i = 0; i + 3 < p->prof_ev.size(); i += 4) {
+        float a = 0, b = 0, c = 0, d = 0;
+        DX_CUDA(cudaEventElapsedTime(&a, p->prof_ev[i], p->prof_ev[i + 3]));
+        DX_CUDA(cudaEventElapsedTime(&b, p->prof_ev[i + 1], p->prof_ev[i + 2]));
+        DX_CUDA(cudaEventElapsedTime(&c, p->prof_ev[i + 2], p->prof_ev[i + 3]));
+        (void)d;
+        out->fwd_ms += a;
+        out->ffn_ms[0] += b;
+        out->ffn_ms[1] += c;
+    }
+    for (auto e : p->prof_ev) p->prof_free.push_back(e);
+    p->prof_ev.clear();
+    out->forwards = p->prof_fwd;
+    p->prof_fwd = 0;
+    u64 st[4];
+    DX_CUDA(cudaMemcpy(st, p->ws.stats, sizeof(st), cudaMemcpyDeviceToHost));
+    DX_CUDA(cudaMemset(p->ws.stats, 0, sizeof(st)));
+    out->weight_bytes[0] = st[0];
+    out->weight_bytes[1] = st[1];
+    out->active_experts = st[2];
+    return DX_OK;
+}
+
+#define CHECK_LAYER(p, layer)                                                                          \
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");                                                      \
+    DX_CHECK((layer) >= 0 && (layer) < (p)->L, DX_ERR_RANGE, "layer %d out of range [0,%d)", (int)(layer), (p)->L)
+
+extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
+                                    const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
+                                    float* topk_gate) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(T >= 0 && T <= p->cfg.max_tokens, DX_ERR_RANGE, "T=%d outside [0, max_tokens=%d]", T, p->cfg.max_tokens);
+    if (T == 0) return DX_OK;
+    DX_CHECK(x && y, DX_ERR_INVALID_ARG, "null x/y");
+    DX_CHECK((router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG,
+             "exactly one of router_w (router mode) and logits (trace mode) must be given");
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (p->profiling) {
+        for (int i = 0; i < 4; ++i) {
+            if (p->prof_free.empty()) {
+                cudaEvent_t e;
+                DX_CUDA(cudaEventCreate(&e));
+                p->prof_free.push_back(e);
+            }
+            ev[i] = p->prof_free.back();
+            p->prof_free.pop_back();
+            p->prof_ev.push_back(ev[i]);
+        }
+        DX_CUDA(cudaEventRecord(ev[0], p->cs));
+        p->prof_fwd += 1;
+    }
+    RouteWs ws = p->ws;
+    if (topk_idx) ws.idx = topk_idx;
+    if (topk_gate) ws.gate = topk_gate;
+    const float* lg = logits;
+    if (router_w) {
+        launch_router((const __nv_bfloat16*)x, (const __nv_bfloat16*)router_w, router_bias, T, p->E, p->H,
+                      ws.logits, p->cs);
+        lg = ws.logits;
+        p->launches += 1;
+    }
+    const size_t base = (size_t)layer * p->E_loc;
+    launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->cs);
+    launch_scan_scatter(T, p->E, p->k, ws, p->ctrl.tier + base, p->wbytes, p->cs);
+    ExpertArgs a;
+    a.arena_layer = p->weights + (size_t)layer * p->layer_bytes;
+    a.tier = p->ctrl.tier + base;
+    a.slot = p->ctrl.slot + base;
+    a.hi_base = p->hi_base;
+    a.hi = p->hi;
+    a.lo = p->lo;
+    a.H = p->H; a.I = p->I; a.g = p->g; a.k = p->k;
+    if (ev[1]) DX_CUDA(cudaEventRecord(ev[1], p->cs));
+    launch_expert_ffn(a, (const __nv_bfloat16*)x, ws.gate, ws, T, p->E, p->act, p->Y, p->cs, ev[2]);
+    if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));
+    launch_combine(p->Y, T, p->k, p->H, (__nv_bfloat16*)y, p->cs);
+    p->launches += 6;
+    p->pend_tokens[layer] += (u64)T;
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+static dx_status fold(dx_pool p, int layer) {
+    const u64 B = p->pend_tokens[layer];
+    p->pend_tokens[layer] = 0;
+    const i64 t_new = p->t[layer] + 1;
+    if (p->publish_at[layer] == t_new) {
+        // exposed switch time, if any, is spent here: registration waits for the side stream
+        DX_CUDA(cudaStreamWaitEvent(p->cs, p->ev_side[layer], 0));
+        p->publish_at[layer] = -1;
+    }
+    launch_fold(p->ctrl, layer, B, p->cs);
+    p->launches += 1;
+    p->t[layer] = t_new;
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "fold launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+extern "C" dx_status dx_hotness_update(dx_pool p, int32_t layer) {
+    CHECK_LAYER(p, layer);
+    return fold(p, layer);
+}
+
+extern "C" dx_status dx_hotness_update_from(dx_pool p, int32_t layer, const int32_t* idx, const float* gate,
+                                            int32_t T) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(T >= 0 && (T == 0 || (idx && gate)), DX_ERR_INVALID_ARG, "bad idx/gate");
+    const size_t base = (size_t)layer * p->E_loc;
+    if (T > 0) {
+        DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
+        launch_counts_from(idx, gate, T, p->E, p->k, p->e_lo, p->ctrl.cnt + base, p->ctrl.mass + base, p->err_flag, p->cs);
+        p->launches += 1;
+        int32_t err = 0;
+        DX_CUDA(cudaMemcpyAsync(&err, p->err_flag, 4, cudaMemcpyDeviceToHost, p->cs));
+        DX_CUDA(cudaStreamSynchronize(p->cs));
+        DX_CHECK(err == 0, err == 1 ? DX_ERR_INVALID_ARG : DX_ERR_RANGE,
+                 err == 1 ? "duplicate expert within one token (SPEC.md:144)" : "expert id out of range");
+    }
+    p->pend_tokens[layer] += (u64)T;
+    return fold(p, layer);
+}
+
+static XferArgs xfer_args(dx_pool p, int layer) {
+    XferArgs x;
+    x.layer_base = p->weights + (size_t)layer * p->layer_bytes;
+    x.hi_base = p->hi_base;
+    x.hi = p->hi;
+    x.lo = p->lo;
+    x.hi_img = p->hi_img_dev + (size_t)layer * p->E_loc;
+    x.H = p->H; x.I = p->I; x.g = p->g;
+    return x;
+}
+
+static dx_status read_plan(dx_pool p, int layer, dx_plan* out) {
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    int32_t n = 0;
+    DX_CUDA(cudaMemcpy(&n, p->ctrl.plan_n + layer, 4, cudaMemcpyDeviceToHost));
+    std::vector<int4> cmds(n > 0 ? n : 1);
+    if (n > 0) DX_CUDA(cudaMemcpy(cmds.data(), p->ctrl.plan_cmd + (size_t)layer * p->E_loc, n * sizeof(int4), cudaMemcpyDeviceToHost));
+    out->n = n < DX_MAX_CMDS ? n : DX_MAX_CMDS;
+    for (int i = 0; i < out->n; ++i) {
+        out->cmd[i].expert = cmds[i].x;
+        out->cmd[i].dir = cmds[i].y;
+        out->cmd[i].dst_slot = cmds[i].z;
+        out->cmd[i].src_slot = cmds[i].w;
+    }
+    return DX_OK;
+}
+
+extern "C" dx_status dx_plan_precision(dx_pool p, int32_t layer, dx_plan* out) {
+    CHECK_LAYER(p, layer);
+    const i64 t = p->t[layer];
+    const dx_config& c = p->cfg;
+    if (out) { out->due = 0; out->finalize = 0; out->n = 0; out->step = t; out->publish_step = t; }
+    if (!p->finalized[layer] && t == c.warmup_steps) {
+        // §3.5: tau_h and the initial HIGH set, installed synchronously before serving continues
+        launch_plan(p->ctrl, layer, 1, p->cs);
+        launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 1, p->cs);
+        launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 2, p->cs);
+        p->launches += 3;
+        p->finalized[layer] = 1;
+        if (out) {
+            out->due = 1; out->finalize = 1;
+            dx_status st = read_plan(p, layer, out);
+            if (st != DX_OK) return st;
+        }
+        cudaError_t ce = cudaGetLastError();
+        DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "finalize launch failed: %s", cudaGetErrorString(ce));
+        return DX_OK;
+    }
+    if (!p->finalized[layer] || t <= c.warmup_steps || t % c.period != 0 || p->publish_at[layer] >= 0) return DX_OK;
+    launch_plan(p->ctrl, layer, 0, p->cs);
+    DX_CUDA(cudaEventRecord(p->ev_plan, p->cs));
+    DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_plan, 0));
+    launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 0, p->ss);
+    DX_CUDA(cudaEventRecord(p->ev_side[layer], p->ss));
+    p->launches += 2;
+    p->publish_at[layer] = t + c.publish_lag;
+    if (out) {
+        out->due = 1;
+        out->publish_step = t + c.publish_lag;
+        dx_status st = read_plan(p, layer, out);
+        if (st != DX_OK) return st;
+    }
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "plan launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+static dx_status manual(dx_pool p, int layer, const int32_t* experts, int n, int dir) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(n >= 0 && n <= 1024 && (n == 0 || experts), DX_ERR_INVALID_ARG, "bad expert list");
+    if (n == 0) return DX_OK;
+    DX_CHECK(p->finalized[layer], DX_ERR_NOT_READY, "warm-up of layer %d not finished", layer);
+    const i64 due = p->t[layer] + p->cfg.publish_lag;
+    DX_CHECK(p->publish_at[layer] < 0 || p->publish_at[layer] == due, DX_ERR_BUSY,
+             "layer %d has transitions publishing at a different step", layer);
+    std::vector<int2> cmds(n);
+    for (int i = 0; i < n; ++i) cmds[i] = make_int2(experts[i], dir);
+    DX_CUDA(cudaMemcpyAsync(p->manual_cmds, cmds.data(), n * sizeof(int2), cudaMemcpyHostToDevice, p->cs));
+    launch_manual(p->ctrl, layer, p->manual_cmds, n, p->manual_status, p->cs);
+    DX_CUDA(cudaEventRecord(p->ev_plan, p->cs));
+    DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_plan, 0));
+    launch_transitions(p->ctrl, layer, xfer_args(p, layer), n, 0, p->ss);
+    DX_CUDA(cudaEventRecord(p->ev_side[layer], p->ss));
+    p->launches += 2;
+    p->publish_at[layer] = due;
+    std::vector<int32_t> stv(n);
+    DX_CUDA(cudaMemcpyAsync(stv.data(), p->manual_status, n * 4, cudaMemcpyDeviceToHost, p->cs));
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    for (int i = 0; i < n; ++i) {
+        switch (stv[i]) {
+            case 0: break;
+            case 1: dx_set_error("expert %d already at that tier", experts[i]); return DX_ERR_INVALID_ARG;
+            case 2: dx_set_error("expert %d out of range", experts[i]); return DX_ERR_RANGE;
+            case 4: dx_set_error("no free block for expert %d (deferred)", experts[i]); return DX_ERR_POOL_EXHAUSTED;
+            case 5: dx_set_error("expert %d has a transition in flight", experts[i]); return DX_ERR_BUSY;
+            default: return DX_ERR_LEDGER;
+        }
+    }
+    return DX_OK;
+}
+
+extern "C" dx_status dx_promote(dx_pool p, int32_t layer, const int32_t* experts, int32_t n) {
+    return manual(p, layer, experts, n, 1);
+}
+extern "C" dx_status dx_demote(dx_pool p, int32_t layer, const int32_t* experts, int32_t n) {
+    return manual(p, layer, experts, n, -1);
+}
+
+extern "C" dx_status dx_sync(dx_pool p) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    DX_CUDA(cudaStreamSynchronize(p->ss));
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    DX_CUDA(cudaGetLastError());
+    return DX_OK;
+}
+
+extern "C" dx_status dx_get_table(dx_pool p, int32_t layer, int32_t* tier, int32_t* slot, uint32_t* version,
+                                  int32_t* in_flight) {
+    CHECK_LAYER(p, layer);
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    const size_t b = (size_t)layer * p->E_loc, n = p->E_loc;
+    if (tier) DX_CUDA(cudaMemcpy(tier, p->ctrl.tier + b, n * 4, cudaMemcpyDeviceToHost));
+    if (slot) DX_CUDA(cudaMemcpy(slot, p->ctrl.slot + b, n * 4, cudaMemcpyDeviceToHost));
+    if (version) DX_CUDA(cudaMemcpy(version, p->ctrl.version + b, n * 4, cudaMemcpyDeviceToHost));
+    if (in_flight) DX_CUDA(cudaMemcpy(in_flight, p->ctrl.pend_dir + b, n * 4, cudaMemcpyDeviceToHost));
+    return DX_OK;
+}
+
+extern "C" dx_status dx_query_expert(dx_pool p, int32_t layer, int32_t e, int32_t* tier, int32_t* slot,
+                                     uint32_t* version, int32_t* in_flight) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(e >= 0 && e < p->E_loc, DX_ERR_RANGE, "expert %d out of range", e);
+    std::vector<int32_t> tr(p->E_loc), sl(p->E_loc), fl(p->E_loc);
+    std::vector<uint32_t> vr(p->E_loc);
+    dx_status st = dx_get_table(p, layer, tr.data(), sl.data(), vr.data(), fl.data());
+    if (st != DX_OK) return st;
+    if (tier) *tier = tr[e];
+    if (slot) *slot = sl[e];
+    if (version) *version = vr[e];
+    if (in_flight) *in_flight = fl[e];
+    return DX_OK;
+}
+
+extern "C" dx_status dx_occupancy(dx_pool p, int32_t layer, int32_t* used_hi, int32_t* cap_hi, int32_t* used_lo,
+                                  int32_t* cap_lo) {
+    CHECK_LAYER(p, layer);
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    const int n = p->E_loc + p->cfg.n_spare;
+    std::vector<int32_t> lo(n), hi(n);
+    int32_t clo, chi;
+    DX_CUDA(cudaMemcpy(lo.data(), p->ctrl.lo_owner + (size_t)layer * n, n * 4, cudaMemcpyDeviceToHost));
+    DX_CUDA(cudaMemcpy(hi.data(), p->ctrl.hi_owner + (size_t)layer * n, n * 4, cudaMemcpyDeviceToHost));
+    DX_CUDA(cudaMemcpy(&clo, p->ctrl.cap_lo + layer, 4, cudaMemcpyDeviceToHost));
+    DX_CUDA(cudaMemcpy(&chi, p->ctrl.cap_hi + layer, 4, cudaMemcpyDeviceToHost));
+    int uh = 0, ul = 0;
+    for (int i = 0; i < chi; ++i) uh += hi[i] >= 0;
+    for (int i = 0; i < clo; ++i) ul += lo[i] >= 0;
+    if (used_hi) *used_hi = uh;
+    if (cap_hi) *cap_hi = chi;
+    if (used_lo) *used_lo = ul;
+    if (cap_lo) *cap_lo = clo;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_get_hotness(dx_pool p, int32_t layer, double* S, uint32_t* cnt, uint64_t* mass,
+                                    double* tau_h, int32_t* n_hot, int64_t* step) {
+    CHECK_LAYER(p, layer);
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    const size_t b = (size_t)layer * p->E_loc, n = p->E_loc;
+    if (S) DX_CUDA(cudaMemcpy(S, p->ctrl.S + b, n * 8, cudaMemcpyDeviceToHost));
+    if (cnt) DX_CUDA(cudaMemcpy(cnt, p->ctrl.cnt + b, n * 4, cudaMemcpyDeviceToHost));
+    if (mass) DX_CUDA(cudaMemcpy(mass, p->ctrl.mass + b, n * 8, cudaMemcpyDeviceToHost));
+    if (tau_h) DX_CUDA(cudaMemcpy(tau_h, p->ctrl.tau + layer, 8, cudaMemcpyDeviceToHost));
+    if (n_hot) *n_hot = p->info.n_hot;
+    if (step) *step = p->t[layer];
+    return DX_OK;
+}
+
+extern "C" dx_status dx_export_expert(dx_pool p, int32_t layer, int32_t e, void* host_out, int64_t cap,
+                                      int64_t* written) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(e >= 0 && e < p->E_loc, DX_ERR_RANGE, "expert %d out of range", e);
+    DX_CHECK(host_out, DX_ERR_INVALID_ARG, "null output");
+    int32_t tier, slot;
+    dx_status st = dx_query_expert(p, layer, e, &tier, &slot, nullptr, nullptr);
+    if (st != DX_OK) return st;
+    const SlotLayout& Ls = tier ? p->hi : p->lo;
+    const uint8_t* src = p->weights + (size_t)layer * p->layer_bytes + (tier ? p->hi_base + (i64)slot * p->hi.bytes
+                                                                             : (i64)slot * p->lo.bytes);
+    const i64 n = (i64)p->I * p->H, n3 = 3 * n;
+    const i64 need = Ls.bits == 16 ? n3 * 2 : n3 + n3 / p->g * 3;
+    DX_CHECK(cap >= need, DX_ERR_INVALID_ARG, "output buffer too small (%lld < %lld)", (long long)cap, (long long)need);
+    std::vector<uint8_t> img(Ls.bytes);
+    DX_CUDA(cudaMemcpy(img.data(), src, Ls.bytes, cudaMemcpyDeviceToHost));
+    uint8_t* o = (uint8_t*)host_out;
+    if (Ls.bits == 16) {
+        memcpy(o, img.data(), n3 * 2);
+    } else {
+        const int per = 8 / Ls.bits, mask = (1 << Ls.bits) - 1;
+        for (int m = 0; m < 3; ++m) {
+            const uint8_t* codes = img.data() + m * Ls.codes_stride;
+            for (i64 i = 0; i < n; ++i) o[m * n + i] = (codes[i / per] >> ((i % per) * Ls.bits)) & mask;
+            memcpy(o + n3 + m * (n / p->g) * 2, img.data() + Ls.scales_off + m * Ls.scales_stride, (n / p->g) * 2);
+            memcpy(o + n3 + n3 / p->g * 2 + m * (n / p->g), img.data() + Ls.zeros_off + m * Ls.zeros_stride, n / p->g);
+        }
+    }
+    if (written) *written = need;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_quantize(const void* w, int64_t N, int64_t K, int32_t g, int32_t bits, void* codes,
+                                 void* scales, void* zeros, void* stream) {
+    DX_CHECK(w && codes && scales && zeros, DX_ERR_INVALID_ARG, "null pointer");
+    DX_CHECK((g == 32 || g == 64 || g == 128) && K % g == 0 && N >= 0 && (bits == 4 || bits == 2),
+             DX_ERR_INVALID_ARG, "bad shape/bits");
+    launch_quantize(w, 16, nullptr, nullptr, N, K, g, bits, (uint8_t*)codes, (__nv_bfloat16*)scales,
+                    (uint8_t*)zeros, (cudaStream_t)stream);
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "quantize launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+extern "C" dx_status dx_dequantize(const void* codes, const void* scales, const void* zeros, int64_t N, int64_t K,
+                                   int32_t g, int32_t bits, void* w, void* stream) {
+    DX_CHECK(w && codes && scales && zeros, DX_ERR_INVALID_ARG, "null pointer");
+    DX_CHECK((g == 32 || g == 64 || g == 128) && K % g == 0 && K % 8 == 0 && N >= 0 && (bits == 4 || bits == 2),
+             DX_ERR_INVALID_ARG, "bad shape/bits");
+    launch_dequantize((const uint8_t*)codes, (const __nv_bfloat16*)scales, (const uint8_t*)zeros, N, K, g, bits,
+                      (__nv_bfloat16*)w, (cudaStream_t)stream);
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "dequantize launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}

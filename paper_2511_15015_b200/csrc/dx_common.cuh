@@ -1,0 +1,179 @@
+// dx_common.cuh -- shared device/host definitions of the DynaExq B200 library (product code).
+// No code here is shared with oracle/ (the CPU oracle is an independent implementation).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "../../include/dx.h"
+
+#define DX_WARP 32
+#define DX_NUM_SMS 148
+
+typedef unsigned long long u64;
+typedef long long i64;
+
+// ---------------------------------------------------------------- slot layout (DESIGN.md R-P1)
+// Quantised slot of one expert at `bits`: codes gate[I][H*b/8] | up[I][H*b/8] | down[H][I*b/8]
+// | scales (bf16, [rows][K/g]) gate | up | down | zeros (u8) gate | up | down; every sub-array
+// 128 B aligned (the three matrices have I*H elements each, so sub-arrays are equal-sized).
+// bf16 slot: gate[I][H] | up[I][H] | down[H][I].
+struct SlotLayout {
+    int bits;
+    i64 codes_stride;   // bytes per matrix of codes (or bf16 matrix)
+    i64 scales_off, scales_stride;
+    i64 zeros_off, zeros_stride;
+    i64 bytes;          // padded slot size
+};
+
+static inline i64 dx_up(i64 v, i64 a) { return (v + a - 1) / a * a; }
+
+static inline SlotLayout dx_slot_layout(int H, int I, int g, int bits) {
+    SlotLayout s{};
+    s.bits = bits;
+    i64 n = (i64)I * H;
+    if (bits == 16) {
+        s.codes_stride = n * 2;
+        s.scales_off = s.zeros_off = 3 * n * 2;
+        s.scales_stride = s.zeros_stride = 0;
+        s.bytes = dx_up(3 * n * 2, 1024);
+        return s;
+    }
+    s.codes_stride = dx_up(n * bits / 8, 128);
+    s.scales_off = 3 * s.codes_stride;
+    s.scales_stride = dx_up(n / g * 2, 128);
+    s.zeros_off = s.scales_off + 3 * s.scales_stride;
+    s.zeros_stride = dx_up(n / g, 128);
+    s.bytes = dx_up(s.zeros_off + 3 * s.zeros_stride, 1024);
+    return s;
+}
+
+// A matrix view inside a slot: rows x K, at `bits`.
+struct MatView {
+    const uint8_t* codes;     // packed codes, or bf16 data when bits == 16
+    const __nv_bfloat16* scales;
+    const uint8_t* zeros;
+    int bits;
+};
+
+// ---------------------------------------------------------------- controller state (device)
+// Arrays indexed [layer * E + e] (owners: [layer * (E + s) + slot]).
+struct Ctrl {
+    int32_t* tier;         // 1 HIGH, 0 LOW (published / stable)
+    int32_t* slot;         // published block index within the tier region
+    uint32_t* version;
+    double* S;             // EMA hotness (Eq. 2)
+    uint32_t* cnt;         // counters accumulated since the last fold (R-H1)
+    u64* mass;
+    i64* last;             // step of the last transition
+    int32_t* pend_dir;     // +1 / -1 in flight, 0 none
+    int32_t* pend_dst;
+    i64* pend_at;
+    int32_t* lo_owner;     // -1 free, else expert
+    int32_t* hi_owner;
+    i64* t;                // [L] folds done
+    double* tau;           // [L]
+    int32_t* cap_lo;       // [L]
+    int32_t* cap_hi;       // [L]
+    int32_t* plan_n;       // [L]
+    int4* plan_cmd;        // [L * E] (expert, dir, dst, src)
+    int E, s, n_hot, W, Tp, dwell, lag;
+    double alpha;
+};
+
+#define DX_NEVER (-(i64)(1ULL << 61))
+
+// ---------------------------------------------------------------- numerics
+__device__ __forceinline__ float dx_bf2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+
+// dx_expf (DESIGN.md R-G2): every step an IEEE-exact op, no contraction; 2^n applied exactly.
+__device__ __forceinline__ float dx_expf(float x) {
+    if (x < -103.0f) return 0.0f;
+    float n = rintf(__fmul_rn(x, 0x1.715476p+0f));
+    float r = __fmaf_rn(n, -0x1.62e4p-1f, x);
+    r = __fmaf_rn(n, -0x1.7f7d1cp-20f, r);
+    float p = 0x1.a01a02p-13f;            // 1/7!
+    p = __fmaf_rn(p, r, 0x1.6c16c2p-10f); // 1/6!
+    p = __fmaf_rn(p, r, 0x1.111112p-7f);  // 1/5!
+    p = __fmaf_rn(p, r, 0x1.555556p-5f);  // 1/4!
+    p = __fmaf_rn(p, r, 0x1.555556p-3f);  // 1/3!
+    p = __fmaf_rn(p, r, 0.5f);
+    p = __fmaf_rn(p, r, 1.0f);
+    p = __fmaf_rn(p, r, 1.0f);
+    int ni = (int)n;
+    if (ni >= -126) return __fmul_rn(p, __int_as_float((ni + 127) << 23));
+    return __fmul_rn(__fmul_rn(p, 0x1p-64f), __int_as_float((ni + 64 + 127) << 23));
+}
+
+// ---------------------------------------------------------------- host helpers
+struct DxErr;
+void dx_set_error(const char* fmt, ...);
+#define DX_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            dx_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+            return DX_ERR_CUDA;                                                              \
+        }                                                                                    \
+    } while (0)
+
+// ---------------------------------------------------------------- kernel launchers (per file)
+// k_quant.cu
+void launch_quantize(const void* src, int src_bits, const uint8_t* src_scales, const uint8_t* src_zeros,
+                     int64_t N, int64_t K, int g, int bits, uint8_t* codes, __nv_bfloat16* scales,
+                     uint8_t* zeros, cudaStream_t st);
+void launch_dequantize(const uint8_t* codes, const __nv_bfloat16* scales, const uint8_t* zeros,
+                       int64_t N, int64_t K, int g, int bits, __nv_bfloat16* out, cudaStream_t st);
+// quantise all three matrices of a slot image into a slot image of `bits`
+void launch_quantize_slot(const uint8_t* src_slot, const SlotLayout& src, uint8_t* dst_slot,
+                          const SlotLayout& dst, int H, int I, int g, cudaStream_t st);
+
+// k_route.cu
+struct RouteWs {
+    float* logits;        // [T][E]
+    int32_t* idx;         // [T][k]
+    float* gate;          // [T][k]
+    int32_t* hist;        // [nblk][E]
+    int32_t* base;        // [nblk][E]
+    int32_t* off;         // [E+1]
+    int32_t* act_e;       // [E] active experts (ascending)
+    int32_t* n_act;       // [1]
+    int32_t* perm;        // [T*k] entry (t*k+j) at each permuted row
+    int32_t* inv;         // [T*k] permuted row of entry
+    u64* stats;           // [4] device counters: weight bytes gate/up, down, active experts, -
+};
+int route_blocks(int T);
+void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E,
+                   int H, float* logits, cudaStream_t st);
+void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
+                  uint32_t* cnt_acc, u64* mass_acc, cudaStream_t st);
+// tier: layer table (or NULL); bytes[tier][phase]: algorithmic weight bytes of one expert
+void launch_scan_scatter(int T, int E, int k, const RouteWs& ws, const int32_t* tier, const u64 (&bytes)[2][2],
+                         cudaStream_t st);
+void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st);
+void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int k, int e_lo,
+                        uint32_t* cnt_acc, u64* mass_acc, int32_t* err, cudaStream_t st);
+
+// k_expert.cu
+struct ExpertArgs {
+    const uint8_t* arena_layer;   // base of the layer region
+    const int32_t* tier;          // [E] of this layer
+    const int32_t* slot;
+    i64 hi_base;                  // byte offset of the HIGH region inside the layer region
+    SlotLayout hi, lo;
+    int H, I, g, k;
+};
+void launch_expert_ffn(const ExpertArgs& a, const __nv_bfloat16* x, const float* gate, const RouteWs& ws,
+                       int T, int E, __nv_bfloat16* act, __nv_bfloat16* Y, cudaStream_t st, cudaEvent_t mid);
+
+// k_ctrl.cu
+void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st);
+void launch_plan(const Ctrl& c, int layer, int finalize, cudaStream_t st);
+struct XferArgs {
+    uint8_t* layer_base;
+    i64 hi_base;
+    SlotLayout hi, lo;
+    const uint8_t* const* hi_img;   // [E] device-accessible pointers to HIGH images (host-mapped)
+    int H, I, g;
+};
+void launch_transitions(const Ctrl& c, int layer, const XferArgs& x, int max_cmds, int mode,
+                        cudaStream_t st);
