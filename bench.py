@@ -1,0 +1,396 @@
+"""bench.py -- DynaExq hot path on B200: one step = one pass of the whole path over one decode batch
+of the Qwen3-30B-A3B-shaped 48-layer MoE stack (BASELINE.json configs[1]):
+per layer router logits -> top-k/gates/hotness counters -> permutation -> hybrid-precision expert
+FFN over the slot pool -> combine, then the EMA fold, the periodic plan and the side-stream
+promotions/demotions with their publication (DESIGN.md §1 rows a1-a14).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  N > 1 (torchrun): each rank serves its own batch on a full
+replica of the stack (weak scaling, no data-path collective); value = all ranks' tokens / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer tokens/s decode+prefill at 1/2/4/8 B200; weight-byte HBM GB/s vs peak"
+UNIT = "layer-tokens/s"
+
+# C2: Qwen3-30B-A3B expert geometry, 24e9 B expert budget per GPU, bf16/int4.
+C2 = dict(L=48, E=128, k=8, H=2048, I=768, g=128, high=16, low=4, budget=24 * 10**9, s=1,
+          alpha=0.95, Tp=16, W=32, dwell=32, lag=4, zipf=1.2, drift=32, frac=0.25, n_top=24)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--layers", type=int, default=C2["L"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------- ours
+def host_masters(seed, L, E, H, I, rank, world):
+    """bf16 masters of the whole stack in page-locked host memory (the paper's DRAM cache,
+    PAPER.md:236).  Multi-rank runs share one /dev/shm copy."""
+    import torch
+    import synth
+    n = 3 * I * H
+    total = L * E * n
+    if world > 1:
+        path = f"/dev/shm/dx_masters_{seed}_{L}_{E}_{H}_{I}.bin"
+        if rank == 0 and (not os.path.exists(path) or os.path.getsize(path) != total * 2):
+            mm = np.memmap(path + ".tmp", dtype=np.uint16, mode="w+", shape=(total,))
+            _fill(mm, seed, L, E, H, I)
+            mm.flush()
+            del mm
+            os.replace(path + ".tmp", path)
+        import torch.distributed as dist
+        dist.barrier()
+        arr = np.memmap(path, dtype=np.uint16, mode="r+", shape=(total,))
+    else:
+        arr = np.empty(total, dtype=np.uint16)
+        _fill(arr, seed, L, E, H, I)
+    rc = torch.cuda.cudart().cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+    if int(rc) != 0:
+        raise RuntimeError(f"cudaHostRegister failed: {rc}")
+    return arr, [arr.ctypes.data + i * n * 2 for i in range(L * E)]
+
+
+def _fill(arr, seed, L, E, H, I):
+    import synth
+    n = 3 * I * H
+    for l in range(L):
+        for e in range(E):
+            synth.expert_master_into(seed, l, e, H, I, arr[(l * E + e) * n:(l * E + e + 1) * n])
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import synth
+    from paper_2511_15015_b200 import dx
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    c = dict(C2)
+    L, E, k, H, I, g, B = a.layers, c["E"], c["k"], c["H"], c["I"], c["g"], a.batch
+    seed = a.seed
+    t0 = time.time()
+    arr, ptrs = host_masters(seed, L, E, H, I, rank, world)
+    t_gen = time.time() - t0
+    cfg = dx.dx_config()
+    cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = L, E, k, H, I, g
+    cfg.high_bits, cfg.low_bits = c["high"], c["low"]
+    cfg.expert_budget_bytes = c["budget"] * L // C2["L"]
+    cfg.n_spare, cfg.ema_alpha = c["s"], c["alpha"]
+    cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = c["Tp"], c["W"], c["dwell"], c["lag"]
+    cfg.max_tokens, cfg.ep_rank, cfg.ep_size = max(B, 64), 0, 1
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    pool = dx.Pool(cfg, ptrs, stream)
+    t_pool = time.time() - t0
+    n_hot = pool.info.n_hot
+    # router weights per layer + Zipf bias per (layer, drift epoch) -> skewed, drifting routing
+    wr = torch.empty(L, E, H, dtype=torch.bfloat16, device=dev)
+    for l in range(L):
+        wr[l].copy_(torch.from_numpy(synth.router_bf16(seed, l, E, H).view(np.int16)).view(torch.bfloat16))
+    total_steps = c["W"] + a.warmup + 2 * a.steps + 2
+    n_epochs = total_steps // c["drift"] + 2
+    bias = torch.empty(L, n_epochs, E, dtype=torch.float32, device=dev)
+    for l in range(L):
+        for ep in range(n_epochs):
+            rk = synth.rank_perm(seed, l, ep, E, c["n_top"], c["frac"])
+            bias[l, ep].copy_(torch.from_numpy(synth.zipf_logp(rk, c["zipf"])))
+    xs_host = torch.empty(total_steps, B, H, dtype=torch.int16, pin_memory=True)
+    for s_ in range(total_steps):
+        xs_host[s_].copy_(torch.from_numpy(synth.normal_bf16(seed, 100 + rank, s_, 0, (B, H)).view(np.int16)))
+    xs = xs_host.to(dev).view(torch.bfloat16)
+    y = torch.empty(2, B, H, dtype=torch.bfloat16, device=dev)
+    step_counter = [0]
+
+    def step(x):
+        s_ = step_counter[0]
+        ep = s_ // c["drift"]
+        for l in range(L):
+            pool.dx_moe_forward(l, x, B, y[l & 1], router_w=wr[l], router_bias=bias[l, ep])
+            pool.dx_hotness_update(l)
+            pool.dx_plan_precision(l)
+        step_counter[0] += 1
+
+    # controller warm-up (t < W) and finalize at t = W, then the bench warm-up
+    for s_ in range(c["W"]):
+        step(xs[s_])
+    for l in range(L):
+        pool.dx_plan_precision(l)
+    for s_ in range(a.warmup):
+        step(xs[c["W"] + s_])
+    pool.dx_sync()
+    pool.dx_profile_read()
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+    # ---------------- timed region (device-resident inputs)
+    base = c["W"] + a.warmup
+    pool.dx_profile_enable(True)
+    launches0 = pool.dx_kernel_launches()
+    if dist_on:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for s_ in range(a.steps):
+            step(xs[base + s_])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = pool.dx_kernel_launches() - launches0
+    prof = pool.dx_profile_read()
+    pool.dx_profile_enable(False)
+    ms_max = ms
+    if dist_on:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_max = float(tt.item())
+    # ---------------- end-to-end: host x -> device, stack, y -> host, every step
+    e2e = None
+    if not a.no_e2e:
+        yh = torch.empty(B, H, dtype=torch.bfloat16, pin_memory=True)
+        xdev = torch.empty(B, H, dtype=torch.bfloat16, device=dev)
+        base2 = base + a.steps
+        if dist_on:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s_ in range(a.steps):
+            xdev.view(torch.int16).copy_(xs_host[base2 + s_], non_blocking=True)
+            step(xdev)
+            yh.copy_(y[(L - 1) & 1], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        if dist_on:
+            tt = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt.item())
+        e2e = {"value": world * B * L * a.steps / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": B * H * 2, "d2h_bytes_per_step": B * H * 2, "ms_per_step": e_ms / a.steps}
+    peak, peak_src = load_peaks()
+    wb = prof["weight_bytes"]
+    ffn_ms = prof["ffn_ms"]
+    ach0 = wb[0] / (ffn_ms[0] / 1e3) / 1e9 if ffn_ms[0] > 0 else 0.0
+    ach_all = (wb[0] + wb[1]) / ((ffn_ms[0] + ffn_ms[1]) / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ffn_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("gateup_dram_bytes_per_launch")
+    out = {
+        "metric": METRIC, "value": world * B * L * a.steps / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 weights, "
+        "Zipf(1.2) router bias with drift; see DESIGN.md input recipe)",
+        "config": {"workload": f"C2: Qwen3-30B-A3B-shaped {L}-layer MoE decode stack (E=128, top-8, H=2048, "
+                               f"I=768), batch {B} per GPU, 24e9 B expert budget (n_hot={n_hot}/128 bf16, rest "
+                               "int4 g=128), router mode, controller Tp=16 L=4 with drift",
+                   "global_batch": B * world, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "l2": "no flush: each step streams >=48 distinct layers of weights (> 126 MB L2)"},
+        "roofline": {"bound": "hbm", "kernel": "k_ffn gate/up (phase 0)", "achieved": ach0, "peak": peak,
+                     "unit": "GB/s", "frac": ach0 / peak, "traffic": traffic, "peak_source": peak_src,
+                     "ffn_both_phases_gbs": ach_all, "ffn_both_frac": ach_all / peak,
+                     "algorithmic_bytes_per_launch": wb[0] / max(prof["forwards"], 1)},
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "extra": {"ffn_ms_share": (ffn_ms[0] + ffn_ms[1]) / ms if ms > 0 else None,
+                  "fwd_ms_share": prof["fwd_ms"] / ms if ms > 0 else None,
+                  "active_experts_per_layer": prof["active_experts"] / max(prof["forwards"], 1),
+                  "weight_bytes_per_layer": (wb[0] + wb[1]) / max(prof["forwards"], 1),
+                  "setup_s": {"masters": t_gen, "pool_create": t_pool}},
+    }
+    clock = clk.summary()
+    if clock:
+        out["clocks"] = clock
+    pool.close()
+    return out
+
+
+# ---------------------------------------------------------------------------------------- oracle arm
+def oracle_layer_sample(a, seconds=15.0, max_steps=None):
+    """The CPU oracle (as it stands) on a bounded sample of the same workload: one layer of the stack
+    (layer 0), batch B, router mode, controller fold/plan, FFN from pre-dequantised stable images."""
+    import oracle
+    import synth
+    c = dict(C2)
+    E, k, H, I, g, B = c["E"], c["k"], c["H"], c["I"], c["g"], a.batch
+    n_hot = oracle.n_hot(c["budget"] // c["L"], E, oracle.slot_bytes(H, I, g, 16), oracle.slot_bytes(H, I, g, 4),
+                         c["s"])
+    wr = synth.router_bf16(a.seed, 0, E, H)
+    rk = synth.rank_perm(a.seed, 0, 0, E, c["n_top"], c["frac"])
+    bias = synth.zipf_logp(rk, c["zipf"])
+    tiers = {e: bool(rk[e] < n_hot) for e in range(E)}
+    ctrl = oracle.Controller(E, n_hot, c["s"], c["alpha"], c["Tp"], 0, c["dwell"], c["lag"])
+    ctrl.plan()
+    Wcache = {}
+    nthreads = os.cpu_count() or 1
+    times = []
+    t_start = time.time()
+    s_ = 0
+    while True:
+        x = synth.normal_bf16(a.seed, 100, s_, 0, (B, H))
+        lg = oracle.router_logits(x, wr, bias).astype(np.float32)
+        idx, gate = oracle.route(lg, k)
+        for e in np.unique(idx):          # stable images prepared outside the timed part (as the pool is)
+            e = int(e)
+            if e not in Wcache:
+                Wcache[e] = oracle.expert_tier(synth.expert_master(a.seed, 0, e, H, I), H, I, g, 16, 4, tiers[e])
+        t0 = time.perf_counter()
+        lg = oracle.router_logits(x, wr, bias).astype(np.float32)
+        idx, gate = oracle.route(lg, k)
+        _, y = oracle.moe_ffn(x, idx, gate, Wcache, H, I, nthreads=nthreads)
+        _, mass = oracle.counts(idx, gate, E)
+        ctrl.fold(mass, B)
+        ctrl.plan()
+        times.append(time.perf_counter() - t0)
+        s_ += 1
+        if (max_steps and s_ >= max_steps) or (not max_steps and sum(times) >= seconds) or \
+                time.time() - t_start > 4 * seconds:
+            break
+    return B / statistics.mean(times), nthreads, len(times), times
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return None
+    n = a.warmup + a.steps
+    val, cores, nsteps, times = oracle_layer_sample(a, max_steps=n)
+    t = times[a.warmup:] if len(times) > a.warmup else times
+    v = a.batch / statistics.mean(t)
+    sample = f"layer 0 of the C2 stack, batch {a.batch}, {len(t)} timed steps (router, top-k, FFN, fold, plan)"
+    return {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * statistics.mean(t), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2 layer sample, batch {a.batch}", "global_batch": a.batch},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if a.impl == "ours":
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl" if a.impl == "ours" else "gloo")
+    if a.impl == "reference":
+        out = run_reference(a, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    out = run_ours(a, rank, world, local_rank)
+    if rank == 0:
+        if not a.no_cpu_baseline:
+            v, cores, nsteps, _ = oracle_layer_sample(a, seconds=15.0)
+            out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                   "sample": f"layer 0 of the C2 stack, batch {a.batch}, {nsteps} steps "
+                                             "(router, top-k, FFN over pre-dequantised stable images, fold, plan)"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

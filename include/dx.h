@@ -181,6 +181,10 @@ dx_status dx_dequantize(const void* codes_packed, const void* scales_bf16, const
 int64_t dx_slot_bytes(int32_t H, int32_t I, int32_t g, int32_t bits);
 int64_t dx_solve_n_hot(int64_t layer_budget, int32_t n_experts, int64_t S_h, int64_t S_l, int32_t n_spare);
 
+/* Expert-FFN implementation: 0 = tcgen05/TMEM grouped GEMM with TMA and in-smem dequant (default),
+ * 1 = register-dequant mma.sync streaming kernel (kept as an independent cross-check). */
+dx_status dx_set_ffn_path(dx_pool pool, int32_t path);
+
 /* ---------------------------------------------------------------- profiling for benches */
 typedef struct {
     int64_t  forwards;          /* dx_moe_forward calls (T > 0) since the last read */

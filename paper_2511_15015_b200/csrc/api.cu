@@ -6,6 +6,7 @@
 #include <vector>
 #include <cmath>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include "dx_common.cuh"
 
 void launch_manual(const Ctrl& c, int layer, const int2* cmds, int n, int32_t* status, cudaStream_t st);
@@ -60,7 +61,88 @@ struct dx_pool_s {
     std::vector<cudaEvent_t> prof_ev;       // 4 per forward: start, after routing, between FFN phases, end
     std::vector<cudaEvent_t> prof_free;
     i64 prof_fwd = 0;
+    int ffn_path = 0;                       // 0: tcgen05 grouped GEMM, 1: mma.sync decode kernel
+    __nv_bfloat16* Xp = nullptr;            // x rows in permuted order (B operand of gate/up)
+    std::vector<GemmMaps> gmaps;            // per layer (weights); xb filled per launch
+    CUtensorMap xb0[4], xb1[4];             // B operand maps for BN = 32, 64, 128, 256
 };
+
+// ---------------------------------------------------------------- TMA tensor maps (driver entry point)
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static bool get_encode() {
+    if (g_encode) return true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+        cudaGetLastError();
+        return false;
+    }
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    return true;
+}
+static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const uint64_t* dims,
+                     const uint64_t* strides, const uint32_t* box, CUtensorMapSwizzle sw) {
+    uint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_encode(m, dt, rank, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+static dx_status build_maps(dx_pool p) {
+    if (!get_encode()) { dx_set_error("cuTensorMapEncodeTiled unavailable"); return DX_ERR_CUDA; }
+    const int H = p->H, I = p->I, E = p->E_loc, s = p->cfg.n_spare, T = p->cfg.max_tokens, k = p->k;
+    const int cap_hi = p->info.cap_hi;
+    p->gmaps.assign(p->L, GemmMaps{});
+    for (int l = 0; l < p->L; ++l) {
+        GemmMaps& g = p->gmaps[l];
+        const uint8_t* lb = p->weights + (size_t)l * p->layer_bytes;
+        bool ok = true;
+        if (p->hi.bits == 16) {
+            const uint64_t d0[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
+            const uint64_t s0[2] = {(uint64_t)H * 2, (uint64_t)p->hi.bytes};
+            const uint32_t b0[3] = {64, 16, 1};
+            ok &= make_map(&g.a16_gu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, lb + p->hi_base, d0, s0, b0,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+            const uint64_t d1[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
+            const uint64_t s1[2] = {(uint64_t)I * 2, (uint64_t)p->hi.bytes};
+            const uint32_t b1[3] = {64, 128, 1};
+            ok &= make_map(&g.a16_dn, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, lb + p->hi_base + (size_t)2 * I * H * 2, d1, s1,
+                           b1, CU_TENSOR_MAP_SWIZZLE_128B);
+        }
+        for (int t = 0; t < 2; ++t) {
+            const SlotLayout& Ls = t ? p->hi : p->lo;
+            if (Ls.bits == 16) continue;
+            const uint8_t* base = lb + (t ? p->hi_base : 0);
+            const uint64_t slots = t ? (uint64_t)(cap_hi > 0 ? cap_hi : 1) : (uint64_t)(E + s);
+            const uint64_t rb0 = (uint64_t)H * Ls.bits / 8, rb1 = (uint64_t)I * Ls.bits / 8;
+            const uint32_t kb = 64 * Ls.bits / 8;
+            const uint64_t d0[3] = {rb0, (uint64_t)2 * I, slots};
+            const uint64_t s0[2] = {rb0, (uint64_t)Ls.bytes};
+            const uint32_t b0[3] = {kb, 64, 1};
+            ok &= make_map(t ? &g.ahi_gu : &g.alo_gu, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, d0, s0, b0,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
+            const uint64_t d1[3] = {rb1, (uint64_t)H, slots};
+            const uint64_t s1[2] = {rb1, (uint64_t)Ls.bytes};
+            const uint32_t b1[3] = {kb, 128, 1};
+            ok &= make_map(t ? &g.ahi_dn : &g.alo_dn, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * Ls.codes_stride, d1, s1,
+                           b1, CU_TENSOR_MAP_SWIZZLE_NONE);
+        }
+        if (!ok) { dx_set_error("tensor map encoding failed (layer %d)", l); return DX_ERR_CUDA; }
+    }
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t bn = 32u << i;
+        const uint64_t rows = (uint64_t)T * k;
+        const uint64_t d0[2] = {(uint64_t)H, rows}, s0[1] = {(uint64_t)H * 2};
+        const uint64_t d1[2] = {(uint64_t)I, rows}, s1[1] = {(uint64_t)I * 2};
+        const uint32_t b[2] = {64, bn};
+        if (!make_map(&p->xb0[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->Xp, d0, s0, b, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !make_map(&p->xb1[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, b, CU_TENSOR_MAP_SWIZZLE_128B)) {
+            dx_set_error("tensor map encoding failed (activations)");
+            return DX_ERR_CUDA;
+        }
+    }
+    return DX_OK;
+}
 
 static u64 phase_bytes(const SlotLayout& L, int H, int I, int g, int nmat) {
     const u64 n = (u64)I * H;
@@ -157,7 +239,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         ctrl_bytes = LE * (4 + 4 + 4 + 8 + 4 + 8 + 8 + 4 + 4 + 8 + 16) + LO * 8 + L * (8 + 8 + 4 * 3) + 64 * 256;
     }
     const size_t ws_bytes = (size_t)T * p->E * 4 + (size_t)T * k * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
-                            (size_t)(p->E + 1) * 8 + (size_t)T * k * (p->I + p->H) * 2 + 64 * 256 + 4096 * 8;
+                            (size_t)(p->E + 1) * 8 + (size_t)T * k * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8;
     const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
     const size_t total = (size_t)L * p->layer_bytes + ctrl_bytes + ws_bytes + stage_bytes + ptr_bytes + 4096;
@@ -206,6 +288,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     w.stats = carve<u64>(q, 4);
     p->act = carve<__nv_bfloat16>(q, (size_t)T * k * p->I);
     p->Y = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
+    p->Xp = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
     p->err_flag = carve<int32_t>(q, 1);
     p->manual_cmds = carve<int2>(q, 1024);
     p->manual_status = carve<int32_t>(q, 1024);
@@ -338,7 +421,16 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     const i64 n3 = (i64)3 * p->I * p->H;
     inf.export_bytes_hi = cfg->high_bits == 16 ? n3 * 2 : n3 + n3 / p->g * 3;
     inf.export_bytes_lo = n3 + n3 / p->g * 3;
+    st = build_maps(p);
+    if (st != DX_OK) return fail(st);
     *out = p;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_set_ffn_path(dx_pool p, int32_t path) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    DX_CHECK(path == 0 || path == 1, DX_ERR_INVALID_ARG, "path must be 0 (tcgen05) or 1 (mma.sync)");
+    p->ffn_path = path;
     return DX_OK;
 }
 
@@ -448,7 +540,28 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
     a.lo = p->lo;
     a.H = p->H; a.I = p->I; a.g = p->g; a.k = p->k;
     if (ev[1]) DX_CUDA(cudaEventRecord(ev[1], p->cs));
-    launch_expert_ffn(a, (const __nv_bfloat16*)x, ws.gate, ws, T, p->E, p->act, p->Y, p->cs, ev[2]);
+    if (p->ffn_path == 1) {
+        launch_expert_ffn(a, (const __nv_bfloat16*)x, ws.gate, ws, T, p->E, p->act, p->Y, p->cs, ev[2]);
+    } else {
+        // tcgen05 grouped GEMMs (k_gemm.cu): gather x rows in permuted order, gate/up + SwiGLU, down
+        const int bn = gemm_bn_for(T);
+        int bi = 0;
+        while ((32 << bi) < bn) ++bi;
+        const int max_act = T * p->k < p->E ? T * p->k : p->E;
+        GemmArgs ga;
+        ga.layer = a.arena_layer; ga.hi_base = p->hi_base; ga.hi = p->hi; ga.lo = p->lo;
+        ga.tier = a.tier; ga.slot = a.slot; ga.off = ws.off; ga.act_e = ws.act_e; ga.n_act = ws.n_act;
+        ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = p->k;
+        ga.act = p->act; ga.Y = p->Y;
+        GemmMaps gm = p->gmaps[layer];
+        launch_gather((const __nv_bfloat16*)x, ws.perm, T * p->k, p->k, p->H, p->Xp, p->cs);
+        gm.xb = p->xb0[bi];
+        launch_gemm(0, bn, gm, ga, max_act * (p->I / 64), p->cs);
+        if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
+        gm.xb = p->xb1[bi];
+        launch_gemm(1, bn, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
+        p->launches += 1;
+    }
     if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));
     launch_combine(p->Y, T, p->k, p->H, (__nv_bfloat16*)y, p->cs);
     p->launches += 6;

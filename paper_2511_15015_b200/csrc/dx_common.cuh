@@ -165,6 +165,34 @@ struct ExpertArgs {
 void launch_expert_ffn(const ExpertArgs& a, const __nv_bfloat16* x, const float* gate, const RouteWs& ws,
                        int T, int E, __nv_bfloat16* act, __nv_bfloat16* Y, cudaStream_t st, cudaEvent_t mid);
 
+// k_gemm.cu (tcgen05 grouped GEMM)
+#include <cuda.h>
+struct GemmMaps {
+    CUtensorMap a16_gu, a16_dn;     // bf16 HIGH region: dims {K, rows, slots}, 128 B swizzle
+    CUtensorMap ahi_gu, ahi_dn;     // raw codes of a quantised HIGH region
+    CUtensorMap alo_gu, alo_dn;     // raw codes of the LOW region
+    CUtensorMap xb;                 // B operand rows [rows][K] bf16, box {64, BN}, 128 B swizzle
+};
+struct GemmArgs {
+    const uint8_t* layer;
+    i64 hi_base;
+    SlotLayout hi, lo;
+    const int32_t* tier;
+    const int32_t* slot;
+    const int32_t* off;
+    const int32_t* act_e;
+    const int32_t* n_act;
+    const int32_t* perm;
+    const float* gate;
+    int H, I, g, k;
+    __nv_bfloat16* act;
+    __nv_bfloat16* Y;
+};
+int gemm_bn_for(int T);
+void launch_gather(const __nv_bfloat16* x, const int32_t* perm, int rows, int k, int H, __nv_bfloat16* Xp,
+                   cudaStream_t st);
+void launch_gemm(int phase, int bn, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
+
 // k_ctrl.cu
 void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st);
 void launch_plan(const Ctrl& c, int layer, int finalize, cudaStream_t st);

@@ -6,7 +6,7 @@
 // R-H1 (cnt u32, mass = sum rint(g * 2^24) u64: integer sums are order-free => bit-exact).
 #include "dx_common.cuh"
 
-#define ROUTE_TOK_PER_BLK 64
+#define ROUTE_TOK_PER_BLK 8
 #define ROUTE_MAX_E 512
 #define ROUTE_MAX_K 16
 
@@ -72,8 +72,10 @@ __device__ __forceinline__ bool better(float a, int ea, float b, int eb) {
 }
 
 // ------------------------------------------------------------------ a2 + a3: top-k, gates, counters
-// One warp per token, k rounds of (value desc, id asc) warp arg-max; per-block shared histograms
-// merged into the layer's global accumulators with one atomic per touched expert.
+// One warp per token (8 tokens per block), k rounds of (value desc, id asc) warp arg-max over NVT
+// logits per lane; per-block shared histograms merged into the layer's global accumulators with one
+// atomic per touched expert.
+template <int NVT>
 __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits, int T, int E, int k,
                                                int e_lo, int e_cnt, int32_t* __restrict__ idx_out,
                                                float* __restrict__ gate_out, int32_t* __restrict__ hist,
@@ -83,18 +85,16 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
     for (int e = threadIdx.x; e < E; e += blockDim.x) { cnt_s[e] = 0; mass_s[e] = 0; }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int NV = (E + 31) / 32;
-    for (int tt = warp; tt < ROUTE_TOK_PER_BLK; tt += 8) {
-        const int t = blockIdx.x * ROUTE_TOK_PER_BLK + tt;
-        if (t >= T) break;
-        float v[ROUTE_MAX_E / 32];
+    const int t = blockIdx.x * ROUTE_TOK_PER_BLK + warp;
+    if (t < T) {
+        float v[NVT];
         uint32_t taken = 0;
         const float* lrow = logits + (size_t)t * E;
 #pragma unroll
-        for (int i = 0; i < ROUTE_MAX_E / 32; ++i) {
+        for (int i = 0; i < NVT; ++i) {
             const int e = lane + 32 * i;
-            v[i] = (i < NV && e < E) ? lrow[e] : -INFINITY;
-            if (!(i < NV && e < E)) taken |= 1u << i;
+            v[i] = e < E ? lrow[e] : -INFINITY;
+            if (e >= E) taken |= 1u << i;
         }
         float sel_v[ROUTE_MAX_K];
         int sel_e[ROUTE_MAX_K];
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
             float bv = -INFINITY;
             int be = 0x7fffffff;
 #pragma unroll
-            for (int i = 0; i < ROUTE_MAX_E / 32; ++i) {
+            for (int i = 0; i < NVT; ++i) {
                 const int e = lane + 32 * i;
                 if (!((taken >> i) & 1u) && better(v[i], e, bv, be)) { bv = v[i]; be = e; }
             }
@@ -214,36 +214,20 @@ __global__ void __launch_bounds__(512) k_scan(const int32_t* __restrict__ hist, 
     (void)tot_s;
 }
 
-// one warp per route block: walk entries (t*k + j) in order, place each at base + rank among
-// earlier entries of the same expert (stable counting sort).
-__global__ void __launch_bounds__(32) k_scatter(const int32_t* __restrict__ idx, int T, int E, int k,
-                                                const int32_t* __restrict__ base,
-                                                int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
-    __shared__ int32_t run[ROUTE_MAX_E];
-    const int lane = threadIdx.x;
-    for (int e = lane; e < E; e += 32) run[e] = base[(size_t)blockIdx.x * E + e];
-    __syncwarp();
-    const int t0 = blockIdx.x * ROUTE_TOK_PER_BLK;
-    const int n_ent = (min(T, t0 + ROUTE_TOK_PER_BLK) - t0) * k;
-    const int ent0 = t0 * k;
-    for (int b = 0; b < n_ent; b += 32) {
-        const int i = b + lane;
-        const bool valid = i < n_ent;
-        const int e = valid ? idx[ent0 + i] : -1 - lane;
-        const unsigned act = __ballot_sync(0xffffffffu, valid);
-        const unsigned peers = __match_any_sync(0xffffffffu, e);
-        const int rank = __popc(peers & ((1u << lane) - 1u));
-        int pos = 0;
-        if (valid) pos = run[e] + rank;
-        __syncwarp();
-        if (valid) {
-            perm[pos] = ent0 + i;
-            inv[ent0 + i] = pos;
-            if ((31 - __clz(peers)) == lane) run[e] += __popc(peers);   // highest lane updates
-        }
-        __syncwarp();
-        (void)act;
-    }
+// one thread per entry (t*k + j): position = base[block][e] + number of earlier entries of the same
+// expert inside its route block (<= 8k comparisons): the stable counting-sort order (t asc, j asc).
+__global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ idx, int T, int E, int k,
+                                                 const int32_t* __restrict__ base,
+                                                 int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= T * k) return;
+    const int b = (i / k) / ROUTE_TOK_PER_BLK;
+    const int e = idx[i];
+    int r = 0;
+    for (int q = b * ROUTE_TOK_PER_BLK * k; q < i; ++q) r += (idx[q] == e);
+    const int pos = base[(size_t)b * E + e] + r;
+    perm[pos] = i;
+    inv[i] = pos;
 }
 
 // ------------------------------------------------------------------ a8: y_t = bf16(sum_j Y[t,j])
@@ -307,8 +291,10 @@ void launch_route(const float* logits, int T, int E, int k, int e_lo, const Rout
                   uint32_t* cnt_acc, u64* mass_acc, cudaStream_t st) {
     (void)e_lo;
     if (T <= 0) return;
-    k_route<<<route_blocks(T), 256, 0, st>>>(logits, T, E, k, e_lo, cnt_acc ? E : 0, ws.idx, ws.gate,
-                                             ws.hist, cnt_acc, mass_acc);
+    const int nb = route_blocks(T), ec = cnt_acc ? E : 0;
+    if (E <= 128)      k_route<4><<<nb, 256, 0, st>>>(logits, T, E, k, e_lo, ec, ws.idx, ws.gate, ws.hist, cnt_acc, mass_acc);
+    else if (E <= 256) k_route<8><<<nb, 256, 0, st>>>(logits, T, E, k, e_lo, ec, ws.idx, ws.gate, ws.hist, cnt_acc, mass_acc);
+    else               k_route<16><<<nb, 256, 0, st>>>(logits, T, E, k, e_lo, ec, ws.idx, ws.gate, ws.hist, cnt_acc, mass_acc);
 }
 
 void launch_scan_scatter(int T, int E, int k, const RouteWs& ws, const int32_t* tier, const u64 (&bytes)[2][2],
@@ -317,7 +303,7 @@ void launch_scan_scatter(int T, int E, int k, const RouteWs& ws, const int32_t* 
     const int nblk = route_blocks(T);
     k_scan<<<1, 512, 0, st>>>(ws.hist, nblk, E, ws.base, ws.off, ws.act_e, ws.n_act, tier, bytes[0][0],
                               bytes[0][1], bytes[1][0], bytes[1][1], ws.stats);
-    k_scatter<<<nblk, 32, 0, st>>>(ws.idx, T, E, k, ws.base, ws.perm, ws.inv);
+    k_scatter<<<(T * k + 255) / 256, 256, 0, st>>>(ws.idx, T, E, k, ws.base, ws.perm, ws.inv);
 }
 
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st) {

@@ -93,6 +93,7 @@ _SIG = {
     "dx_quantize": [_vp, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp],
     "dx_dequantize": [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp],
     "dx_profile_enable": [_vp, _i32],
+    "dx_set_ffn_path": [_vp, _i32],
     "dx_profile_read": [_vp, _P(dx_profile_t)],
 }
 for _n, _a in _SIG.items():
@@ -264,6 +265,9 @@ class Pool:
 
     def dx_kernel_launches(self) -> int:
         return _lib.dx_kernel_launches(self.h)
+
+    def dx_set_ffn_path(self, path: int):
+        _check(_lib.dx_set_ffn_path(self.h, path), "dx_set_ffn_path")
 
     def dx_profile_enable(self, enable: bool = True):
         _check(_lib.dx_profile_enable(self.h, int(enable)), "dx_profile_enable")

@@ -211,18 +211,31 @@ def test_router_mode_logits_and_routing(dx):
 
 
 # ------------------------------------------------------------------ Qwen3-30B / Qwen3-Next-80B shapes
+_MASTERS = {}
+
+
+def _masters_cached(seed, E, H, I):
+    key = (seed, E, H, I)
+    if key not in _MASTERS:
+        _MASTERS.clear()
+        _MASTERS[key] = Masters(seed, 1, E, H, I)
+    return _MASTERS[key]
+
+
+@pytest.mark.parametrize("path", [0, 1], ids=["tcgen05", "mma"])
 @pytest.mark.parametrize("shape", ["q30b", "q80b"])
-@pytest.mark.parametrize("T", [1, 64])
-def test_layer_parity_paper_shapes(dx, shape, T):
+@pytest.mark.parametrize("T", [1, 64, 200])
+def test_layer_parity_paper_shapes(dx, shape, T, path):
     if shape == "q30b":
         E, k, H, I, g, hb, lb = 128, 8, 2048, 768, 128, 16, 4
     else:
         E, k, H, I, g, hb, lb = 512, 10, 2048, 512, 128, 4, 2
     n_hot = E // 5
-    m = Masters(1, 1, E, H, I)
+    m = _masters_cached(1, E, H, I)
     cfg = make_cfg(dx, 1, E, k, H, I, g, hb, lb, budget_for(E, H, I, g, hb, lb, n_hot, 1), 1, 0.95, 16, 1, 32,
-                   4, 64)
+                   4, 256)
     pool = dx.Pool(cfg, m.ptrs(), torch.cuda.current_stream())
+    pool.dx_set_ffn_path(path)
     assert pool.info.n_hot == n_hot
     # one warm-up step, then finalize: the top n_hot by the first step's mass go HIGH
     lg0 = synth.trace_logits(1, 0, 0, 64, E, 1.2)
@@ -239,6 +252,7 @@ def test_layer_parity_paper_shapes(dx, shape, T):
     assert np.array_equal(tab["tier"], ctrl.state()["tier"])
     lg = synth.trace_logits(1, 0, 1, T, E, 1.2)
     x = synth.normal_bf16(1, 0, 1, 0, (T, H))
+    y = torch.zeros(T, H, dtype=torch.bfloat16, device="cuda")
     idx = torch.zeros(T, k, dtype=torch.int32, device="cuda")
     gate = torch.zeros(T, k, dtype=torch.float32, device="cuda")
     pool.dx_moe_forward(0, bf16_dev(x), T, y, logits=torch.from_numpy(lg).cuda(), topk_idx=idx, topk_gate=gate)
