@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=C2["L"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--router-scale", type=float, default=3.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -139,6 +140,18 @@ def host_masters(seed, L, E, H, I, rank, world):
     return arr, [arr.ctypes.data + i * n * 2 for i in range(L * E)]
 
 
+def router_weights(seed, l, E, H, scale):
+    """Router W_r of layer l: synth uniform(±1/sqrt(H)) scaled by `scale` (x W_r^T then has std
+    ~0.58*scale per logit, a per-token spread comparable to the Gumbel noise of the trace recipe) and
+    re-rounded to bf16."""
+    import synth
+    w = synth.router_bf16(seed, l, E, H)
+    f = (w.astype(np.uint32) << 16).view(np.float32) * np.float32(scale)
+    u = f.view(np.uint32)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16        # round to nearest even
+    return u.astype(np.uint16)
+
+
 def _fill(arr, seed, L, E, H, I):
     import synth
     n = 3 * I * H
@@ -174,7 +187,7 @@ def run_ours(a, rank, world, local_rank):
     # router weights per layer + Zipf bias per (layer, drift epoch) -> skewed, drifting routing
     wr = torch.empty(L, E, H, dtype=torch.bfloat16, device=dev)
     for l in range(L):
-        wr[l].copy_(torch.from_numpy(synth.router_bf16(seed, l, E, H).view(np.int16)).view(torch.bfloat16))
+        wr[l].copy_(torch.from_numpy(router_weights(seed, l, E, H, a.router_scale).view(np.int16)).view(torch.bfloat16))
     total_steps = c["W"] + a.warmup + 2 * a.steps + 2
     n_epochs = total_steps // c["drift"] + 2
     bias = torch.empty(L, n_epochs, E, dtype=torch.float32, device=dev)
@@ -276,7 +289,8 @@ def run_ours(a, rank, world, local_rank):
         "Zipf(1.2) router bias with drift; see DESIGN.md input recipe)",
         "config": {"workload": f"C2: Qwen3-30B-A3B-shaped {L}-layer MoE decode stack (E=128, top-8, H=2048, "
                                f"I=768), batch {B} per GPU, 24e9 B expert budget (n_hot={n_hot}/128 bf16, rest "
-                               "int4 g=128), router mode, controller Tp=16 L=4 with drift",
+                               f"int4 g=128), router mode (W_r x{a.router_scale:g} + Zipf(1.2) bias, ~90 experts "
+                               "touched per layer), controller Tp=16 L=4 with drift",
                    "global_batch": B * world, "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "l2": "no flush: each step streams >=48 distinct layers of weights (> 126 MB L2)"},
         "roofline": {"bound": "hbm", "kernel": "k_ffn gate/up (phase 0)", "achieved": ach0, "peak": peak,
@@ -308,7 +322,7 @@ def oracle_layer_sample(a, seconds=15.0, max_steps=None):
     E, k, H, I, g, B = c["E"], c["k"], c["H"], c["I"], c["g"], a.batch
     n_hot = oracle.n_hot(c["budget"] // c["L"], E, oracle.slot_bytes(H, I, g, 16), oracle.slot_bytes(H, I, g, 4),
                          c["s"])
-    wr = synth.router_bf16(a.seed, 0, E, H)
+    wr = router_weights(a.seed, 0, E, H, a.router_scale)
     rk = synth.rank_perm(a.seed, 0, 0, E, c["n_top"], c["frac"])
     bias = synth.zipf_logp(rk, c["zipf"])
     tiers = {e: bool(rk[e] < n_hot) for e in range(E)}

@@ -11,6 +11,11 @@
 
 void launch_manual(const Ctrl& c, int layer, const int2* cmds, int n, int32_t* status, cudaStream_t st);
 
+bool g_dx_pdl = [] {
+    const char* s = getenv("DX_PDL");
+    return !(s && s[0] == '0');
+}();
+
 static thread_local char g_err[1024] = "";
 void dx_set_error(const char* fmt, ...) {
     va_list ap;
@@ -286,6 +291,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     w.perm = carve<int32_t>(q, (size_t)T * k);
     w.inv = carve<int32_t>(q, (size_t)T * k);
     w.stats = carve<u64>(q, 4);
+    w.done = carve<unsigned>(q, 1);
     p->act = carve<__nv_bfloat16>(q, (size_t)T * k * p->I);
     p->Y = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
     p->Xp = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
@@ -380,6 +386,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         DX_CUDA(cudaMemcpyAsync(c.plan_n, pn.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
         DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
+        DX_CUDA(cudaMemsetAsync(w.done, 0, 4, p->cs));
         DX_CUDA(cudaStreamSynchronize(p->cs));
     }
     for (int ti = 0; ti < 2; ++ti) {
@@ -529,8 +536,10 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
         p->launches += 1;
     }
     const size_t base = (size_t)layer * p->E_loc;
-    launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->cs);
-    launch_scan_scatter(T, p->E, p->k, ws, p->ctrl.tier + base, p->wbytes, p->cs);
+    // a2+a3 (+ the a4 offset scan in the last block), then a4 placement (+ x gather for tcgen05)
+    launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->ctrl.tier + base,
+                 p->wbytes, p->cs);
+    launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
     ExpertArgs a;
     a.arena_layer = p->weights + (size_t)layer * p->layer_bytes;
     a.tier = p->ctrl.tier + base;
@@ -554,17 +563,15 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
         ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = p->k;
         ga.act = p->act; ga.Y = p->Y;
         GemmMaps gm = p->gmaps[layer];
-        launch_gather((const __nv_bfloat16*)x, ws.perm, T * p->k, p->k, p->H, p->Xp, p->cs);
         gm.xb = p->xb0[bi];
         launch_gemm(0, bn, gm, ga, max_act * (p->I / 64), p->cs);
         if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
         gm.xb = p->xb1[bi];
         launch_gemm(1, bn, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
-        p->launches += 1;
     }
     if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));
     launch_combine(p->Y, T, p->k, p->H, (__nv_bfloat16*)y, p->cs);
-    p->launches += 6;
+    p->launches += 5;
     p->pend_tokens[layer] += (u64)T;
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "launch failed: %s", cudaGetErrorString(ce));

@@ -82,6 +82,33 @@ struct Ctrl {
 
 #define DX_NEVER (-(i64)(1ULL << 61))
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every hot-path kernel waits for its predecessor's memory with griddepcontrol.wait (a no-op when it
+// was launched without the PDL attribute) and immediately allows its successor to be scheduled, so
+// launch latency and prologues (barrier init, TMEM alloc, descriptor prefetch) overlap the tail of the
+// previous kernel.
+#define DX_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define DX_GRID_LAUNCH() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+
+#ifdef __CUDACC__
+template <typename... KArgs, typename... Args>
+static inline cudaError_t dx_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                    bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+#endif
+extern bool g_dx_pdl;   // library-wide switch (default on; DX_PDL=0 disables)
+
 // ---------------------------------------------------------------- numerics
 __device__ __forceinline__ float dx_bf2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 
@@ -140,15 +167,22 @@ struct RouteWs {
     int32_t* perm;        // [T*k] entry (t*k+j) at each permuted row
     int32_t* inv;         // [T*k] permuted row of entry
     u64* stats;           // [4] device counters: weight bytes gate/up, down, active experts, -
+    unsigned* done;       // [1] route-block completion counter (last block runs the scan)
+};
+struct RouteStats {       // profiling: algorithmic weight bytes per touched expert [tier][phase]
+    const int32_t* tier;
+    u64 b00, b01, b10, b11;
+    u64* stats;
 };
 int route_blocks(int T);
 void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E,
                    int H, float* logits, cudaStream_t st);
-void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
-                  uint32_t* cnt_acc, u64* mass_acc, cudaStream_t st);
 // tier: layer table (or NULL); bytes[tier][phase]: algorithmic weight bytes of one expert
-void launch_scan_scatter(int T, int E, int k, const RouteWs& ws, const int32_t* tier, const u64 (&bytes)[2][2],
-                         cudaStream_t st);
+void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
+                  uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st);
+// stable placement of every (t, j) entry; Xp != NULL also gathers x rows in permuted order
+void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
+                  cudaStream_t st);
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st);
 void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int k, int e_lo,
                         uint32_t* cnt_acc, u64* mass_acc, int32_t* err, cudaStream_t st);
@@ -189,8 +223,6 @@ struct GemmArgs {
     __nv_bfloat16* Y;
 };
 int gemm_bn_for(int T);
-void launch_gather(const __nv_bfloat16* x, const int32_t* perm, int rows, int k, int H, __nv_bfloat16* Xp,
-                   cudaStream_t st);
 void launch_gemm(int phase, int bn, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
 
 // k_ctrl.cu

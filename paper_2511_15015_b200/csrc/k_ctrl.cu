@@ -40,6 +40,8 @@ __device__ __forceinline__ int32_t bscan_excl(int32_t v, int32_t* tmp, int32_t* 
 
 // ------------------------------------------------------------------ a10 + a14
 __global__ void __launch_bounds__(CTRL_THREADS) k_fold(Ctrl c, int layer, u64 B_tot, double oma) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
     const int E = c.E;
     const i64 t_new = c.t[layer] + 1;
     __syncthreads();
@@ -71,6 +73,8 @@ __global__ void __launch_bounds__(CTRL_THREADS) k_plan(Ctrl c, int layer, int fi
     __shared__ int32_t freelist[CTRL_THREADS];
     __shared__ int32_t tmp[32];
     __shared__ int32_t any_pending;
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
     const int E = c.E, s = c.s, n_hot = c.n_hot;
     const int tid = threadIdx.x;
     const int base = layer * E, ob = layer * (E + s);
@@ -291,11 +295,11 @@ __global__ void __launch_bounds__(256) k_xfer(Ctrl c, int layer, XferArgs x, int
 }  // namespace
 
 void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st) {
-    k_fold<<<1, CTRL_THREADS, 0, st>>>(c, layer, B_tot, 1.0 - c.alpha);
+    dx_launch(k_fold, dim3(1), dim3(CTRL_THREADS), 0, st, g_dx_pdl, c, layer, B_tot, 1.0 - c.alpha);
 }
 
 void launch_plan(const Ctrl& c, int layer, int finalize, cudaStream_t st) {
-    k_plan<<<1, CTRL_THREADS, 0, st>>>(c, layer, finalize);
+    dx_launch(k_plan, dim3(1), dim3(CTRL_THREADS), 0, st, g_dx_pdl, c, layer, finalize);
 }
 
 void launch_manual(const Ctrl& c, int layer, const int2* cmds, int n, int32_t* status, cudaStream_t st) {

@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(256) k_ffn(ExpertArgs a, const __nv_bfloat16* 
                                              __nv_bfloat16* __restrict__ act, __nv_bfloat16* __restrict__ Y) {
     constexpr int RT = 2;
     extern __shared__ __align__(16) uint32_t smem[];
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
     const int K = PHASE == 0 ? a.H : a.I;
     const int rows_per_item = PHASE == 0 ? 16 : 32;
     const int nrb = (PHASE == 0 ? a.I : a.H) / rows_per_item;
@@ -240,7 +242,8 @@ void launch_phase(const ExpertArgs& a, const __nv_bfloat16* x, const float* gate
         attr = true;
     }
     if (max_items <= 0) return;
-    k_ffn<PHASE, NT><<<max_items, 256, sm, st>>>(a, x, gate, ws.perm, ws.off, ws.act_e, ws.n_act, act, Y);
+    dx_launch(k_ffn<PHASE, NT>, dim3(max_items), dim3(256), sm, st, g_dx_pdl, a, x, gate, (const int32_t*)ws.perm,
+              (const int32_t*)ws.off, (const int32_t*)ws.act_e, (const int32_t*)ws.n_act, act, Y);
 }
 
 }  // namespace

@@ -19,6 +19,8 @@ __global__ void __launch_bounds__(256) k_router(const __nv_bfloat16* __restrict_
                                                 const float* __restrict__ bias, int T, int E, int H,
                                                 float* __restrict__ logits) {
     extern __shared__ float xs[];   // [TT][H]
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
     const int t0 = blockIdx.y * TT;
     const int nt = min(TT, T - t0);
     for (int i = threadIdx.x; i < TT * H / 8; i += blockDim.x) {
@@ -36,12 +38,13 @@ __global__ void __launch_bounds__(256) k_router(const __nv_bfloat16* __restrict_
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (e >= E) return;
     const __nv_bfloat16* row = wr + (size_t)e * H;
     float acc[TT];
 #pragma unroll
     for (int t = 0; t < TT; ++t) acc[t] = 0.0f;
+#pragma unroll 8
     for (int k = lane * 8; k < H; k += 256) {
         uint4 v = __ldg(reinterpret_cast<const uint4*>(row + k));
         const uint16_t* b = reinterpret_cast<const uint16_t*>(&v);
@@ -75,14 +78,25 @@ __device__ __forceinline__ bool better(float a, int ea, float b, int eb) {
 // One warp per token (8 tokens per block), k rounds of (value desc, id asc) warp arg-max over NVT
 // logits per lane; per-block shared histograms merged into the layer's global accumulators with one
 // atomic per touched expert.
+template <typename Tv>
+__device__ Tv block_excl_scan(Tv v, Tv* tmp, Tv* total);
+__device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int32_t* __restrict__ base,
+                          int32_t* __restrict__ off, int32_t* __restrict__ act_e, int32_t* __restrict__ n_act,
+                          const RouteStats& rs);
+
 template <int NVT>
 __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits, int T, int E, int k,
                                                int e_lo, int e_cnt, int32_t* __restrict__ idx_out,
                                                float* __restrict__ gate_out, int32_t* __restrict__ hist,
-                                               uint32_t* __restrict__ cnt_acc, u64* __restrict__ mass_acc) {
+                                               uint32_t* __restrict__ cnt_acc, u64* __restrict__ mass_acc,
+                                               int32_t* __restrict__ base, int32_t* __restrict__ off,
+                                               int32_t* __restrict__ act_e, int32_t* __restrict__ n_act,
+                                               RouteStats rs, unsigned* __restrict__ done) {
     __shared__ uint32_t cnt_s[ROUTE_MAX_E];
     __shared__ u64 mass_s[ROUTE_MAX_E];
     for (int e = threadIdx.x; e < E; e += blockDim.x) { cnt_s[e] = 0; mass_s[e] = 0; }
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x * ROUTE_TOK_PER_BLK + warp;
@@ -148,6 +162,16 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
             atomicAdd(&mass_acc[le], mass_s[e]);
         }
     }
+    // the last block to finish runs the offset scan (a4) for the whole forward
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    scan_tail(hist, gridDim.x, E, base, off, act_e, n_act, rs);
+    if (threadIdx.x == 0) *done = 0;
 }
 
 // ------------------------------------------------------------------ a4: offsets + stable scatter
@@ -178,60 +202,86 @@ __device__ Tv block_excl_scan(Tv v, Tv* tmp /*[32]*/, Tv* total) {
     return before;
 }
 
-// single block of 512 threads: E <= 512
-__global__ void __launch_bounds__(512) k_scan(const int32_t* __restrict__ hist, int nblk, int E,
-                                              int32_t* __restrict__ base, int32_t* __restrict__ off,
-                                              int32_t* __restrict__ act_e, int32_t* __restrict__ n_act,
-                                              const int32_t* __restrict__ tier, u64 b00, u64 b01, u64 b10,
-                                              u64 b11, u64* __restrict__ stats) {
+// Offsets of every expert's row segment, per-route-block bases and the active-expert list.  Run by
+// the LAST route block to finish (threadfence + completion counter), so routing and its scan are one
+// launch.  256 threads, 2 experts per thread (E <= 512).
+__device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int32_t* __restrict__ base,
+                          int32_t* __restrict__ off, int32_t* __restrict__ act_e, int32_t* __restrict__ n_act,
+                          const RouteStats& rs) {
     __shared__ int32_t tmp[32];
-    __shared__ int32_t tot_s, na_s;
-    const int e = threadIdx.x;
-    int32_t tot = 0;
-    if (e < E)
-        for (int b = 0; b < nblk; ++b) tot += hist[(size_t)b * E + e];
-    int32_t total;
-    const int32_t o = block_excl_scan<int32_t>(e < E ? tot : 0, tmp, &total);
-    const int32_t a = block_excl_scan<int32_t>((e < E && tot > 0) ? 1 : 0, tmp, &na_s);
-    if (e < E) {
-        off[e] = o;
+    __shared__ int32_t total_s, na_s;
+    const int e0 = 2 * threadIdx.x, e1 = e0 + 1;
+    int32_t t0 = 0, t1 = 0;
+    for (int b = 0; b < nblk; ++b) {
+        if (e0 < E) t0 += __ldcg(hist + (size_t)b * E + e0);
+        if (e1 < E) t1 += __ldcg(hist + (size_t)b * E + e1);
+    }
+    const int32_t o = block_excl_scan<int32_t>(t0 + t1, tmp, &total_s);
+    const int32_t a = block_excl_scan<int32_t>((t0 > 0) + (t1 > 0), tmp, &na_s);
+    int32_t ai = a;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int e = h ? e1 : e0;
+        const int32_t tot = h ? t1 : t0;
+        if (e >= E) continue;
+        const int32_t oe = h ? o + t0 : o;
+        off[e] = oe;
         if (tot > 0) {
-            act_e[a] = e;
-            if (stats && tier) {          // algorithmic weight bytes of this forward (profiling)
-                const int ti = tier[e];
-                atomicAdd(&stats[0], ti ? b10 : b00);
-                atomicAdd(&stats[1], ti ? b11 : b01);
-                atomicAdd(&stats[2], 1ull);
+            act_e[ai++] = e;
+            if (rs.stats && rs.tier) {          // algorithmic weight bytes of this forward (profiling)
+                const int ti = rs.tier[e];
+                atomicAdd(&rs.stats[0], ti ? rs.b10 : rs.b00);
+                atomicAdd(&rs.stats[1], ti ? rs.b11 : rs.b01);
+                atomicAdd(&rs.stats[2], 1ull);
             }
         }
-        int32_t run = o;
+        int32_t run = oe;
         for (int b = 0; b < nblk; ++b) {
             base[(size_t)b * E + e] = run;
-            run += hist[(size_t)b * E + e];
+            run += __ldcg(hist + (size_t)b * E + e);
         }
     }
-    if (threadIdx.x == 0) { off[E] = total; *n_act = na_s; }
-    (void)tot_s;
+    if (threadIdx.x == 0) { off[E] = total_s; *n_act = na_s; }
 }
 
-// one thread per entry (t*k + j): position = base[block][e] + number of earlier entries of the same
-// expert inside its route block (<= 8k comparisons): the stable counting-sort order (t asc, j asc).
-__global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ idx, int T, int E, int k,
-                                                 const int32_t* __restrict__ base,
-                                                 int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= T * k) return;
-    const int b = (i / k) / ROUTE_TOK_PER_BLK;
-    const int e = idx[i];
-    int r = 0;
-    for (int q = b * ROUTE_TOK_PER_BLK * k; q < i; ++q) r += (idx[q] == e);
-    const int pos = base[(size_t)b * E + e] + r;
-    perm[pos] = i;
-    inv[i] = pos;
+// One block per entry (t*k + j): its row position = base[block][e] + number of earlier entries of the
+// same expert inside its route block (the stable counting-sort order: t asc, j asc); the block then
+// copies x[t] into Xp[pos] (the B operand of the gate/up GEMM) when Xp != NULL.
+__global__ void __launch_bounds__(128) k_place(const int32_t* __restrict__ idx, int T, int E, int k,
+                                               const int32_t* __restrict__ base, int32_t* __restrict__ perm,
+                                               int32_t* __restrict__ inv, const __nv_bfloat16* __restrict__ x,
+                                               int H, __nv_bfloat16* __restrict__ Xp) {
+    __shared__ int pos_s;
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int i = blockIdx.x;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int b = (i / k) / ROUTE_TOK_PER_BLK;
+        const int e = idx[i];
+        int r = 0;
+        for (int q = b * ROUTE_TOK_PER_BLK * k + lane; q < i; q += 32) r += (idx[q] == e);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (lane == 0) {
+            const int pos = base[(size_t)b * E + e] + r;
+            perm[pos] = i;
+            inv[i] = pos;
+            pos_s = pos;
+        }
+    }
+    if (!Xp) return;
+    __syncthreads();
+    const int pos = pos_s;
+    const __nv_bfloat16* src = x + (size_t)(i / k) * H;
+    for (int h = threadIdx.x * 8; h < H; h += blockDim.x * 8)
+        *reinterpret_cast<uint4*>(Xp + (size_t)pos * H + h) = *reinterpret_cast<const uint4*>(src + h);
 }
 
 // ------------------------------------------------------------------ a8: y_t = bf16(sum_j Y[t,j])
 __global__ void k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, __nv_bfloat16* __restrict__ y) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
     const int t = blockIdx.x;
     for (int h = threadIdx.x * 8; h < H; h += blockDim.x * 8) {
         float acc[8];
@@ -275,41 +325,46 @@ int route_blocks(int T) { return (T + ROUTE_TOK_PER_BLK - 1) / ROUTE_TOK_PER_BLK
 void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E,
                    int H, float* logits, cudaStream_t st) {
     if (T <= 0) return;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_router<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_router<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    // 4 warps (experts) per block: decode batches still spread the 4 KB router rows over >= 32 blocks
     if (T <= 4) {
-        dim3 grid((E + 7) / 8, (T + 3) / 4);
-        k_router<4><<<grid, 256, 4 * H * sizeof(float), st>>>(x, wr, bias, T, E, H, logits);
+        dim3 grid((E + 3) / 4, (T + 3) / 4);
+        dx_launch(k_router<4>, grid, dim3(128), 4 * H * sizeof(float), st, g_dx_pdl, x, wr, bias, T, E, H, logits);
     } else {
-        dim3 grid((E + 7) / 8, (T + 7) / 8);
-        size_t sm = 8 * H * sizeof(float);
-        static bool attr = false;
-        if (!attr) { cudaFuncSetAttribute(k_router<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); attr = true; }
-        k_router<8><<<grid, 256, sm, st>>>(x, wr, bias, T, E, H, logits);
+        dim3 grid((E + 3) / 4, (T + 7) / 8);
+        dx_launch(k_router<8>, grid, dim3(128), 8 * H * sizeof(float), st, g_dx_pdl, x, wr, bias, T, E, H, logits);
     }
 }
 
 void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
-                  uint32_t* cnt_acc, u64* mass_acc, cudaStream_t st) {
-    (void)e_lo;
+                  uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st) {
     if (T <= 0) return;
     const int nb = route_blocks(T), ec = cnt_acc ? E : 0;
-    if (E <= 128)      k_route<4><<<nb, 256, 0, st>>>(logits, T, E, k, e_lo, ec, ws.idx, ws.gate, ws.hist, cnt_acc, mass_acc);
-    else if (E <= 256) k_route<8><<<nb, 256, 0, st>>>(logits, T, E, k, e_lo, ec, ws.idx, ws.gate, ws.hist, cnt_acc, mass_acc);
-    else               k_route<16><<<nb, 256, 0, st>>>(logits, T, E, k, e_lo, ec, ws.idx, ws.gate, ws.hist, cnt_acc, mass_acc);
+    RouteStats rs{tier, bytes[0][0], bytes[0][1], bytes[1][0], bytes[1][1], ws.stats};
+#define DX_ROUTE_ARGS logits, T, E, k, e_lo, ec, ws.idx, ws.gate, ws.hist, cnt_acc, mass_acc, ws.base, ws.off, \
+                      ws.act_e, ws.n_act, rs, ws.done
+    if (E <= 128)      dx_launch(k_route<4>, dim3(nb), dim3(256), 0, st, g_dx_pdl, DX_ROUTE_ARGS);
+    else if (E <= 256) dx_launch(k_route<8>, dim3(nb), dim3(256), 0, st, g_dx_pdl, DX_ROUTE_ARGS);
+    else               dx_launch(k_route<16>, dim3(nb), dim3(256), 0, st, g_dx_pdl, DX_ROUTE_ARGS);
+#undef DX_ROUTE_ARGS
 }
 
-void launch_scan_scatter(int T, int E, int k, const RouteWs& ws, const int32_t* tier, const u64 (&bytes)[2][2],
-                         cudaStream_t st) {
+void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
+                  cudaStream_t st) {
     if (T <= 0) return;
-    const int nblk = route_blocks(T);
-    k_scan<<<1, 512, 0, st>>>(ws.hist, nblk, E, ws.base, ws.off, ws.act_e, ws.n_act, tier, bytes[0][0],
-                              bytes[0][1], bytes[1][0], bytes[1][1], ws.stats);
-    k_scatter<<<(T * k + 255) / 256, 256, 0, st>>>(ws.idx, T, E, k, ws.base, ws.perm, ws.inv);
+    dx_launch(k_place, dim3(T * k), dim3(128), 0, st, g_dx_pdl, (const int32_t*)ws.idx, T, E, k,
+              (const int32_t*)ws.base, ws.perm, ws.inv, x, H, Xp);
 }
 
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st) {
     if (T <= 0) return;
     int threads = H / 8 < 256 ? H / 8 : 256;
-    k_combine<<<T, threads, 0, st>>>(Y, k, H, y);
+    dx_launch(k_combine, dim3(T), dim3(threads), 0, st, g_dx_pdl, Y, k, H, y);
 }
 
 void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int k, int e_lo,
