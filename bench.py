@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--router-scale", type=float, default=3.0)
+    ap.add_argument("--prefill-tokens", type=int, default=4096)
+    ap.add_argument("--prefill-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -178,7 +180,7 @@ def run_ours(a, rank, world, local_rank):
     cfg.expert_budget_bytes = c["budget"] * L // C2["L"]
     cfg.n_spare, cfg.ema_alpha = c["s"], c["alpha"]
     cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = c["Tp"], c["W"], c["dwell"], c["lag"]
-    cfg.max_tokens, cfg.ep_rank, cfg.ep_size = max(B, 64), 0, 1
+    cfg.max_tokens, cfg.ep_rank, cfg.ep_size = max(B, 64, a.prefill_tokens), 0, 1
     stream = torch.cuda.current_stream()
     t0 = time.time()
     pool = dx.Pool(cfg, ptrs, stream)
@@ -303,13 +305,73 @@ def run_ours(a, rank, world, local_rank):
                   "fwd_ms_share": prof["fwd_ms"] / ms if ms > 0 else None,
                   "active_experts_per_layer": prof["active_experts"] / max(prof["forwards"], 1),
                   "weight_bytes_per_layer": (wb[0] + wb[1]) / max(prof["forwards"], 1),
+                  "route_ms_share": prof["route_ms"] / ms if ms > 0 else None,
+                  "switch": {"plans": prof["plans"], "promotions": prof["promotions"],
+                             "demotions": prof["demotions"], "publishes": prof["publishes"],
+                             "exposed_ms_total": prof["exposed_ms"],
+                             "exposed_frac_of_step_time": prof["exposed_ms"] / ms if ms > 0 else None,
+                             "xfer_ms_mean": prof["xfer_ms"] / max(prof["plans"], 1),
+                             "xfer_ms_max": prof["xfer_max_ms"]},
                   "setup_s": {"masters": t_gen, "pool_create": t_pool}},
     }
     clock = clk.summary()
     if clock:
         out["clocks"] = clock
+    if a.prefill_tokens > 0:
+        out["extra"]["prefill"] = prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream)
     pool.close()
     return out
+
+
+def prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream):
+    """C3: 4k-token prefill steps over the same stack and pool (drifting routing, the
+    controller keeps planning and transitioning).  Reports layer-tokens/s and the expert GEMMs'
+    tensor-pipe utilisation (FLOPs = 2*T*k*3*I*H per layer) against the measured bf16 peak."""
+    import torch
+    import synth
+    T = a.prefill_tokens
+    xs = [torch.from_numpy(synth.normal_bf16(a.seed, 900, i, 0, (T, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+          for i in range(2)]
+    y = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+
+    def pstep(x):
+        ep = step_counter[0] // c["drift"]
+        for l in range(L):
+            pool.dx_moe_forward(l, x, T, y, router_w=wr[l], router_bias=bias[l, min(ep, bias.shape[1] - 1)])
+            pool.dx_hotness_update(l)
+            pool.dx_plan_precision(l)
+        step_counter[0] += 1
+
+    for i in range(2):
+        pstep(xs[i % 2])
+    pool.dx_sync()
+    pool.dx_profile_read()
+    pool.dx_profile_enable(True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(a.prefill_steps):
+        pstep(xs[i % 2])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = pool.dx_profile_read()
+    pool.dx_profile_enable(False)
+    flops_layer = 2.0 * T * k * 3 * I * H
+    gemm_ms = prof["ffn_ms"][0] + prof["ffn_ms"][1]
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    peak_tf = float(peaks.get("bf16_tflops", 1590.0))
+    tf = flops_layer * prof["forwards"] / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    return {"workload": f"C3: {L}-layer stack, T={T} tokens per step, same pool/controller",
+            "value": T * L * a.prefill_steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / a.prefill_steps,
+            "steps": a.prefill_steps, "gemm_tflops": tf, "tensor_peak_tflops": peak_tf,
+            "tensor_frac": tf / peak_tf, "gemm_ms_share": gemm_ms / ms,
+            "weight_bytes_per_layer": sum(prof["weight_bytes"]) / max(prof["forwards"], 1)}
 
 
 # ---------------------------------------------------------------------------------------- oracle arm

@@ -123,6 +123,30 @@ dx_status dx_moe_forward(dx_pool pool, int32_t layer, const void* x_bf16, int32_
                          const void* router_w_bf16, const float* router_bias, const float* logits,
                          void* y_bf16, int32_t* topk_idx, float* topk_gate);
 
+/* ---------------------------------------------------------------- expert parallelism
+ * ep_size G > 1: GPU r owns experts [r*E/G, (r+1)*E/G) (its pool holds only those, master pointers
+ * [L][E/G]); tokens are data-parallel.  One layer is dispatch -> all-to-all -> owner FFN ->
+ * all-to-all -> combine.  The two all-to-alls are NCCL collectives issued by the caller (plumbing,
+ * torch.distributed.all_to_all_single on the compute stream); every step of the path is in these
+ * calls.  Hotness is counted on the owner from the received (expert, gate) rows, so counters and
+ * plans are identical to a single-GPU run on the same global batch. */
+
+/* Route the T local tokens over the GLOBAL experts (router mode or trace mode as dx_moe_forward) and
+ * build the send buffers, rows grouped by owner rank in (t asc, j asc) order:
+ *   send_rows  [T*k][H] bf16 device (x rows), send_meta [T*k] int2 device {local expert id at the owner,
+ *   gate bits (fp32)}, send_counts [G] int32 device (rows per owner).  No hotness counting here. */
+dx_status dx_ep_dispatch(dx_pool pool, int32_t layer, const void* x_bf16, int32_t T, const void* router_w_bf16,
+                         const float* router_bias, const float* logits, void* send_rows, void* send_meta,
+                         int32_t* send_counts, int32_t* topk_idx, float* topk_gate);
+/* Owner side: R received rows [R][H] bf16 with their meta [R] int2; y_rows[R][H] = gate * E_e(row) for
+ * the local expert e of each row (k = 1 routing given).  Accumulates the layer's hotness counters and
+ * adds tokens_global (the step's global token count, B_tot of R-H2) to the fold's denominator. */
+dx_status dx_moe_forward_routed(dx_pool pool, int32_t layer, const void* rows_bf16, int32_t R, const void* meta,
+                                void* y_rows_bf16, int64_t tokens_global);
+/* Source side: back_rows [T*k][H] bf16 are the owner results returned in dispatch order; y[T][H] =
+ * bf16(sum_j back_rows[row of (t, j)]) in rank order (a8).  T must equal the last dispatch's T. */
+dx_status dx_ep_combine(dx_pool pool, int32_t layer, const void* back_rows, int32_t T, void* y_bf16);
+
 /* Fold the counters accumulated since the last fold into the EMA scores (Eq. 2, PAPER.md:226,
  * with Alg. 1's passive decay, R-H2); step t += 1; publish transitions due at the new t (R-T1).
  * Asynchronous on the compute stream (waits on the side stream only when a publish is due). */
@@ -193,6 +217,14 @@ typedef struct {
     uint64_t weight_bytes[2];   /* algorithmic expert-weight bytes those kernels must read: every touched
                                    expert's gate+up (0) / down (1) codes+scales+zeros at its stable tier */
     uint64_t active_experts;    /* touched experts summed over forwards */
+    double   route_ms;          /* summed device time of router + top-k + placement */
+    double   exposed_ms;        /* compute-stream stall waiting for side-stream transitions at publish
+                                   (the exposed switch time, "never affects the forward") */
+    int64_t  publishes;         /* publish points seen */
+    double   xfer_ms;           /* summed side-stream duration of issued transitions (issue -> ready) */
+    double   xfer_max_ms;       /* longest single plan's transitions */
+    int64_t  plans;             /* plans whose transitions were issued */
+    int64_t  promotions, demotions; /* transitions those plans issued */
 } dx_profile_t;
 /* Enable/disable per-forward CUDA-event timing (weight-byte counters always run, on the device). */
 dx_status dx_profile_enable(dx_pool pool, int32_t enable);

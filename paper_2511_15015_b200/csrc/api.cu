@@ -5,6 +5,7 @@
 #include <cstring>
 #include <vector>
 #include <cmath>
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include "dx_common.cuh"
@@ -43,7 +44,11 @@ struct dx_pool_s {
     uint8_t* arena = nullptr;
     uint8_t* weights = nullptr;
     Ctrl ctrl;
-    RouteWs ws;
+    RouteWs ws;                             // routing of the rows this GPU's experts process
+    RouteWs ws_src{};                       // EP: routing of this GPU's own tokens over global experts
+    RouteWs ws_src_live{};                  // ws_src as used by the last dispatch (caller idx/gate)
+    size_t n_ent = 0;                       // workspace rows
+    int ep_T = 0;                           // tokens of the last dispatch (for the combine)
     __nv_bfloat16* act = nullptr;
     __nv_bfloat16* Y = nullptr;
     int32_t* err_flag = nullptr;
@@ -65,6 +70,8 @@ struct dx_pool_s {
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;       // 4 per forward: start, after routing, between FFN phases, end
     std::vector<cudaEvent_t> prof_free;
+    std::vector<cudaEvent_t> prof_wait_ev;  // pairs around the publish wait (exposed switch time)
+    std::vector<cudaEvent_t> prof_xfer_ev;  // pairs around side-stream transitions (switch latency)
     i64 prof_fwd = 0;
     int ffn_path = 0;                       // 0: tcgen05 grouped GEMM, 1: mma.sync decode kernel
     __nv_bfloat16* Xp = nullptr;            // x rows in permuted order (B operand of gate/up)
@@ -136,7 +143,8 @@ static dx_status build_maps(dx_pool p) {
     }
     for (int i = 0; i < 4; ++i) {
         const uint32_t bn = 32u << i;
-        const uint64_t rows = (uint64_t)T * k;
+        const uint64_t rows = (uint64_t)p->n_ent;
+        (void)T; (void)k;
         const uint64_t d0[2] = {(uint64_t)H, rows}, s0[1] = {(uint64_t)H * 2};
         const uint64_t d1[2] = {(uint64_t)I, rows}, s1[1] = {(uint64_t)I * 2};
         const uint32_t b[2] = {64, bn};
@@ -147,6 +155,17 @@ static dx_status build_maps(dx_pool p) {
         }
     }
     return DX_OK;
+}
+
+static cudaEvent_t prof_event(dx_pool p) {
+    if (p->prof_free.empty()) {
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    cudaEvent_t e = p->prof_free.back();
+    p->prof_free.pop_back();
+    return e;
 }
 
 static u64 phase_bytes(const SlotLayout& L, int H, int I, int g, int nmat) {
@@ -195,10 +214,10 @@ static dx_status validate(const dx_config* c) {
              "period >= 1, warmup >= 0, dwell >= 0, n_spare >= 0");
     DX_CHECK(c->publish_lag >= 1 && c->publish_lag < c->period, DX_ERR_INVALID_ARG, "1 <= publish_lag < period");
     DX_CHECK(c->max_tokens >= 1, DX_ERR_INVALID_ARG, "max_tokens >= 1");
-    DX_CHECK(c->ep_size == 1 && c->ep_rank == 0, DX_ERR_INVALID_ARG,
-             "expert parallelism (ep_size > 1) is not available in this build");
+    DX_CHECK(c->ep_size >= 1 && c->ep_rank >= 0 && c->ep_rank < c->ep_size && c->num_experts % c->ep_size == 0,
+             DX_ERR_INVALID_ARG, "ep_size must divide num_experts and 0 <= ep_rank < ep_size");
     DX_CHECK(c->num_experts <= 512 && c->num_experts + c->n_spare <= 1024, DX_ERR_INVALID_ARG,
-             "experts per GPU must be <= 512");
+             "num_experts must be <= 512");
     return DX_OK;
 }
 
@@ -236,15 +255,22 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
 
     // ---- the one device allocation: weights | controller | workspace | staging
     const int T = cfg->max_tokens, k = p->k, L = p->L;
-    const int nblk = route_blocks(T);
+    const int G = cfg->ep_size;
+    // entries (rows) one forward can see: T*k locally; an EP owner receives up to G*T*min(k, E_loc) rows
+    const size_t n_ent = G > 1 ? std::max((size_t)T * k, (size_t)G * T * std::min(k, E)) : (size_t)T * k;
+    p->n_ent = n_ent;
+    const int nblk = route_blocks((int)(G > 1 ? n_ent : (size_t)T));
     const size_t Ek = (size_t)E;
     size_t ctrl_bytes = 0;
     {
         const size_t LE = (size_t)L * Ek, LO = (size_t)L * (Ek + s);
         ctrl_bytes = LE * (4 + 4 + 4 + 8 + 4 + 8 + 8 + 4 + 4 + 8 + 16) + LO * 8 + L * (8 + 8 + 4 * 3) + 64 * 256;
     }
-    const size_t ws_bytes = (size_t)T * p->E * 4 + (size_t)T * k * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
-                            (size_t)(p->E + 1) * 8 + (size_t)T * k * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8;
+    size_t ws_bytes = (size_t)T * p->E * 4 + n_ent * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
+                      (size_t)(p->E + 1) * 8 + n_ent * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8;
+    if (G > 1)   // dispatch-side routing workspace (global experts, local tokens)
+        ws_bytes += (size_t)T * p->E * 4 + (size_t)T * k * 16 + (size_t)route_blocks(T) * p->E * 8 +
+                    (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
     const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
     const size_t total = (size_t)L * p->layer_bytes + ctrl_bytes + ws_bytes + stage_bytes + ptr_bytes + 4096;
@@ -277,24 +303,40 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     c.cap_lo = carve<int32_t>(q, L);
     c.cap_hi = carve<int32_t>(q, L);
     c.plan_n = carve<int32_t>(q, L);
+    c.tstats = carve<u64>(q, 2);
     c.E = E; c.s = s; c.n_hot = (int)n_hot; c.W = cfg->warmup_steps; c.Tp = cfg->period;
     c.dwell = cfg->dwell_min; c.lag = cfg->publish_lag; c.alpha = cfg->ema_alpha;
     RouteWs& w = p->ws;
     w.logits = carve<float>(q, (size_t)T * p->E);
-    w.idx = carve<int32_t>(q, (size_t)T * k);
-    w.gate = carve<float>(q, (size_t)T * k);
+    w.idx = carve<int32_t>(q, n_ent);
+    w.gate = carve<float>(q, n_ent);
     w.hist = carve<int32_t>(q, (size_t)nblk * p->E);
     w.base = carve<int32_t>(q, (size_t)nblk * p->E);
     w.off = carve<int32_t>(q, p->E + 1);
     w.act_e = carve<int32_t>(q, p->E);
     w.n_act = carve<int32_t>(q, 1);
-    w.perm = carve<int32_t>(q, (size_t)T * k);
-    w.inv = carve<int32_t>(q, (size_t)T * k);
+    w.perm = carve<int32_t>(q, n_ent);
+    w.inv = carve<int32_t>(q, n_ent);
     w.stats = carve<u64>(q, 4);
     w.done = carve<unsigned>(q, 1);
-    p->act = carve<__nv_bfloat16>(q, (size_t)T * k * p->I);
-    p->Y = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
-    p->Xp = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
+    if (G > 1) {
+        RouteWs& v = p->ws_src;
+        v.logits = carve<float>(q, (size_t)T * p->E);
+        v.idx = carve<int32_t>(q, (size_t)T * k);
+        v.gate = carve<float>(q, (size_t)T * k);
+        v.hist = carve<int32_t>(q, (size_t)route_blocks(T) * p->E);
+        v.base = carve<int32_t>(q, (size_t)route_blocks(T) * p->E);
+        v.off = carve<int32_t>(q, p->E + 1);
+        v.act_e = carve<int32_t>(q, p->E);
+        v.n_act = carve<int32_t>(q, 1);
+        v.perm = carve<int32_t>(q, (size_t)T * k);
+        v.inv = carve<int32_t>(q, (size_t)T * k);
+        v.stats = nullptr;
+        v.done = carve<unsigned>(q, 1);
+    }
+    p->act = carve<__nv_bfloat16>(q, n_ent * p->I);
+    p->Y = carve<__nv_bfloat16>(q, n_ent * p->H);
+    p->Xp = carve<__nv_bfloat16>(q, n_ent * p->H);
     p->err_flag = carve<int32_t>(q, 1);
     p->manual_cmds = carve<int2>(q, 1024);
     p->manual_status = carve<int32_t>(q, 1024);
@@ -387,6 +429,8 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
         DX_CUDA(cudaMemsetAsync(w.done, 0, 4, p->cs));
+        if (G > 1) DX_CUDA(cudaMemsetAsync(p->ws_src.done, 0, 4, p->cs));
+        DX_CUDA(cudaMemsetAsync(c.tstats, 0, 16, p->cs));
         DX_CUDA(cudaStreamSynchronize(p->cs));
     }
     for (int ti = 0; ti < 2; ++ti) {
@@ -473,19 +517,38 @@ extern "C" dx_status dx_profile_enable(dx_pool p, int32_t enable) {
 extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
     DX_CHECK(p && out, DX_ERR_INVALID_ARG, "null pool/out");
     DX_CUDA(cudaStreamSynchronize(p->cs));
+    DX_CUDA(cudaStreamSynchronize(p->ss));
     memset(out, 0, sizeof(*out));
     for (size_t i = 0; i + 3 < p->prof_ev.size(); i += 4) {
         float a = 0, b = 0, c = 0, d = 0;
         DX_CUDA(cudaEventElapsedTime(&a, p->prof_ev[i], p->prof_ev[i + 3]));
         DX_CUDA(cudaEventElapsedTime(&b, p->prof_ev[i + 1], p->prof_ev[i + 2]));
         DX_CUDA(cudaEventElapsedTime(&c, p->prof_ev[i + 2], p->prof_ev[i + 3]));
-        (void)d;
+        DX_CUDA(cudaEventElapsedTime(&d, p->prof_ev[i], p->prof_ev[i + 1]));
         out->fwd_ms += a;
         out->ffn_ms[0] += b;
         out->ffn_ms[1] += c;
+        out->route_ms += d;
+    }
+    for (size_t i = 0; i + 1 < p->prof_wait_ev.size(); i += 2) {
+        float a = 0;
+        DX_CUDA(cudaEventElapsedTime(&a, p->prof_wait_ev[i], p->prof_wait_ev[i + 1]));
+        out->exposed_ms += a;
+        out->publishes += 1;
+    }
+    for (size_t i = 0; i + 1 < p->prof_xfer_ev.size(); i += 2) {
+        float a = 0;
+        DX_CUDA(cudaEventElapsedTime(&a, p->prof_xfer_ev[i], p->prof_xfer_ev[i + 1]));
+        out->xfer_ms += a;
+        out->xfer_max_ms = a > out->xfer_max_ms ? a : out->xfer_max_ms;
+        out->plans += 1;
     }
     for (auto e : p->prof_ev) p->prof_free.push_back(e);
+    for (auto e : p->prof_wait_ev) p->prof_free.push_back(e);
+    for (auto e : p->prof_xfer_ev) p->prof_free.push_back(e);
     p->prof_ev.clear();
+    p->prof_wait_ev.clear();
+    p->prof_xfer_ev.clear();
     out->forwards = p->prof_fwd;
     p->prof_fwd = 0;
     u64 st[4];
@@ -494,8 +557,17 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
     out->weight_bytes[0] = st[0];
     out->weight_bytes[1] = st[1];
     out->active_experts = st[2];
+    u64 ts[2];
+    DX_CUDA(cudaMemcpy(ts, p->ctrl.tstats, sizeof(ts), cudaMemcpyDeviceToHost));
+    DX_CUDA(cudaMemset(p->ctrl.tstats, 0, sizeof(ts)));
+    out->promotions = (int64_t)ts[0];
+    out->demotions = (int64_t)ts[1];
     return DX_OK;
 }
+
+static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void* x, int T, int k, void* y,
+                            cudaEvent_t* ev);
+static void prof_begin(dx_pool p, cudaEvent_t* ev);
 
 #define CHECK_LAYER(p, layer)                                                                          \
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");                                                      \
@@ -510,21 +582,10 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
     DX_CHECK(x && y, DX_ERR_INVALID_ARG, "null x/y");
     DX_CHECK((router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG,
              "exactly one of router_w (router mode) and logits (trace mode) must be given");
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (p->profiling) {
-        for (int i = 0; i < 4; ++i) {
-            if (p->prof_free.empty()) {
-                cudaEvent_t e;
-                DX_CUDA(cudaEventCreate(&e));
-                p->prof_free.push_back(e);
-            }
-            ev[i] = p->prof_free.back();
-            p->prof_free.pop_back();
-            p->prof_ev.push_back(ev[i]);
-        }
-        DX_CUDA(cudaEventRecord(ev[0], p->cs));
-        p->prof_fwd += 1;
-    }
+    DX_CHECK(p->cfg.ep_size == 1, DX_ERR_INVALID_ARG,
+             "ep_size > 1: use dx_ep_dispatch / dx_moe_forward_routed / dx_ep_combine");
+    cudaEvent_t ev[4];
+    prof_begin(p, ev);
     RouteWs ws = p->ws;
     if (topk_idx) ws.idx = topk_idx;
     if (topk_gate) ws.gate = topk_gate;
@@ -540,6 +601,19 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
     launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->ctrl.tier + base,
                  p->wbytes, p->cs);
     launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
+    p->launches += 2;
+    dx_status st = expert_ffn(p, layer, ws, x, T, p->k, y, ev);
+    if (st != DX_OK) return st;
+    p->pend_tokens[layer] += (u64)T;
+    return DX_OK;
+}
+
+// a6-a8 on rows already routed and placed in `ws`: grouped expert GEMMs over the slot pool, then the
+// weighted combine of k rows per token into y (k = 1: the rows themselves, EP owner side).
+static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void* x, int T, int k, void* y,
+                            cudaEvent_t* ev) {
+    const size_t base = (size_t)layer * p->E_loc;
+    const int E = p->E_loc;
     ExpertArgs a;
     a.arena_layer = p->weights + (size_t)layer * p->layer_bytes;
     a.tier = p->ctrl.tier + base;
@@ -547,20 +621,21 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
     a.hi_base = p->hi_base;
     a.hi = p->hi;
     a.lo = p->lo;
-    a.H = p->H; a.I = p->I; a.g = p->g; a.k = p->k;
+    a.H = p->H; a.I = p->I; a.g = p->g; a.k = k;
     if (ev[1]) DX_CUDA(cudaEventRecord(ev[1], p->cs));
+    const int max_act = T * k < E ? T * k : E;
     if (p->ffn_path == 1) {
-        launch_expert_ffn(a, (const __nv_bfloat16*)x, ws.gate, ws, T, p->E, p->act, p->Y, p->cs, ev[2]);
+        launch_expert_ffn(a, (const __nv_bfloat16*)x, ws.gate, ws, T, E, p->act, p->Y, p->cs, ev[2]);
     } else {
-        // tcgen05 grouped GEMMs (k_gemm.cu): gather x rows in permuted order, gate/up + SwiGLU, down
+        // tcgen05 grouped GEMMs (k_gemm.cu) over the rows placed in Xp: gate/up + SwiGLU, then down.
+        // m_e <= T for top-k routing; the owner side (k = 1) sees m_e <= T rows as well.
         const int bn = gemm_bn_for(T);
         int bi = 0;
         while ((32 << bi) < bn) ++bi;
-        const int max_act = T * p->k < p->E ? T * p->k : p->E;
         GemmArgs ga;
         ga.layer = a.arena_layer; ga.hi_base = p->hi_base; ga.hi = p->hi; ga.lo = p->lo;
         ga.tier = a.tier; ga.slot = a.slot; ga.off = ws.off; ga.act_e = ws.act_e; ga.n_act = ws.n_act;
-        ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = p->k;
+        ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = k;
         ga.act = p->act; ga.Y = p->Y;
         GemmMaps gm = p->gmaps[layer];
         gm.xb = p->xb0[bi];
@@ -570,11 +645,90 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
         launch_gemm(1, bn, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
     }
     if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));
-    launch_combine(p->Y, T, p->k, p->H, (__nv_bfloat16*)y, p->cs);
-    p->launches += 5;
-    p->pend_tokens[layer] += (u64)T;
+    launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs);
+    p->launches += 3;
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+static void prof_begin(dx_pool p, cudaEvent_t* ev) {
+    ev[0] = ev[1] = ev[2] = ev[3] = nullptr;
+    if (!p->profiling) return;
+    for (int i = 0; i < 4; ++i) {
+        ev[i] = prof_event(p);
+        p->prof_ev.push_back(ev[i]);
+    }
+    cudaEventRecord(ev[0], p->cs);
+    p->prof_fwd += 1;
+}
+
+// ---------------------------------------------------------------- expert parallelism (a15)
+extern "C" dx_status dx_ep_dispatch(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
+                                    const float* router_bias, const float* logits, void* send_rows, void* send_meta,
+                                    int32_t* send_counts, int32_t* topk_idx, float* topk_gate) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(p->cfg.ep_size > 1, DX_ERR_INVALID_ARG, "dx_ep_dispatch needs ep_size > 1 (use dx_moe_forward)");
+    DX_CHECK(T >= 0 && T <= p->cfg.max_tokens, DX_ERR_RANGE, "T=%d outside [0, max_tokens]", T);
+    DX_CHECK((router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG, "exactly one of router_w / logits");
+    DX_CHECK(send_rows && send_meta && send_counts && (T == 0 || x), DX_ERR_INVALID_ARG, "null buffer");
+    p->ep_T = T;
+    if (T == 0) {
+        DX_CUDA(cudaMemsetAsync(send_counts, 0, sizeof(int32_t) * p->cfg.ep_size, p->cs));
+        return DX_OK;
+    }
+    RouteWs ws = p->ws_src;
+    if (topk_idx) ws.idx = topk_idx;
+    if (topk_gate) ws.gate = topk_gate;
+    p->ws_src_live = ws;
+    const float* lg = logits;
+    if (router_w) {
+        launch_router((const __nv_bfloat16*)x, (const __nv_bfloat16*)router_w, router_bias, T, p->E, p->H, ws.logits,
+                      p->cs);
+        lg = ws.logits;
+        p->launches += 1;
+    }
+    const u64 nob[2][2] = {{0, 0}, {0, 0}};
+    // top-k over the GLOBAL experts; no hotness here (owners count what they receive)
+    launch_route(lg, T, p->E, p->k, 0, ws, nullptr, nullptr, nullptr, nob, p->cs);
+    // rows sorted by global expert = grouped by owner rank: the placement IS the send buffer
+    launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, (__nv_bfloat16*)send_rows, p->cs);
+    launch_ep_meta(ws, T * p->k, p->E_loc, p->cfg.ep_size, (int2*)send_meta, send_counts, p->cs);
+    p->launches += 3;
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "dispatch launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+extern "C" dx_status dx_moe_forward_routed(dx_pool p, int32_t layer, const void* rows, int32_t R, const void* meta,
+                                           void* y_rows, int64_t tokens_global) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(R >= 0 && (size_t)R <= p->n_ent, DX_ERR_RANGE, "R=%d exceeds the workspace (%zu rows)", R, p->n_ent);
+    DX_CHECK(tokens_global >= 0, DX_ERR_INVALID_ARG, "tokens_global < 0");
+    p->pend_tokens[layer] += (u64)tokens_global;
+    if (R == 0) return DX_OK;
+    DX_CHECK(rows && meta && y_rows, DX_ERR_INVALID_ARG, "null buffer");
+    cudaEvent_t ev[4];
+    prof_begin(p, ev);
+    const size_t base = (size_t)layer * p->E_loc;
+    DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
+    launch_route_given((const int2*)meta, R, p->E_loc, p->ws, p->ctrl.cnt + base, p->ctrl.mass + base,
+                       p->ctrl.tier + base, p->wbytes, p->err_flag, p->cs);
+    launch_place(R, p->E_loc, 1, p->ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
+    p->launches += 2;
+    return expert_ffn(p, layer, p->ws, rows, R, 1, y_rows, ev);
+}
+
+extern "C" dx_status dx_ep_combine(dx_pool p, int32_t layer, const void* back_rows, int32_t T, void* y) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(p->cfg.ep_size > 1, DX_ERR_INVALID_ARG, "dx_ep_combine needs ep_size > 1");
+    DX_CHECK(T == p->ep_T, DX_ERR_INVALID_ARG, "T=%d does not match the last dispatch (%d)", T, p->ep_T);
+    if (T == 0) return DX_OK;
+    DX_CHECK(back_rows && y, DX_ERR_INVALID_ARG, "null buffer");
+    launch_combine((const __nv_bfloat16*)back_rows, T, p->k, p->H, (__nv_bfloat16*)y, p->cs, p->ws_src_live.inv);
+    p->launches += 1;
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "combine launch failed: %s", cudaGetErrorString(ce));
     return DX_OK;
 }
 
@@ -584,7 +738,16 @@ static dx_status fold(dx_pool p, int layer) {
     const i64 t_new = p->t[layer] + 1;
     if (p->publish_at[layer] == t_new) {
         // exposed switch time, if any, is spent here: registration waits for the side stream
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (p->profiling) {
+            e0 = prof_event(p);
+            e1 = prof_event(p);
+            p->prof_wait_ev.push_back(e0);
+            p->prof_wait_ev.push_back(e1);
+            DX_CUDA(cudaEventRecord(e0, p->cs));
+        }
         DX_CUDA(cudaStreamWaitEvent(p->cs, p->ev_side[layer], 0));
+        if (e1) DX_CUDA(cudaEventRecord(e1, p->cs));
         p->publish_at[layer] = -1;
     }
     launch_fold(p->ctrl, layer, B, p->cs);
@@ -671,7 +834,18 @@ extern "C" dx_status dx_plan_precision(dx_pool p, int32_t layer, dx_plan* out) {
     launch_plan(p->ctrl, layer, 0, p->cs);
     DX_CUDA(cudaEventRecord(p->ev_plan, p->cs));
     DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_plan, 0));
+    cudaEvent_t x0 = nullptr;
+    if (p->profiling) {
+        x0 = prof_event(p);
+        p->prof_xfer_ev.push_back(x0);
+        DX_CUDA(cudaEventRecord(x0, p->ss));
+    }
     launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 0, p->ss);
+    if (x0) {
+        cudaEvent_t x1 = prof_event(p);
+        p->prof_xfer_ev.push_back(x1);
+        DX_CUDA(cudaEventRecord(x1, p->ss));
+    }
     DX_CUDA(cudaEventRecord(p->ev_side[layer], p->ss));
     p->launches += 2;
     p->publish_at[layer] = t + c.publish_lag;

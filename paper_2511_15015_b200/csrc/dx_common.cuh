@@ -76,6 +76,7 @@ struct Ctrl {
     int32_t* cap_hi;       // [L]
     int32_t* plan_n;       // [L]
     int4* plan_cmd;        // [L * E] (expert, dir, dst, src)
+    u64* tstats;           // [2] promotions, demotions issued (profiling counters)
     int E, s, n_hot, W, Tp, dwell, lag;
     double alpha;
 };
@@ -183,7 +184,13 @@ void launch_route(const float* logits, int T, int E, int k, int e_lo, const Rout
 // stable placement of every (t, j) entry; Xp != NULL also gathers x rows in permuted order
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
                   cudaStream_t st);
-void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st);
+void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st,
+                    const int32_t* inv = nullptr);
+// expert parallelism: owner-side routing from received (local expert, gate) rows (k = 1), and the
+// source-side dispatch metadata / per-owner counts
+void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
+                        const int32_t* tier, const u64 (&bytes)[2][2], int32_t* err, cudaStream_t st);
+void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, cudaStream_t st);
 void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int k, int e_lo,
                         uint32_t* cnt_acc, u64* mass_acc, int32_t* err, cudaStream_t st);
 

@@ -191,7 +191,10 @@ __global__ void __launch_bounds__(CTRL_THREADS) k_plan(Ctrl c, int layer, int fi
         plan[nd + ppos] = make_int4(er, 1, d, c.slot[i]);
         c.pend_dir[i] = 1; c.pend_dst[i] = d; c.pend_at[i] = t + c.lag; c.last[i] = t;
     }
-    if (tid == 0) c.plan_n[layer] = nd + np;
+    if (tid == 0) {
+        c.plan_n[layer] = nd + np;
+        if (c.tstats) { c.tstats[0] += (u64)np; c.tstats[1] += (u64)nd; }
+    }
 }
 
 // ------------------------------------------------------------------ manual commands (host-chosen)

@@ -6,9 +6,10 @@
 // tokens of one expert are N (B, K-major), the accumulator D[128 x BN] fp32 lives in TMEM (two
 // buffers, so the epilogue of one work item overlaps the MMAs of the next).
 // Persistent CTAs (one per SM) walk the work items (expert, 128-row block) round-robin.
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + single-thread MMA issuer,
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM owner + single-thread MMA issuer,
 // warps 2-5 = dequant transform (quantised tiers: raw codes TMA'd to smem -> bf16 SW128 A tile,
-// exactly bf16_rn((q-z)s), R-Q1) and epilogue (tcgen05.ld -> SwiGLU / gate scale -> global).
+// exactly bf16_rn((q-z)s), R-Q1), warps 6-9 = epilogue (tcgen05.ld -> SwiGLU / gate scale -> global),
+// so the epilogue of one item overlaps the mainloop of the next.
 // bf16 tiers are TMA'd straight into the swizzled A tile.  An mbarrier ring of 3-8 stages overlaps
 // TMA, dequant and MMA.  Gate/up tiles interleave 16 gate and 16 up rows per 32-lane TMEM quarter so
 // the SwiGLU pairs meet in one warp (shfl_xor 16).
@@ -19,7 +20,7 @@ using namespace sm100;
 
 namespace {
 
-constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_THREADS = 320;
 constexpr int KCH = 64;                  // K elements per stage (128 B of bf16)
 
 template <int BN>
@@ -161,14 +162,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 }
             }
         }
-    } else {
-        // ------------------------------------------------ transform + epilogue (128 threads)
-        const int r = threadIdx.x - 64;                 // A tile row handled by this thread (transform)
-        const int q = warp & 3;                         // TMEM lane quarter of this warp (epilogue)
+    } else if (warp < 6) {
+        // ------------------------------------------------ dequant transform (128 threads, warps 2-5)
+        const int r = threadIdx.x - 64;                 // A tile row handled by this thread
         const int rows_total = PHASE == 0 ? 2 * a.I : a.H;
         const int mat = PHASE == 0 ? 0 : 2;
         const int G = K / a.g;
-        int it = 0, cc = 0;
+        int it = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
             const Item w = decode<PHASE>(a, item, nmb);
             int raw_row, mat_row;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             const uint16_t* scales = reinterpret_cast<const uint16_t*>(slot_base + L.scales_off + mat * L.scales_stride);
             const uint8_t* zeros = slot_base + L.zeros_off + mat * L.zeros_stride;
             const int nchunk = (w.m + BN - 1) / BN;
-            for (int c = 0; c < nchunk; ++c, ++cc) {
+            for (int c = 0; c < nchunk; ++c) {
                 if (w.bits == 16) {
                     // bf16 tier: A arrived by TMA; still consume the stage so that aready[] completes
                     // exactly once per stage use for every tier (keeps all phases in lock-step)
@@ -241,7 +241,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         mbar_arrive(&aready[st]);
                     }
                 }
-                // epilogue of chunk c
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (128 threads, warps 6-9)
+        const int q = warp & 3;                         // TMEM lane quarter this warp may access
+        int cc = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+            const Item w = decode<PHASE>(a, item, nmb);
+            const int nchunk = (w.m + BN - 1) / BN;
+            for (int c = 0; c < nchunk; ++c, ++cc) {
                 const int buf = cc & 1;
                 mbar_wait(&tfull[buf], (cc >> 1) & 1);
                 tc_fence_after();

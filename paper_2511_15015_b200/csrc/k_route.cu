@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(128) k_place(const int32_t* __restrict__ idx, 
 }
 
 // ------------------------------------------------------------------ a8: y_t = bf16(sum_j Y[t,j])
-__global__ void k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, __nv_bfloat16* __restrict__ y) {
+// inv == NULL: Y rows in entry order (t*k + j); else Y rows in permuted order, entry i at row inv[i]
+// (expert-parallel combine: the rows come back from their owners in dispatch order).
+__global__ void k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, __nv_bfloat16* __restrict__ y,
+                          const int32_t* __restrict__ inv) {
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
     const int t = blockIdx.x;
@@ -288,7 +291,8 @@ __global__ void k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, __n
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
         for (int j = 0; j < k; ++j) {
-            uint4 v = *reinterpret_cast<const uint4*>(Y + ((size_t)t * k + j) * H + h);
+            const size_t row = inv ? (size_t)inv[(size_t)t * k + j] : (size_t)t * k + j;
+            uint4 v = *reinterpret_cast<const uint4*>(Y + row * H + h);
             const uint16_t* b = reinterpret_cast<const uint16_t*>(&v);
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], dx_bf2f(b[i]));
@@ -298,6 +302,72 @@ __global__ void k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, __n
         for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16_rn(acc[i]);
         *reinterpret_cast<uint4*>(y + (size_t)t * H + h) = *reinterpret_cast<const uint4*>(o);
     }
+}
+
+// ------------------------------------------------------------------ expert parallelism (a15)
+// Owner side: rows arrive with (local expert, gate); k = 1 routing is given.  Per block of 8 rows:
+// copy idx/gate into the workspace, shared histograms, hotness counters (owner-side counting, SURVEY
+// §8(e)), then the last block runs the offset scan exactly as after top-k.
+__global__ void __launch_bounds__(256) k_route_given(const int2* __restrict__ meta, int R, int E,
+                                                     int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
+                                                     int32_t* __restrict__ hist, uint32_t* __restrict__ cnt_acc,
+                                                     u64* __restrict__ mass_acc, int32_t* __restrict__ base,
+                                                     int32_t* __restrict__ off, int32_t* __restrict__ act_e,
+                                                     int32_t* __restrict__ n_act, RouteStats rs,
+                                                     unsigned* __restrict__ done, int32_t* __restrict__ err) {
+    __shared__ uint32_t cnt_s[ROUTE_MAX_E];
+    __shared__ u64 mass_s[ROUTE_MAX_E];
+    for (int e = threadIdx.x; e < E; e += blockDim.x) { cnt_s[e] = 0; mass_s[e] = 0; }
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    __syncthreads();
+    const int r = blockIdx.x * ROUTE_TOK_PER_BLK + threadIdx.x;
+    if (threadIdx.x < ROUTE_TOK_PER_BLK && r < R) {
+        const int2 m = meta[r];
+        const float g = __int_as_float(m.y);
+        if (m.x < 0 || m.x >= E) {
+            atomicExch(err, 2);
+        } else {
+            idx_out[r] = m.x;
+            gate_out[r] = g;
+            atomicAdd(&cnt_s[m.x], 1u);
+            atomicAdd(&mass_s[m.x], (u64)rintf(__fmul_rn(g, 16777216.0f)));
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        hist[(size_t)blockIdx.x * E + e] = (int32_t)cnt_s[e];
+        if (cnt_s[e] && cnt_acc) {
+            atomicAdd(&cnt_acc[e], cnt_s[e]);
+            atomicAdd(&mass_acc[e], mass_s[e]);
+        }
+    }
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    scan_tail(hist, gridDim.x, E, base, off, act_e, n_act, rs);
+    if (threadIdx.x == 0) *done = 0;
+}
+
+// Source side after placement: metadata of every dispatched row (local expert id at its owner, gate
+// bits) and per-owner row counts (rows for owner o are contiguous because experts are partitioned
+// contiguously: [off[o*E_loc], off[(o+1)*E_loc]) ).
+__global__ void k_ep_meta(const int32_t* __restrict__ perm, const int32_t* __restrict__ idx,
+                          const float* __restrict__ gate, const int32_t* __restrict__ off, int n, int E_loc, int G,
+                          int2* __restrict__ meta, int32_t* __restrict__ counts) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos < n) {
+        const int ent = perm[pos];
+        const int e = idx[ent];
+        meta[pos] = make_int2(e % E_loc, __float_as_int(gate[ent]));
+    }
+    if (pos < G) counts[pos] = off[(pos + 1) * E_loc] - off[pos * E_loc];
 }
 
 // ------------------------------------------------------------------ trace-mode counters
@@ -361,10 +431,25 @@ void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x
               (const int32_t*)ws.base, ws.perm, ws.inv, x, H, Xp);
 }
 
-void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st) {
+void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st,
+                    const int32_t* inv) {
     if (T <= 0) return;
     int threads = H / 8 < 256 ? H / 8 : 256;
-    dx_launch(k_combine, dim3(T), dim3(threads), 0, st, g_dx_pdl, Y, k, H, y);
+    dx_launch(k_combine, dim3(T), dim3(threads), 0, st, g_dx_pdl, Y, k, H, y, inv);
+}
+
+void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
+                        const int32_t* tier, const u64 (&bytes)[2][2], int32_t* err, cudaStream_t st) {
+    if (R <= 0) return;
+    RouteStats rs{tier, bytes[0][0], bytes[0][1], bytes[1][0], bytes[1][1], ws.stats};
+    dx_launch(k_route_given, dim3(route_blocks(R)), dim3(256), 0, st, g_dx_pdl, meta, R, E, ws.idx, ws.gate, ws.hist,
+              cnt_acc, mass_acc, ws.base, ws.off, ws.act_e, ws.n_act, rs, ws.done, err);
+}
+
+void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, cudaStream_t st) {
+    const int thr = 256, nb = ((n > G ? n : G) + thr - 1) / thr;
+    dx_launch(k_ep_meta, dim3(nb > 0 ? nb : 1), dim3(thr), 0, st, g_dx_pdl, (const int32_t*)ws.perm,
+              (const int32_t*)ws.idx, (const float*)ws.gate, (const int32_t*)ws.off, n, E_loc, G, meta, counts);
 }
 
 void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int k, int e_lo,

@@ -64,7 +64,10 @@ class dx_cmd(ctypes.Structure):
 
 class dx_profile_t(ctypes.Structure):
     _fields_ = [("forwards", ctypes.c_int64), ("fwd_ms", ctypes.c_double), ("ffn_ms", ctypes.c_double * 2),
-                ("weight_bytes", ctypes.c_uint64 * 2), ("active_experts", ctypes.c_uint64)]
+                ("weight_bytes", ctypes.c_uint64 * 2), ("active_experts", ctypes.c_uint64),
+                ("route_ms", ctypes.c_double), ("exposed_ms", ctypes.c_double), ("publishes", ctypes.c_int64),
+                ("xfer_ms", ctypes.c_double), ("xfer_max_ms", ctypes.c_double), ("plans", ctypes.c_int64),
+                ("promotions", ctypes.c_int64), ("demotions", ctypes.c_int64)]
 
 
 class dx_plan(ctypes.Structure):
@@ -92,6 +95,9 @@ _SIG = {
     "dx_export_expert": [_vp, _i32, _i32, _vp, _i64, _vp],
     "dx_quantize": [_vp, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp],
     "dx_dequantize": [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp],
+    "dx_ep_dispatch": [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "dx_moe_forward_routed": [_vp, _i32, _vp, _i32, _vp, _vp, _i64],
+    "dx_ep_combine": [_vp, _i32, _vp, _i32, _vp],
     "dx_profile_enable": [_vp, _i32],
     "dx_set_ffn_path": [_vp, _i32],
     "dx_profile_read": [_vp, _P(dx_profile_t)],
@@ -195,6 +201,19 @@ class Pool:
         _check(_lib.dx_moe_forward(self.h, layer, _ptr(x), T, _ptr(router_w), _ptr(router_bias), _ptr(logits),
                                    _ptr(y), _ptr(topk_idx), _ptr(topk_gate)), "dx_moe_forward")
 
+    def dx_ep_dispatch(self, layer, x, T, send_rows, send_meta, send_counts, router_w=None, router_bias=None,
+                       logits=None, topk_idx=None, topk_gate=None):
+        _check(_lib.dx_ep_dispatch(self.h, layer, _ptr(x), T, _ptr(router_w), _ptr(router_bias), _ptr(logits),
+                                   _ptr(send_rows), _ptr(send_meta), _ptr(send_counts), _ptr(topk_idx),
+                                   _ptr(topk_gate)), "dx_ep_dispatch")
+
+    def dx_moe_forward_routed(self, layer, rows, R, meta, y_rows, tokens_global):
+        _check(_lib.dx_moe_forward_routed(self.h, layer, _ptr(rows), R, _ptr(meta), _ptr(y_rows), tokens_global),
+               "dx_moe_forward_routed")
+
+    def dx_ep_combine(self, layer, back_rows, T, y):
+        _check(_lib.dx_ep_combine(self.h, layer, _ptr(back_rows), T, _ptr(y)), "dx_ep_combine")
+
     def dx_hotness_update(self, layer):
         _check(_lib.dx_hotness_update(self.h, layer), "dx_hotness_update")
 
@@ -277,4 +296,6 @@ class Pool:
         _check(_lib.dx_profile_read(self.h, ctypes.byref(pr)), "dx_profile_read")
         return dict(forwards=pr.forwards, fwd_ms=pr.fwd_ms, ffn_ms=[pr.ffn_ms[0], pr.ffn_ms[1]],
                     weight_bytes=[int(pr.weight_bytes[0]), int(pr.weight_bytes[1])],
-                    active_experts=int(pr.active_experts))
+                    active_experts=int(pr.active_experts), route_ms=pr.route_ms, exposed_ms=pr.exposed_ms,
+                    publishes=pr.publishes, xfer_ms=pr.xfer_ms, xfer_max_ms=pr.xfer_max_ms, plans=pr.plans,
+                    promotions=pr.promotions, demotions=pr.demotions)

@@ -1,0 +1,82 @@
+"""Expert parallelism on one GPU: G pools (ep_rank r of ep_size G) in one process, the all-to-all done by
+tensor copies (paper_2511_15015_b200.ep.ep_forward_local), against the oracle and against the G = 1 path.
+
+Bars: owner-side counters and EMA scores bit-exact to the oracle over the GLOBAL batch;
+y within 2e-2 of the oracle; while every expert is LOW (warm-up) y is bitwise equal to the single-pool
+dx_moe_forward of the same global batch.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from dxtest import Masters, bf16_dev, budget_for, make_cfg, rel_err, to_u16
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2511_15015_b200 import dx as _dx
+    return _dx
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_ep_local_matches_oracle_and_single_gpu(dx, G):
+    from paper_2511_15015_b200 import ep
+    E, k, H, I, g, T, W = 16, 4, 256, 128, 64, 24, 3
+    e_loc = E // G
+    n_hot_loc = max(1, e_loc // 4)
+    m = Masters(5, 1, E, H, I)
+    ptrs = m.ptrs()
+    pools, bufs = [], []
+    for r in range(G):
+        cfg = make_cfg(dx, 1, E, k, H, I, g, 16, 4, budget_for(e_loc, H, I, g, 16, 4, n_hot_loc, 1), 1, 0.9, 2, W,
+                       2, 1, T)
+        cfg.ep_rank, cfg.ep_size = r, G
+        pools.append(dx.Pool(cfg, ptrs[r * e_loc:(r + 1) * e_loc], torch.cuda.current_stream()))
+        bufs.append(ep.EPBuffers(T, k, H, G, e_loc, "cuda"))
+    cfg1 = make_cfg(dx, 1, E, k, H, I, g, 16, 4, budget_for(E, H, I, g, 16, 4, G * n_hot_loc, 1), 1, 0.9, 2, W, 2, 1,
+                    G * T)
+    single = dx.Pool(cfg1, ptrs, torch.cuda.current_stream())
+    ctrls = [oracle.Controller(e_loc, pools[r].info.n_hot, 1, 0.9, 2, W, 2, 1) for r in range(G)]
+    ys = [torch.zeros(T, H, dtype=torch.bfloat16, device="cuda") for _ in range(G)]
+    y1 = torch.zeros(G * T, H, dtype=torch.bfloat16, device="cuda")
+    for step in range(8):
+        lgs = [synth.trace_logits(5, 0, step * G + r, T, E, 1.2) for r in range(G)]
+        xs = [synth.normal_bf16(5, 1, step * G + r, 0, (T, H)) for r in range(G)]
+        tabs = [pools[r].dx_get_table(0) for r in range(G)]
+        ep.ep_forward_local(pools, bufs, 0, [bf16_dev(x) for x in xs], [T] * G, ys,
+                            logits_list=[torch.from_numpy(lg).cuda() for lg in lgs])
+        lg_all, x_all = np.concatenate(lgs), np.concatenate(xs)
+        idx_o, gate_o = oracle.route(lg_all, k)
+        tier_of = {r * e_loc + e: bool(tabs[r]["tier"][e]) for r in range(G) for e in range(e_loc)}
+        Wt = {int(e): oracle.expert_tier(m.get(0, int(e)), H, I, g, 16, 4, tier_of[int(e)]) for e in np.unique(idx_o)}
+        _, y_o = oracle.moe_ffn(x_all, idx_o, gate_o, Wt, H, I, nthreads=8)
+        y_ep = np.concatenate([to_u16(y) for y in ys])
+        assert rel_err(y_ep, y_o) <= 2e-2, step
+        cnt_all, mass_all = oracle.counts(idx_o, gate_o, E)
+        for r in range(G):
+            hot = pools[r].dx_get_hotness(0)
+            assert np.array_equal(hot["cnt"], cnt_all[r * e_loc:(r + 1) * e_loc]), (step, r)
+            assert np.array_equal(hot["mass"], mass_all[r * e_loc:(r + 1) * e_loc]), (step, r)
+        if step < W:     # all LOW on both sides: EP is bitwise the single-GPU layer
+            single.dx_moe_forward(0, bf16_dev(x_all), G * T, y1, logits=torch.from_numpy(lg_all).cuda())
+            assert np.array_equal(to_u16(y1), y_ep), step
+            single.dx_hotness_update(0)
+        for r in range(G):
+            pools[r].dx_hotness_update(0)
+            pools[r].dx_plan_precision(0)
+            ctrls[r].fold(mass_all[r * e_loc:(r + 1) * e_loc], G * T)
+            ctrls[r].plan()
+            st = ctrls[r].state()
+            hot = pools[r].dx_get_hotness(0)
+            assert np.array_equal(hot["S"].view(np.uint64), st["S"].view(np.uint64)), (step, r)
+            tab = pools[r].dx_get_table(0)
+            assert np.array_equal(tab["tier"], st["tier"]) and np.array_equal(tab["slot"], st["slot"]), (step, r)
+    for p in pools:
+        p.close()
+    single.close()
