@@ -1,12 +1,12 @@
 #!/bin/bash
-# tests + bench (+ optional launch list) in one GPU call
+# tests + bench (+ optional launch list) in one GPU call; every stage under its own timeout
 python __graft_entry__.py > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
-timeout 1500 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/gpu_tests.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/gpu_tests.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
 tail -4 gpurun_out/gpu_tests.log
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
-cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo "bench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
 if [ "$1" == "ncu" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_' -s 20000 -c 1500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_' -s 20000 -c 1500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --prefill-tokens 0 > gpurun_out/ncu.log 2>&1
 python scripts/launch_summary.py gpurun_out/launches.csv
 fi
