@@ -6,9 +6,10 @@
 // tokens of one expert are N (B, K-major), the accumulator D[128 x BN] fp32 lives in TMEM (two
 // buffers, so the epilogue of one work item overlaps the MMAs of the next).
 // Persistent CTAs (one per SM) walk the work items (expert, 128-row block) round-robin.
-// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM owner + single-thread MMA issuer,
-// warps 2-5 = dequant transform (quantised tiers: raw codes TMA'd to smem -> bf16 SW128 A tile,
-// exactly bf16_rn((q-z)s), R-Q1), warps 6-9 = epilogue (tcgen05.ld -> SwiGLU / gate scale -> global),
+// Warp roles (448 threads): warp 0 = TMA producer, warp 1 = TMEM owner + single-thread MMA issuer,
+// warps 2-9 = dequant transform in two groups taking alternate stages (quantised tiers: raw codes
+// TMA'd to smem, dequantised exactly to bf16_rn((q-z)s) (R-Q1) and written straight into TMEM as the
+// A operand, lane = weight row), warps 10-13 = epilogue (tcgen05.ld -> SwiGLU / gate scale -> global),
 // so the epilogue of one item overlaps the mainloop of the next.
 // bf16 tiers are TMA'd straight into the swizzled A tile.  An mbarrier ring of 3-8 stages overlaps
 // TMA, dequant and MMA.  Gate/up tiles interleave 16 gate and 16 up rows per 32-lane TMEM quarter so
@@ -20,7 +21,7 @@ using namespace sm100;
 
 namespace {
 
-constexpr int GEMM_THREADS = 320;
+constexpr int GEMM_THREADS = 448;        // producer, MMA, 2 x 4 transform warps, 4 epilogue warps
 constexpr int KCH = 64;                  // K elements per stage (128 B of bf16)
 
 template <int BN>
@@ -30,8 +31,13 @@ struct GemmCfg {
     static constexpr int RAW_BYTES = 128 * 32;        // int4 worst case
     static constexpr int STAGE = A_BYTES + B_BYTES + RAW_BYTES;
     static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
-    static constexpr int TMEM_COLS = 2 * BN < 64 ? 64 : 2 * BN;   // two accumulator buffers
-    static constexpr int SMEM = 1024 + STAGES * STAGE + 1024;
+    // TMEM: ACC_BUFS accumulators of BN columns, then one 32-column A buffer per stage for the
+    // quantised tiers (dequantised bf16 A written straight into tensor memory: lane = weight row)
+    static constexpr int ACC_BUFS = BN <= 128 ? 2 : 1;
+    static constexpr int A_COL0 = ACC_BUFS * BN;
+    static constexpr int TMEM_COLS = 512;
+    static_assert(A_COL0 + STAGES * 32 <= TMEM_COLS, "TMEM budget");
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 1024 + 8 * BN;
 };
 
 __device__ __forceinline__ uint32_t bf2_sub_mul(uint32_t v, uint32_t zz, uint32_t ss) {
@@ -72,6 +78,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     uint64_t* tfull = bars + 3 * C::STAGES;               // [2] accumulator ready
     uint64_t* tempty = tfull + 2;                         // [2] accumulator drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int32_t* ent_s = reinterpret_cast<int32_t*>(tmem_slot + 4);     // [BN] epilogue: entry ids
+    float* gate_s = reinterpret_cast<float*>(ent_s + BN);            // [BN] epilogue: gates
 
     const int K = PHASE == 0 ? a.H : a.I;
     const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
@@ -144,27 +152,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 const Item w = decode<PHASE>(a, item, nmb);
                 const int nchunk = (w.m + BN - 1) / BN;
                 for (int c = 0; c < nchunk; ++c, ++cc) {
-                    const int buf = cc & 1;
-                    mbar_wait(&tempty[buf], ((cc >> 1) & 1) ^ 1);
+                    const int buf = cc % C::ACC_BUFS;
+                    mbar_wait(&tempty[buf], ((cc / C::ACC_BUFS) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t d = tmem + buf * BN;
                     for (int kb = 0; kb < nk; ++kb, ++it) {
                         const int st = it % C::STAGES, ph = (it / C::STAGES) & 1;
                         mbar_wait(&aready[st], ph);          // every stage use: transform warps arrive
                         tc_fence_after();
-                        const uint32_t a0 = smem_u32(sA + st * C::A_BYTES), b0 = smem_u32(sB + st * C::B_BYTES);
+                        const uint32_t b0 = smem_u32(sB + st * C::B_BYTES);
+                        if (w.bits == 16) {                  // A: bf16 tile TMA'd into smem (SW128)
+                            const uint32_t a0 = smem_u32(sA + st * C::A_BYTES);
 #pragma unroll
-                        for (int s = 0; s < KCH / 16; ++s)
-                            mma_bf16(d, umma_desc_sw128(a0 + 32 * s), umma_desc_sw128(b0 + 32 * s), idesc, (kb | s) != 0);
+                            for (int s = 0; s < KCH / 16; ++s)
+                                mma_bf16(d, umma_desc_sw128(a0 + 32 * s), umma_desc_sw128(b0 + 32 * s), idesc,
+                                         (kb | s) != 0);
+                        } else {                             // A: dequantised into TMEM by the transform warps
+                            const uint32_t at = tmem + C::A_COL0 + 32 * st;
+#pragma unroll
+                            for (int s = 0; s < KCH / 16; ++s)
+                                mma_bf16_ts(d, at + 8 * s, umma_desc_sw128(b0 + 32 * s), idesc, (kb | s) != 0);
+                        }
                         mma_commit(&empty[st]);
                     }
                     mma_commit(&tfull[buf]);
                 }
             }
         }
-    } else if (warp < 6) {
-        // ------------------------------------------------ dequant transform (128 threads, warps 2-5)
-        const int r = threadIdx.x - 64;                 // A tile row handled by this thread
+    } else if (warp < 10) {
+        // ------------------------------------------------ dequant transform: two groups of 4 warps
+        // (warps 2-5, 6-9) take alternate stage uses, so two stages are dequantised concurrently
+        const int grp = (warp - 2) >> 2;
+        const int qa = warp & 3;                        // TMEM lane quarter this warp may write
+        const int r = 32 * qa + lane;                   // A tile row (= TMEM lane) handled by this thread
         const int rows_total = PHASE == 0 ? 2 * a.I : a.H;
         const int mat = PHASE == 0 ? 0 : 2;
         const int G = K / a.g;
@@ -191,12 +211,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                     // bf16 tier: A arrived by TMA; still consume the stage so that aready[] completes
                     // exactly once per stage use for every tier (keeps all phases in lock-step)
                     for (int kb = 0; kb < nk; ++kb, ++it) {
+                        if ((it & 1) != grp) continue;
                         const int st = it % C::STAGES, ph = (it / C::STAGES) & 1;
                         mbar_wait(&full[st], ph);
                         mbar_arrive(&aready[st]);
                     }
                 } else {
                     for (int kb = 0; kb < nk; ++kb, ++it) {
+                        if ((it & 1) != grp) continue;
                         const int st = it % C::STAGES, ph = (it / C::STAGES) & 1;
                         // scales/zeros first (global, independent of the stage) to overlap the wait
                         uint32_t zz[2] = {0x43004300u, 0x43004300u}, ss[2] = {0x3f803f80u, 0x3f803f80u};
@@ -213,7 +235,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         }
                         mbar_wait(&full[st], ph);
                         const uint8_t* raw = sR + st * C::RAW_BYTES + raw_row * (KCH * w.bits / 8);
-                        uint8_t* arow = sA + st * C::A_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
                         uint32_t wv[KCH / 2];                 // 32 bf16x2 words = 64 elements
                         if (w.bits == 4) {
                             const uint4 v0 = *reinterpret_cast<const uint4*>(raw);
@@ -233,29 +254,37 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                                 wv[b] = bf2_sub_mul((x & 0x3u) | ((x & 0xCu) << 14) | 0x43004300u, zz[b >> 4], ss[b >> 4]);
                             }
                         }
-#pragma unroll
-                        for (int ch = 0; ch < 8; ++ch)
-                            *reinterpret_cast<uint4*>(arow + ((ch ^ (r & 7)) << 4)) =
-                                make_uint4(wv[4 * ch], wv[4 * ch + 1], wv[4 * ch + 2], wv[4 * ch + 3]);
-                        fence_proxy_async_smem();
+                        // row r of the A tile -> TMEM lane r, columns [A_COL0 + 32 st, +32)
+                        tmem_st32(tmem + ((uint32_t)(32 * qa) << 16) + C::A_COL0 + 32 * st, wv);
+                        tmem_st_wait();
+                        tc_fence_before();
                         mbar_arrive(&aready[st]);
                     }
                 }
             }
         }
     } else {
-        // ------------------------------------------------ epilogue (128 threads, warps 6-9)
+        // ------------------------------------------------ epilogue (128 threads, warps 10-13)
         const int q = warp & 3;                         // TMEM lane quarter this warp may access
+        const int et = threadIdx.x - 320;               // 0..127
         int cc = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
             const Item w = decode<PHASE>(a, item, nmb);
             const int nchunk = (w.m + BN - 1) / BN;
             for (int c = 0; c < nchunk; ++c, ++cc) {
-                const int buf = cc & 1;
-                mbar_wait(&tfull[buf], (cc >> 1) & 1);
-                tc_fence_after();
+                const int buf = cc % C::ACC_BUFS;
                 const int n0 = c * BN;
                 const int nvalid = min(BN, w.m - n0);
+                if (PHASE == 1) {                       // entry ids and gates of this chunk's tokens -> smem
+                    for (int i = et; i < nvalid; i += 128) {
+                        const int ent = a.perm[w.r0 + n0 + i];
+                        ent_s[i] = ent;
+                        gate_s[i] = a.gate[ent];
+                    }
+                    named_bar(1, 128);
+                }
+                mbar_wait(&tfull[buf], (cc / C::ACC_BUFS) & 1);
+                tc_fence_after();
                 for (int col = 0; col < nvalid; col += 32) {
                     uint32_t v[32];
                     tmem_ld32(tmem + buf * BN + ((uint32_t)(32 * q) << 16) + col, v);
@@ -273,17 +302,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         }
                     } else {
                         const int h = w.mb * 128 + 32 * q + lane;
-#pragma unroll 4
+#pragma unroll 8
                         for (int j = 0; j < 32; ++j) {
                             if (col + j < nvalid && h < a.H) {
-                                const int ent = a.perm[w.r0 + n0 + col + j];
-                                a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(a.gate[ent] * __uint_as_float(v[j]));
+                                const int ent = ent_s[col + j];
+                                a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(gate_s[col + j] * __uint_as_float(v[j]));
                             }
                         }
                     }
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[buf]);
+                if (PHASE == 1) named_bar(1, 128);      // ent_s / gate_s reused by the next chunk
             }
         }
     }
@@ -319,8 +349,10 @@ void launch_bn(int bn, const GemmMaps& maps, const GemmArgs& a, int items, cudaS
 }  // namespace
 
 int gemm_bn_for(int T) {
+    // N tile: the whole expert in one chunk for decode; 128 (two TMEM accumulators, so the epilogue
+    // of one chunk overlaps the MMAs of the next) for prefill
     int bn = 32;
-    while (bn < T && bn < 256) bn *= 2;
+    while (bn < T && bn < 128) bn *= 2;
     return bn;
 }
 
