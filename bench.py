@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--router-scale", type=float, default=3.0)
+    ap.add_argument("--budget-gb", type=float, default=0.0, help="override the 24 GB expert budget (sweeps)")
+    ap.add_argument("--ffn-path", type=int, default=0, help="0 tcgen05 grouped GEMM, 1 mma.sync cross-check")
     ap.add_argument("--prefill-tokens", type=int, default=4096)
     ap.add_argument("--prefill-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -177,7 +179,8 @@ def run_ours(a, rank, world, local_rank):
     cfg = dx.dx_config()
     cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = L, E, k, H, I, g
     cfg.high_bits, cfg.low_bits = c["high"], c["low"]
-    cfg.expert_budget_bytes = c["budget"] * L // C2["L"]
+    budget = int(a.budget_gb * 1e9) if a.budget_gb > 0 else c["budget"]
+    cfg.expert_budget_bytes = budget * L // C2["L"]
     cfg.n_spare, cfg.ema_alpha = c["s"], c["alpha"]
     cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = c["Tp"], c["W"], c["dwell"], c["lag"]
     cfg.max_tokens, cfg.ep_rank, cfg.ep_size = max(B, 64, a.prefill_tokens), 0, 1
@@ -186,6 +189,8 @@ def run_ours(a, rank, world, local_rank):
     pool = dx.Pool(cfg, ptrs, stream)
     t_pool = time.time() - t0
     n_hot = pool.info.n_hot
+    if a.ffn_path:
+        pool.dx_set_ffn_path(a.ffn_path)
     # router weights per layer + Zipf bias per (layer, drift epoch) -> skewed, drifting routing
     wr = torch.empty(L, E, H, dtype=torch.bfloat16, device=dev)
     for l in range(L):

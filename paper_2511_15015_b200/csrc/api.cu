@@ -76,7 +76,7 @@ struct dx_pool_s {
     int ffn_path = 0;                       // 0: tcgen05 grouped GEMM, 1: mma.sync decode kernel
     __nv_bfloat16* Xp = nullptr;            // x rows in permuted order (B operand of gate/up)
     std::vector<GemmMaps> gmaps;            // per layer (weights); xb filled per launch
-    CUtensorMap xb0[4], xb1[4];             // B operand maps for BN = 32, 64, 128, 256
+    CUtensorMap xb0[4], xb1[4];             // B operand maps (Xp / act) for tiles of 16, 32, 64, 128 rows
 };
 
 // ---------------------------------------------------------------- TMA tensor maps (driver entry point)
@@ -112,7 +112,7 @@ static dx_status build_maps(dx_pool p) {
         if (p->hi.bits == 16) {
             const uint64_t d0[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
             const uint64_t s0[2] = {(uint64_t)H * 2, (uint64_t)p->hi.bytes};
-            const uint32_t b0[3] = {64, 16, 1};
+            const uint32_t b0[3] = {64, 64, 1};              // 64 gate rows, then the 64 matching up rows
             ok &= make_map(&g.a16_gu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, lb + p->hi_base, d0, s0, b0,
                            CU_TENSOR_MAP_SWIZZLE_128B);
             const uint64_t d1[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
@@ -142,7 +142,7 @@ static dx_status build_maps(dx_pool p) {
         if (!ok) { dx_set_error("tensor map encoding failed (layer %d)", l); return DX_ERR_CUDA; }
     }
     for (int i = 0; i < 4; ++i) {
-        const uint32_t bn = 32u << i;
+        const uint32_t bn = 16u << i;                       // B tile rows 16, 32, 64, 128
         const uint64_t rows = (uint64_t)p->n_ent;
         (void)T; (void)k;
         const uint64_t d0[2] = {(uint64_t)H, rows}, s0[1] = {(uint64_t)H * 2};
@@ -629,20 +629,18 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
     } else {
         // tcgen05 grouped GEMMs (k_gemm.cu) over the rows placed in Xp: gate/up + SwiGLU, then down.
         // m_e <= T for top-k routing; the owner side (k = 1) sees m_e <= T rows as well.
-        const int bn = gemm_bn_for(T);
-        int bi = 0;
-        while ((32 << bi) < bn) ++bi;
+        const bool dec = gemm_decode_cfg(T);
         GemmArgs ga;
         ga.layer = a.arena_layer; ga.hi_base = p->hi_base; ga.hi = p->hi; ga.lo = p->lo;
         ga.tier = a.tier; ga.slot = a.slot; ga.off = ws.off; ga.act_e = ws.act_e; ga.n_act = ws.n_act;
         ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = k;
         ga.act = p->act; ga.Y = p->Y;
         GemmMaps gm = p->gmaps[layer];
-        gm.xb = p->xb0[bi];
-        launch_gemm(0, bn, gm, ga, max_act * (p->I / 64), p->cs);
+        for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb0[i];
+        launch_gemm(0, dec, gm, ga, max_act * (p->I / 64), p->cs);
         if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
-        gm.xb = p->xb1[bi];
-        launch_gemm(1, bn, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
+        for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb1[i];
+        launch_gemm(1, dec, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
     }
     if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));
     launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs);

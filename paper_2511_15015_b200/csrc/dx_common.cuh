@@ -212,7 +212,7 @@ struct GemmMaps {
     CUtensorMap a16_gu, a16_dn;     // bf16 HIGH region: dims {K, rows, slots}, 128 B swizzle
     CUtensorMap ahi_gu, ahi_dn;     // raw codes of a quantised HIGH region
     CUtensorMap alo_gu, alo_dn;     // raw codes of the LOW region
-    CUtensorMap xb;                 // B operand rows [rows][K] bf16, box {64, BN}, 128 B swizzle
+    CUtensorMap xb[4];              // B operand rows [rows][K] bf16, boxes {64, 16/32/64/128}, 128 B swizzle
 };
 struct GemmArgs {
     const uint8_t* layer;
@@ -229,8 +229,8 @@ struct GemmArgs {
     __nv_bfloat16* act;
     __nv_bfloat16* Y;
 };
-int gemm_bn_for(int T);
-void launch_gemm(int phase, int bn, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
+bool gemm_decode_cfg(int T);
+void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
 
 // k_ctrl.cu
 void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st);
