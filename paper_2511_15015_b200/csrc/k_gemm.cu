@@ -222,28 +222,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             const uint16_t* scales = reinterpret_cast<const uint16_t*>(slot_base + L.scales_off + mat * L.scales_stride);
             const uint8_t* zeros = slot_base + L.zeros_off + mat * L.zeros_stride;
             const int rawc = 128 * KCH * w.bits / 8, rowb = KCH * w.bits / 8;
+            // this row's scales / zeros for the whole item, once (G <= 16: g = 128, K <= 2048), packed
+            // as (bf16 scale | bf16(128 + z) << 16); otherwise fetched per chunk
+            uint32_t sz[16];
+            const bool sz_reg = G <= 16 && w.bits != 16;
+            if (sz_reg) {
+#pragma unroll
+                for (int gi = 0; gi < 16; ++gi) {
+                    uint32_t v = 0x43003f80u;
+                    if (gi < G && mat_row < rows_total)
+                        v = (uint32_t)scales[(int64_t)mat_row * G + gi] | ((0x4300u + zeros[(int64_t)mat_row * G + gi]) << 16);
+                    sz[gi] = v;
+                }
+            }
             for (int n0 = 0; n0 < w.m; n0 += nb) {
                 for (int kb0 = 0; kb0 < nk; kb0 += ks, ++it) {
+                    const int st = it % STAGES, ph = (it / STAGES) & 1;
+                    // every transform thread observes every phase of full[] (no phase aliasing)
+                    mbar_wait(&full[st], ph);
                     if (w.bits == 16) continue;                   // bf16 stages need no transform
                     const int kc = min(ks, nk - kb0);
-                    const int st = it % STAGES, ph = (it / STAGES) & 1;
-                    bool waited = false;
                     for (int j = 0; j < kc; ++j, ++ac) {
                         if ((ac & 1) != grp) continue;
                         const int kb = kb0 + j;
-                        uint32_t zz[2] = {0x43004300u, 0x43004300u}, ss[2] = {0x3f803f80u, 0x3f803f80u};
-                        if (mat_row < rows_total) {
+                        uint32_t zz[2], ss[2];
 #pragma unroll
-                            for (int h2 = 0; h2 < 2; ++h2) {       // one or two groups per 64-element chunk
-                                const int gi = (kb * KCH + h2 * 32) / a.g;
-                                const uint32_t sb = scales[(int64_t)mat_row * G + gi];
-                                const uint32_t z = zeros[(int64_t)mat_row * G + gi];
-                                const uint32_t zb = __float_as_uint(128.0f + (float)z) >> 16;
-                                zz[h2] = zb | (zb << 16);
-                                ss[h2] = sb | (sb << 16);
+                        for (int h2 = 0; h2 < 2; ++h2) {           // one or two groups per 64-element chunk
+                            const int gi = (kb * KCH + h2 * 32) / a.g;
+                            uint32_t v = 0x43003f80u;
+                            if (sz_reg) {
+#pragma unroll
+                                for (int q2 = 0; q2 < 16; ++q2) if (q2 == gi) v = sz[q2];
+                            } else if (mat_row < rows_total) {
+                                v = (uint32_t)scales[(int64_t)mat_row * G + gi] |
+                                    ((0x4300u + zeros[(int64_t)mat_row * G + gi]) << 16);
                             }
+                            zz[h2] = (v >> 16) * 0x10001u;
+                            ss[h2] = (v & 0xFFFFu) * 0x10001u;
                         }
-                        if (!waited) { mbar_wait(&full[st], ph); waited = true; }
                         const int ab = ac % C::NA;
                         mbar_wait(&aempty[ab], ((ac / C::NA) & 1) ^ 1);
                         const uint32_t raw_addr = smem_u32(sS + st * STAGE_BYTES + j * rawc + r * rowb);
