@@ -635,6 +635,8 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         ga.tier = a.tier; ga.slot = a.slot; ga.off = ws.off; ga.act_e = ws.act_e; ga.n_act = ws.n_act;
         ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = k;
         ga.act = p->act; ga.Y = p->Y;
+        static const int dbg = [] { const char* s = getenv("DX_GEMM_DBG"); return s ? atoi(s) : 0; }();
+        ga.dbg = dbg;
         GemmMaps gm = p->gmaps[layer];
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb0[i];
         launch_gemm(0, dec, gm, ga, max_act * (p->I / 64), p->cs);
@@ -989,10 +991,16 @@ extern "C" dx_status dx_export_expert(dx_pool p, int32_t layer, int32_t e, void*
     if (Ls.bits == 16) {
         memcpy(o, img.data(), n3 * 2);
     } else {
-        const int per = 8 / Ls.bits, mask = (1 << Ls.bits) - 1;
+        // slots hold the pair-interleaved packing (dx_quant.cuh): un-interleave to canonical u8 codes
+        const int W = 32 / Ls.bits, mask = (1 << Ls.bits) - 1;
         for (int m = 0; m < 3; ++m) {
             const uint8_t* codes = img.data() + m * Ls.codes_stride;
-            for (i64 i = 0; i < n; ++i) o[m * n + i] = (codes[i / per] >> ((i % per) * Ls.bits)) & mask;
+            for (i64 i = 0; i < n; ++i) {
+                uint32_t word;
+                memcpy(&word, codes + (i / W) * 4, 4);
+                const int e = (int)(i % W), slot = (e & 1) ? W / 2 + e / 2 : e / 2;
+                o[m * n + i] = (word >> (Ls.bits * slot)) & mask;
+            }
             memcpy(o + n3 + m * (n / p->g) * 2, img.data() + Ls.scales_off + m * Ls.scales_stride, (n / p->g) * 2);
             memcpy(o + n3 + n3 / p->g * 2 + m * (n / p->g), img.data() + Ls.zeros_off + m * Ls.zeros_stride, n / p->g);
         }

@@ -228,6 +228,7 @@ struct GemmArgs {
     int H, I, g, k;
     __nv_bfloat16* act;
     __nv_bfloat16* Y;
+    int dbg;                        // performance experiments only (DX_GEMM_DBG): 1 skip dequant, 2 skip TMEM store
 };
 bool gemm_decode_cfg(int T);
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);

@@ -287,9 +287,10 @@ __global__ void __launch_bounds__(256) k_xfer(Ctrl c, int layer, XferArgs x, int
                 uint8_t* dc = ls + m * x.lo.codes_stride + row * (K * x.lo.bits / 8);
                 __nv_bfloat16* dsc = reinterpret_cast<__nv_bfloat16*>(ls + x.lo.scales_off + m * x.lo.scales_stride) + row * G + gi;
                 uint8_t* dz = ls + x.lo.zeros_off + m * x.lo.zeros_stride + row * G + gi;
-                if (g == 32)      { float wv[1]; dxq_fetch_group<1>(sc, x.hi.bits, ssc, sz, row, gi, K, g, lane, wv); dxq_quantize_group<1>(wv, x.lo.bits, gi, K, lane, dc, dsc, dz); }
-                else if (g == 64) { float wv[2]; dxq_fetch_group<2>(sc, x.hi.bits, ssc, sz, row, gi, K, g, lane, wv); dxq_quantize_group<2>(wv, x.lo.bits, gi, K, lane, dc, dsc, dz); }
-                else              { float wv[4]; dxq_fetch_group<4>(sc, x.hi.bits, ssc, sz, row, gi, K, g, lane, wv); dxq_quantize_group<4>(wv, x.lo.bits, gi, K, lane, dc, dsc, dz); }
+                // slots hold codes in the pair-interleaved packing (dx_quant.cuh) on both sides
+                if (g == 32)      { float wv[1]; dxq_fetch_group<1>(sc, x.hi.bits, ssc, sz, row, gi, K, g, lane, wv, true); dxq_quantize_group<1>(wv, x.lo.bits, gi, K, lane, dc, dsc, dz, true); }
+                else if (g == 64) { float wv[2]; dxq_fetch_group<2>(sc, x.hi.bits, ssc, sz, row, gi, K, g, lane, wv, true); dxq_quantize_group<2>(wv, x.lo.bits, gi, K, lane, dc, dsc, dz, true); }
+                else              { float wv[4]; dxq_fetch_group<4>(sc, x.hi.bits, ssc, sz, row, gi, K, g, lane, wv, true); dxq_quantize_group<4>(wv, x.lo.bits, gi, K, lane, dc, dsc, dz, true); }
             }
         }
     }

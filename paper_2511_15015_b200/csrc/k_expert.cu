@@ -71,13 +71,12 @@ __device__ __forceinline__ uint32_t slice_word(const RowSlice<BITS>& r, int w) {
     if constexpr (BITS == 16) {
         return r.raw[w];
     } else if constexpr (BITS == 4) {
-        const uint32_t x = r.raw[w >> 2] >> (8 * (w & 3));             // byte w: codes 2w, 2w+1
-        const uint32_t v = (x & 0xFu) | ((x & 0xF0u) << 12) | 0x43004300u;
-        return bf2_sub_mul(v, r.zz, r.ss);
+        // pair-interleaved slot packing (dx_quant.cuh): codes (2w, 2w+1) at bits 4j, 16+4j of word w/4
+        const uint32_t x = r.raw[w >> 2] >> (4 * (w & 3));
+        return bf2_sub_mul((x & 0x000F000Fu) | 0x43004300u, r.zz, r.ss);
     } else {
-        const uint32_t x = r.raw[0] >> (4 * w);                         // nibble w: codes 2w, 2w+1
-        const uint32_t v = (x & 0x3u) | ((x & 0xCu) << 14) | 0x43004300u;
-        return bf2_sub_mul(v, r.zz, r.ss);
+        const uint32_t x = r.raw[0] >> (2 * w);                         // bits 2w, 16+2w
+        return bf2_sub_mul((x & 0x00030003u) | 0x43004300u, r.zz, r.ss);
     }
 }
 

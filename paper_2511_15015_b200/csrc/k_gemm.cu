@@ -37,7 +37,7 @@ template <bool DEC>
 struct Cfg {
     static constexpr int NBMAX = DEC ? 64 : 128;
     static constexpr int NA = (512 - 2 * NBMAX) / 32;          // TMEM A buffers (32 columns each)
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + 2 * 128 * 17 * 4;
     __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : 128; }
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int32_t* ent_s = reinterpret_cast<int32_t*>(tmem_slot + 4);     // [128] epilogue: entry ids
     float* gate_s = reinterpret_cast<float*>(ent_s + 128);           // [128] epilogue: gates
+    uint32_t* sz_tab = reinterpret_cast<uint32_t*>(gate_s + 128);    // [2 groups][128 rows][17] scale|zero
 
     const int K = PHASE == 0 ? a.H : a.I;
     const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
@@ -224,13 +225,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             const int rawc = 128 * KCH * w.bits / 8, rowb = KCH * w.bits / 8;
             // this row's scales / zeros for the whole item, once (G <= 16: g = 128, K <= 2048), packed
             // as (bf16 scale | bf16(128 + z) << 16); otherwise fetched per chunk
-            uint32_t sz[16];
+            // thread-private row table in smem (only this thread writes and reads it)
+            uint32_t* sz = sz_tab + (grp * 128 + r) * 17;
             const bool sz_reg = G <= 16 && w.bits != 16;
             if (sz_reg) {
-#pragma unroll
-                for (int gi = 0; gi < 16; ++gi) {
+                for (int gi = 0; gi < G; ++gi) {
                     uint32_t v = 0x43003f80u;
-                    if (gi < G && mat_row < rows_total)
+                    if (mat_row < rows_total)
                         v = (uint32_t)scales[(int64_t)mat_row * G + gi] | ((0x4300u + zeros[(int64_t)mat_row * G + gi]) << 16);
                     sz[gi] = v;
                 }
@@ -251,8 +252,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                             const int gi = (kb * KCH + h2 * 32) / a.g;
                             uint32_t v = 0x43003f80u;
                             if (sz_reg) {
-#pragma unroll
-                                for (int q2 = 0; q2 < 16; ++q2) if (q2 == gi) v = sz[q2];
+                                v = sz[gi];
                             } else if (mat_row < rows_total) {
                                 v = (uint32_t)scales[(int64_t)mat_row * G + gi] |
                                     ((0x4300u + zeros[(int64_t)mat_row * G + gi]) << 16);
@@ -264,29 +264,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         mbar_wait(&aempty[ab], ((ac / C::NA) & 1) ^ 1);
                         const uint32_t raw_addr = smem_u32(sS + st * STAGE_BYTES + j * rawc + r * rowb);
                         uint32_t wv[KCH / 2];                      // 32 bf16x2 words = 64 elements
-                        if (w.bits == 4) {
+                        if (a.dbg == 1) {                          // perf experiment: no dequant
+#pragma unroll
+                            for (int b = 0; b < 32; ++b) wv[b] = zz[0] ^ b;
+                        } else if (w.bits == 4) {
                             uint32_t s0, s1, s2, s3, s4, s5, s6, s7;
                             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(raw_addr));
                             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s4), "=r"(s5), "=r"(s6), "=r"(s7) : "r"(raw_addr + 16));
                             const uint32_t src[8] = {s0, s1, s2, s3, s4, s5, s6, s7};
 #pragma unroll
-                            for (int b = 0; b < 32; ++b) {
-                                const uint32_t x = src[b >> 2] >> (8 * (b & 3));
-                                wv[b] = bf2_sub_mul((x & 0xFu) | ((x & 0xF0u) << 12) | 0x43004300u, zz[b >> 4], ss[b >> 4]);
+                            for (int b = 0; b < 32; ++b) {      // pair-interleaved: pair j at bits 4j, 16+4j
+                                const uint32_t x = src[b >> 2] >> (4 * (b & 3));
+                                wv[b] = bf2_sub_mul((x & 0x000F000Fu) | 0x43004300u, zz[b >> 4], ss[b >> 4]);
                             }
                         } else {
                             uint32_t s0, s1, s2, s3;
                             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(raw_addr));
                             const uint32_t src[4] = {s0, s1, s2, s3};
 #pragma unroll
-                            for (int b = 0; b < 32; ++b) {
-                                const uint32_t x = src[b >> 3] >> (4 * (b & 7));
-                                wv[b] = bf2_sub_mul((x & 0x3u) | ((x & 0xCu) << 14) | 0x43004300u, zz[b >> 4], ss[b >> 4]);
+                            for (int b = 0; b < 32; ++b) {      // pair-interleaved: pair j at bits 2j, 16+2j
+                                const uint32_t x = src[b >> 3] >> (2 * (b & 7));
+                                wv[b] = bf2_sub_mul((x & 0x00030003u) | 0x43004300u, zz[b >> 4], ss[b >> 4]);
                             }
                         }
                         tc_fence_after();
-                        tmem_st32(tmem_a + ((uint32_t)(32 * qa) << 16) + 32 * ab, wv);
-                        tmem_st_wait();
+                        if (a.dbg != 2) {                          // dbg 2: perf experiment, no TMEM store
+                            tmem_st32(tmem_a + ((uint32_t)(32 * qa) << 16) + 32 * ab, wv);
+                            tmem_st_wait();
+                        } else if (wv[lane] == 0x12345678u) {
+                            a.act[0] = __float2bfloat16_rn(0.0f);
+                        }
                         tc_fence_before();
                         mbar_arrive(&aready[ab]);
                     }
@@ -327,18 +334,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         named_bar(1, 128);
                         if (q < 2) {
                             const int f = w.mb * 64 + 32 * q + lane;
-                            for (int j = 0; j < 32 && col + j < nvalid; ++j) {
-                                const float gv = __uint_as_float(v[j]);
-                                const float uv = xch[j * 64 + 32 * q + lane];
-                                const float sg = gv / (1.0f + expf(-gv));
-                                a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {           // fully unrolled: v[] stays in registers
+                                if (col + j < nvalid) {
+                                    const float gv = __uint_as_float(v[j]);
+                                    const float uv = xch[j * 64 + 32 * q + lane];
+                                    const float sg = gv / (1.0f + __expf(-gv));
+                                    a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
+                                }
                             }
                         }
                         named_bar(1, 128);
                     } else {
                         const int h = w.mb * 128 + 32 * q + lane;
-#pragma unroll 8
-                        for (int j = 0; j < 32; ++j) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {           // fully unrolled: v[] stays in registers
                             if (col + j < nvalid && h < a.H) {
                                 const int ent = ent_s[col + j];
                                 a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(gate_s[col + j] * __uint_as_float(v[j]));
