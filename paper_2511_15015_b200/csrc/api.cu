@@ -77,6 +77,7 @@ struct dx_pool_s {
     __nv_bfloat16* Xp = nullptr;            // x rows in permuted order (B operand of gate/up)
     std::vector<GemmMaps> gmaps;            // per layer (weights); xb filled per launch
     CUtensorMap xb0[4], xb1[4];             // B operand maps (Xp / act) for tiles of 16, 32, 64, 128 rows
+    CUtensorMap xk0[3], xk1[3];             // 3-D B maps (Xp / act): several K chunks per box (decode int)
 };
 
 // ---------------------------------------------------------------- TMA tensor maps (driver entry point)
@@ -110,10 +111,10 @@ static dx_status build_maps(dx_pool p) {
         const uint8_t* lb = p->weights + (size_t)l * p->layer_bytes;
         bool ok = true;
         if (p->hi.bits == 16) {
-            const uint64_t d0[3] = {(uint64_t)H, (uint64_t)2 * I, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
-            const uint64_t s0[2] = {(uint64_t)H * 2, (uint64_t)p->hi.bytes};
-            const uint32_t b0[3] = {64, 64, 1};              // 64 gate rows, then the 64 matching up rows
-            ok &= make_map(&g.a16_gu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, lb + p->hi_base, d0, s0, b0,
+            const uint64_t d0[4] = {(uint64_t)H, (uint64_t)I, 2, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
+            const uint64_t s0[3] = {(uint64_t)H * 2, (uint64_t)p->hi.codes_stride, (uint64_t)p->hi.bytes};
+            const uint32_t b0[4] = {64, 64, 2, 1};           // 64 gate rows, then the 64 matching up rows
+            ok &= make_map(&g.a16_gu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, lb + p->hi_base, d0, s0, b0,
                            CU_TENSOR_MAP_SWIZZLE_128B);
             const uint64_t d1[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
             const uint64_t s1[2] = {(uint64_t)I * 2, (uint64_t)p->hi.bytes};
@@ -128,16 +129,23 @@ static dx_status build_maps(dx_pool p) {
             const uint64_t slots = t ? (uint64_t)(cap_hi > 0 ? cap_hi : 1) : (uint64_t)(E + s);
             const uint64_t rb0 = (uint64_t)H * Ls.bits / 8, rb1 = (uint64_t)I * Ls.bits / 8;
             const uint32_t kb = 64 * Ls.bits / 8;
-            const uint64_t d0[3] = {rb0, (uint64_t)2 * I, slots};
-            const uint64_t s0[2] = {rb0, (uint64_t)Ls.bytes};
-            const uint32_t b0[3] = {kb, 64, 1};
-            ok &= make_map(t ? &g.ahi_gu : &g.alo_gu, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, d0, s0, b0,
+            const uint64_t d0[4] = {rb0, (uint64_t)I, 2, slots};
+            const uint64_t s0[3] = {rb0, (uint64_t)Ls.codes_stride, (uint64_t)Ls.bytes};
+            const uint32_t b0[4] = {kb, 64, 2, 1};
+            ok &= make_map(t ? &g.ahi_gu : &g.alo_gu, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, d0, s0, b0,
                            CU_TENSOR_MAP_SWIZZLE_NONE);
             const uint64_t d1[3] = {rb1, (uint64_t)H, slots};
             const uint64_t s1[2] = {rb1, (uint64_t)Ls.bytes};
             const uint32_t b1[3] = {kb, 128, 1};
             ok &= make_map(t ? &g.ahi_dn : &g.alo_dn, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * Ls.codes_stride, d1, s1,
                            b1, CU_TENSOR_MAP_SWIZZLE_NONE);
+            // decode stages: 128 B of codes per row (16 / bits K chunks) in one box; the tail past the row
+            // end is zero-filled by TMA and never read
+            const uint32_t w0[4] = {128, 64, 2, 1}, w1[3] = {128, 128, 1};
+            ok &= make_map(t ? &g.whi_gu : &g.wlo_gu, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, d0, s0, w0,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+            ok &= make_map(t ? &g.whi_dn : &g.wlo_dn, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * Ls.codes_stride, d1, s1,
+                           w1, CU_TENSOR_MAP_SWIZZLE_128B);
         }
         if (!ok) { dx_set_error("tensor map encoding failed (layer %d)", l); return DX_ERR_CUDA; }
     }
@@ -151,6 +159,18 @@ static dx_status build_maps(dx_pool p) {
         if (!make_map(&p->xb0[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->Xp, d0, s0, b, CU_TENSOR_MAP_SWIZZLE_128B) ||
             !make_map(&p->xb1[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, b, CU_TENSOR_MAP_SWIZZLE_128B)) {
             dx_set_error("tensor map encoding failed (activations)");
+            return DX_ERR_CUDA;
+        }
+    }
+    for (int i = 0; i < 3; ++i) {                           // {rows, chunks}: {16, 4}, {32, 4}, {16, 8}
+        const uint32_t bn = i == 1 ? 32 : 16, nc = i == 2 ? 8 : 4;
+        const uint64_t rows = (uint64_t)p->n_ent;
+        const uint64_t d0[3] = {64, rows, (uint64_t)H / 64}, s0[2] = {(uint64_t)H * 2, 128};
+        const uint64_t d1[3] = {64, rows, (uint64_t)I / 64}, s1[2] = {(uint64_t)I * 2, 128};
+        const uint32_t b[3] = {64, bn, nc};
+        if (!make_map(&p->xk0[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p->Xp, d0, s0, b, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !make_map(&p->xk1[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p->act, d1, s1, b, CU_TENSOR_MAP_SWIZZLE_128B)) {
+            dx_set_error("tensor map encoding failed (activations, 3-D)");
             return DX_ERR_CUDA;
         }
     }
@@ -639,9 +659,11 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         ga.dbg = dbg;
         GemmMaps gm = p->gmaps[layer];
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb0[i];
+        for (int i = 0; i < 3; ++i) gm.xk[i] = p->xk0[i];
         launch_gemm(0, dec, gm, ga, max_act * (p->I / 64), p->cs);
         if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb1[i];
+        for (int i = 0; i < 3; ++i) gm.xk[i] = p->xk1[i];
         launch_gemm(1, dec, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
     }
     if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));

@@ -209,10 +209,16 @@ void launch_expert_ffn(const ExpertArgs& a, const __nv_bfloat16* x, const float*
 // k_gemm.cu (tcgen05 grouped GEMM)
 #include <cuda.h>
 struct GemmMaps {
-    CUtensorMap a16_gu, a16_dn;     // bf16 HIGH region: dims {K, rows, slots}, 128 B swizzle
-    CUtensorMap ahi_gu, ahi_dn;     // raw codes of a quantised HIGH region
-    CUtensorMap alo_gu, alo_dn;     // raw codes of the LOW region
-    CUtensorMap xb[4];              // B operand rows [rows][K] bf16, boxes {64, 16/32/64/128}, 128 B swizzle
+    // A operands.  gate/up maps are 4-D {K, rows, matrix (gate, up), slot}: one box = 64 gate rows + the
+    // 64 matching up rows; down maps are 3-D {K, rows, slot}, 128-row boxes.
+    CUtensorMap a16_gu, a16_dn;     // bf16 HIGH region, 64-element K boxes, 128 B swizzle
+    CUtensorMap ahi_gu, ahi_dn;     // raw codes of a quantised HIGH region, one 64-wide K chunk per box
+    CUtensorMap alo_gu, alo_dn;     // raw codes of the LOW region, one 64-wide K chunk per box
+    CUtensorMap whi_gu, whi_dn;     // the same, 128 B of codes per row per box (decode stages), 128 B swizzle
+    CUtensorMap wlo_gu, wlo_dn;
+    // B operands (token rows [rows][K] bf16, 128 B swizzle)
+    CUtensorMap xb[4];              // 2-D boxes {64, 16/32/64/128}
+    CUtensorMap xk[3];              // 3-D {64, rows, K/64}: boxes {64,16,4}, {64,32,4}, {64,16,8} (decode int stages)
 };
 struct GemmArgs {
     const uint8_t* layer;
@@ -228,7 +234,8 @@ struct GemmArgs {
     int H, I, g, k;
     __nv_bfloat16* act;
     __nv_bfloat16* Y;
-    int dbg;                        // performance experiments only (DX_GEMM_DBG): 1 skip dequant, 2 skip TMEM store
+    int dbg;                        // performance experiments only (DX_GEMM_DBG): 4 skip the A-in-TMEM MMAs,
+                                    // 5 skip the dequant transform, 6 both
 };
 bool gemm_decode_cfg(int T);
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);

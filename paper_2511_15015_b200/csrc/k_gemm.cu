@@ -30,14 +30,18 @@ constexpr int A_BYTES = 128 * 128;            // A / raw region per stage
 constexpr int B_REGION = 16384;               // B region per stage
 constexpr int STAGE_BYTES = A_BYTES + B_REGION;
 constexpr int XCH_BYTES = 64 * 32 * 4;        // epilogue SwiGLU exchange: 64 rows x 32 columns fp32
+constexpr int MAXIT = 64;                     // work items per CTA decoded once into smem (rest: on the fly)
+constexpr int GTAB = 16;                      // scale/zero groups per row staged in smem per item (G <= 16)
+constexpr int TAB_BYTES = 128 * GTAB * 3;     // one item's table: [128 rows][G] bf16 scales, then u8 zeros
 
 // DEC: decode configuration (T <= 64): N <= 64 for bf16, 32 for int4, 16 for int2 with KS chunks per
 // quantised stage; otherwise (prefill) N <= 128 and one chunk per stage for every tier.
 template <bool DEC>
 struct Cfg {
     static constexpr int NBMAX = DEC ? 64 : 128;
-    static constexpr int NA = (512 - 2 * NBMAX) / 32;          // TMEM A buffers (32 columns each)
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + 2 * 128 * 17 * 4;
+    static constexpr int ACH = DEC ? 4 : 1;                    // K chunks per TMEM A buffer (32 columns each)
+    static constexpr int NA = (512 - 2 * NBMAX) / (32 * ACH);  // TMEM A buffers: 3 (decode) / 8 (prefill)
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + MAXIT * 16 + 2 * TAB_BYTES;
     __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : 128; }
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
@@ -48,18 +52,73 @@ __device__ __forceinline__ uint32_t bf2_sub_mul(uint32_t v, uint32_t zz, uint32_
     return *reinterpret_cast<uint32_t*>(&r);
 }
 
-// Decoded work item: expert e, 128-row block mb, its token rows [r0, r0+m), tier / slot / bits.
+// Exact dequantisation of one 64-element chunk of a row (R-Q1): codes at smem ra0 (and ra1 for the second
+// 16 B of int4), pair-interleaved packing (pair j at bits {bits*j, 16 + bits*j} of a 32-bit word), so a
+// bf16x2 of (128 + q) is (word >> bits*j) & mask | 0x4300_4300; then (. - (128 + z)) * s, each rounded once.
+__device__ __forceinline__ uint32_t and_or(uint32_t x, uint32_t m, uint32_t c) {   // (x & m) | c, one LOP3
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(x), "r"(m), "r"(c));
+    return d;
+}
+__device__ __forceinline__ void dequant_chunk(int bits, uint32_t ra0, uint32_t ra1, const uint32_t (&zz)[2],
+                                              const uint32_t (&ss)[2], uint32_t (&wv)[KCH / 2], uint32_t magic) {
+    if (bits == 4) {
+        uint32_t s0, s1, s2, s3, s4, s5, s6, s7;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(ra0));
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s4), "=r"(s5), "=r"(s6), "=r"(s7) : "r"(ra1));
+        const uint32_t src[8] = {s0, s1, s2, s3, s4, s5, s6, s7};
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t x = src[b >> 2] >> (4 * (b & 3));
+            wv[b] = bf2_sub_mul(and_or(x, 0x000F000Fu, magic), zz[b >> 4], ss[b >> 4]);
+        }
+    } else {
+        uint32_t s0, s1, s2, s3;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(ra0));
+        const uint32_t src[4] = {s0, s1, s2, s3};
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t x = src[b >> 3] >> (2 * (b & 7));
+            wv[b] = bf2_sub_mul(and_or(x, 0x00030003u, magic), zz[b >> 4], ss[b >> 4]);
+        }
+    }
+}
+
+// Decoded work item: 128-row block mb of an active expert, its token rows [r0, r0+m), tier / slot / bits.
 struct Item {
-    int e, mb, r0, m, ti, slot, bits;
+    int mb, r0, m, ti, slot, bits;
 };
-__device__ __forceinline__ Item decode(const GemmArgs& a, int item, int nmb) {
+__device__ __forceinline__ int4 decode_raw(const GemmArgs& a, int item, int nmb) {   // {r0, m, slot, ti}
+    const int e = a.act_e[item / nmb];
+    const int r0 = a.off[e];
+    return make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+}
+// the i-th item of this CTA (item = blockIdx.x + i * gridDim.x): from the smem table when i < MAXIT
+__device__ __forceinline__ Item get_item(const GemmArgs& a, const int4* itab, int i, int item, int nmb) {
+    const int4 v = i < MAXIT ? itab[i] : decode_raw(a, item, nmb);
     Item it;
-    it.e = a.act_e[item / nmb];
     it.mb = item % nmb;
-    it.r0 = a.off[it.e];
-    it.m = a.off[it.e + 1] - it.r0;
-    it.ti = a.tier[it.e];
-    it.slot = a.slot[it.e];
+    it.r0 = v.x;
+    it.m = v.y;
+    it.slot = v.z;
+    it.ti = v.w;
+    it.bits = it.ti ? a.hi.bits : a.lo.bits;
+    return it;
+}
+
+// the same, with every field made warp-uniform (producer / MMA warps)
+__device__ __forceinline__ Item get_item_u(const GemmArgs& a, const int4* itab, int i, int item, int nmb) {
+    int4 v = i < MAXIT ? itab[i] : decode_raw(a, item, nmb);
+    v.x = __shfl_sync(0xffffffffu, v.x, 0);
+    v.y = __shfl_sync(0xffffffffu, v.y, 0);
+    v.z = __shfl_sync(0xffffffffu, v.z, 0);
+    v.w = __shfl_sync(0xffffffffu, v.w, 0);
+    Item it;
+    it.mb = item % nmb;
+    it.r0 = v.x;
+    it.m = v.y;
+    it.slot = v.z;
+    it.ti = v.w;
     it.bits = it.ti ? a.hi.bits : a.lo.bits;
     return it;
 }
@@ -84,220 +143,273 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     uint64_t* aempty = aready + C::NA;                    // [NA] MMA finished with TMEM A buffer
     uint64_t* tfull = aempty + C::NA;                     // [2] accumulator ready
     uint64_t* tempty = tfull + 2;                         // [2] accumulator drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tabfull = tempty + 2;                       // [2] scale/zero table of an item landed
+    uint64_t* tabempty = tabfull + 2;                     // [2] transform finished with the table
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tabempty + 2);
     int32_t* ent_s = reinterpret_cast<int32_t*>(tmem_slot + 4);     // [128] epilogue: entry ids
     float* gate_s = reinterpret_cast<float*>(ent_s + 128);           // [128] epilogue: gates
-    uint32_t* sz_tab = reinterpret_cast<uint32_t*>(gate_s + 128);    // [2 groups][128 rows][17] scale|zero
+    int4* itab = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(bars) + 2048);   // [MAXIT] items
+    uint8_t* tabs = reinterpret_cast<uint8_t*>(itab + MAXIT);        // [2][TAB_BYTES]
 
     const int K = PHASE == 0 ? a.H : a.I;
     const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
     const int nk = K / KCH;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = K / a.g;                                // quantisation groups per weight row
+    const bool tab_ok = G <= GTAB;                        // per-item scale/zero tables staged by TMA
+    // warp index made provably warp-uniform: role branches are uniform and the single-thread issue paths
+    // keep their operands in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
 
     // prologue independent of the predecessor kernels (overlaps their tail under PDL)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], 128); mbar_init(&aempty[b], 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128); }
+        for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? 256 : 128); mbar_init(&aempty[b], 1); }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128);
+            mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], 256);
+        }
         fence_mbar_init();
         for (int i = 0; i < 4; ++i) tma_prefetch(&maps.xb[i]);
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t tmem_a = tmem + 2 * C::NBMAX;          // first TMEM A buffer column
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
     const int n_items = a.n_act[0] * nmb;
+    // this CTA's items, decoded once by all threads (the per-item dependent loads leave every role's
+    // critical path)
+    for (int i = threadIdx.x; i < MAXIT; i += GEMM_THREADS) {
+        const int item = blockIdx.x + i * gridDim.x;
+        if (item < n_items) itab[i] = decode_raw(a, item, nmb);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+    const uint32_t tmem_a = tmem + 2 * C::NBMAX;          // first TMEM A buffer column
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            int it = 0;
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-                const Item w = decode(a, item, nmb);
-                const CUtensorMap* amap = PHASE == 0 ? (w.bits == 16 ? &maps.a16_gu : (w.ti ? &maps.ahi_gu : &maps.alo_gu))
-                                                     : (w.bits == 16 ? &maps.a16_dn : (w.ti ? &maps.ahi_dn : &maps.alo_dn));
-                tma_prefetch(amap);
-                const int nb = C::nb(w.bits), ks = C::ks(w.bits);
-                const int rawc = 128 * KCH * w.bits / 8;          // raw bytes per chunk (int tiers)
-                for (int n0 = 0; n0 < w.m; n0 += nb) {
-                    const int rb = box_rows(min(nb, w.m - n0));
-                    const CUtensorMap* bmap = &maps.xb[rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : 3];
-                    for (int kb0 = 0; kb0 < nk; kb0 += ks, ++it) {
-                        const int kc = min(ks, nk - kb0);
-                        const int st = it % STAGES, ph = (it / STAGES) & 1;
-                        mbar_wait(&empty[st], ph ^ 1);
-                        uint8_t* sA = sS + st * STAGE_BYTES;
-                        uint8_t* sB = sA + A_BYTES;
-                        const uint32_t bytes = kc * rb * 128 + (w.bits == 16 ? A_BYTES : kc * rawc);
-                        mbar_arrive_expect_tx(&full[st], bytes);
-                        for (int j = 0; j < kc; ++j) {
-                            const int kb = kb0 + j;
-                            tma_load_2d(sB + j * rb * 128, bmap, &full[st], kb * KCH, w.r0 + n0);
-                            if (w.bits == 16) {
-                                if (PHASE == 0) {
-                                    tma_load_3d(sA, amap, &full[st], kb * KCH, w.mb * 64, w.slot);
-                                    tma_load_3d(sA + 64 * 128, amap, &full[st], kb * KCH, a.I + w.mb * 64, w.slot);
-                                } else {
-                                    tma_load_3d(sA, amap, &full[st], kb * KCH, w.mb * 128, w.slot);
-                                }
-                            } else {
-                                const int kbytes = kb * KCH * w.bits / 8;
-                                uint8_t* dst = sA + j * rawc;
-                                if (PHASE == 0) {
-                                    tma_load_3d(dst, amap, &full[st], kbytes, w.mb * 64, w.slot);
-                                    tma_load_3d(dst + rawc / 2, amap, &full[st], kbytes, a.I + w.mb * 64, w.slot);
-                                } else {
-                                    tma_load_3d(dst, amap, &full[st], kbytes, w.mb * 128, w.slot);
-                                }
-                            }
+        // ------------------------------------------------ TMA producer: the whole warp walks the stages
+        // with warp-uniform values (uniform registers, no per-lane serialisation); lane 0 issues
+        int st = 0, tc = 0;
+        uint32_t ph = 0;
+        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
+            const Item w = get_item_u(a, itab, ii, item, nmb);
+            const bool qt = w.bits != 16;
+            if (qt && tab_ok) {
+                // this item's scales / zeros: contiguous row spans of the slot's [rows][G] tables
+                const int tb = tc & 1;
+                mbar_wait(&tabempty[tb], ((tc >> 1) & 1) ^ 1);
+                ++tc;
+                if (lane == 0) {
+                    const SlotLayout& L = w.ti ? a.hi : a.lo;
+                    const uint8_t* sb = a.layer + (w.ti ? a.hi_base + (int64_t)w.slot * a.hi.bytes : (int64_t)w.slot * a.lo.bytes);
+                    uint8_t* ts = tabs + tb * TAB_BYTES;
+                    uint8_t* tz = ts + 128 * GTAB * 2;
+                    if (PHASE == 0) {
+                        const uint32_t sbytes = 64 * G * 2, zbytes = 64 * G;
+                        mbar_arrive_expect_tx(&tabfull[tb], 2 * (sbytes + zbytes));
+                        for (int m = 0; m < 2; ++m) {        // gate rows -> table rows 0-63, up rows -> 64-127
+                            const int64_t row = (int64_t)w.mb * 64;
+                            bulk_load(ts + m * sbytes, sb + L.scales_off + m * L.scales_stride + row * G * 2, sbytes,
+                                      &tabfull[tb]);
+                            bulk_load(tz + m * zbytes, sb + L.zeros_off + m * L.zeros_stride + row * G, zbytes,
+                                      &tabfull[tb]);
                         }
+                    } else {
+                        const int rows = min(128, a.H - w.mb * 128);
+                        const int64_t row = (int64_t)w.mb * 128;
+                        mbar_arrive_expect_tx(&tabfull[tb], rows * G * 3);
+                        bulk_load(ts, sb + L.scales_off + 2 * L.scales_stride + row * G * 2, rows * G * 2, &tabfull[tb]);
+                        bulk_load(tz, sb + L.zeros_off + 2 * L.zeros_stride + row * G, rows * G, &tabfull[tb]);
                     }
+                }
+                __syncwarp();
+            }
+            const CUtensorMap* amap =
+                PHASE == 0 ? (!qt ? &maps.a16_gu : DEC ? (w.ti ? &maps.whi_gu : &maps.wlo_gu) : (w.ti ? &maps.ahi_gu : &maps.alo_gu))
+                           : (!qt ? &maps.a16_dn : DEC ? (w.ti ? &maps.whi_dn : &maps.wlo_dn) : (w.ti ? &maps.ahi_dn : &maps.alo_dn));
+            const int nb = C::nb(w.bits), ks = C::ks(w.bits);
+            const int arow = PHASE == 0 ? w.mb * 64 : w.mb * 128;
+            const int kunit = qt ? KCH * w.bits / 8 : KCH;     // A inner coordinate per chunk (bytes / elements)
+            for (int n0 = 0; n0 < w.m; n0 += nb) {
+                const int rb = box_rows(min(nb, w.m - n0));
+                const int ri = rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : 3;
+                const bool multi = DEC && qt;                   // one B box carries the stage's ks chunks
+                const CUtensorMap* bmap = multi ? &maps.xk[w.bits == 2 ? 2 : ri] : &maps.xb[ri];
+                const uint32_t bytes = multi ? A_BYTES + ks * rb * 128 : (qt ? 128 * kunit : A_BYTES) + rb * 128;
+                for (int kb0 = 0; kb0 < nk; kb0 += ks) {
+                    mbar_wait(&empty[st], ph ^ 1);
+                    if (lane == 0) {
+                        uint8_t* sA = sS + st * STAGE_BYTES;
+                        mbar_arrive_expect_tx(&full[st], bytes);
+                        if (PHASE == 0) tma_load_4d(sA, amap, &full[st], kb0 * kunit, arow, 0, w.slot);
+                        else tma_load_3d(sA, amap, &full[st], kb0 * kunit, arow, w.slot);
+                        if (multi) tma_load_3d(sA + A_BYTES, bmap, &full[st], 0, w.r0 + n0, kb0);
+                        else tma_load_2d(sA + A_BYTES, bmap, &full[st], kb0 * KCH, w.r0 + n0);
+                    }
+                    __syncwarp();
+                    if (++st == STAGES) { st = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer (one thread)
-        if (lane == 0) {
-            int it = 0, ac = 0, cc = 0;
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-                const Item w = decode(a, item, nmb);
-                const int nb = C::nb(w.bits), ks = C::ks(w.bits);
-                for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
-                    const int rb = box_rows(min(nb, w.m - n0));
-                    const uint32_t idesc = idesc_bf16(128, rb);
-                    const int buf = cc & 1;
-                    mbar_wait(&tempty[buf], ((cc >> 1) & 1) ^ 1);
+        // ------------------------------------------------ MMA issuer: warp-uniform walk, lane 0 issues
+        // (tcgen05.mma / commit are single-thread instructions; commits must come from the issuing thread)
+        int st = 0, ab = 0, cc = 0;
+        uint32_t ph = 0, aph = 0;
+        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
+            const Item w = get_item_u(a, itab, ii, item, nmb);
+            const int nb = C::nb(w.bits), ks = C::ks(w.bits);
+            for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
+                const int rb = box_rows(min(nb, w.m - n0));
+                const uint32_t idesc = idesc_bf16(128, rb);
+                const int buf = cc & 1;
+                mbar_wait(&tempty[buf], ((cc >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + buf * C::NBMAX;
+                for (int kb0 = 0; kb0 < nk; kb0 += ks) {
+                    const int kc = min(ks, nk - kb0);
+                    mbar_wait(&full[st], ph);
                     tc_fence_after();
-                    const uint32_t d = tmem + buf * C::NBMAX;
-                    for (int kb0 = 0; kb0 < nk; kb0 += ks, ++it) {
-                        const int kc = min(ks, nk - kb0);
-                        const int st = it % STAGES, ph = (it / STAGES) & 1;
-                        mbar_wait(&full[st], ph);
-                        tc_fence_after();
-                        const uint32_t sA = smem_u32(sS + st * STAGE_BYTES), sB = sA + A_BYTES;
-                        if (w.bits == 16) {
+                    const uint32_t sA = smem_u32(sS + st * STAGE_BYTES), sB = sA + A_BYTES;
+                    if (w.bits == 16) {
+                        const uint64_t da = umma_desc_sw128(sA), db = umma_desc_sw128(sB);
+                        if (lane == 0) {
 #pragma unroll
-                            for (int s = 0; s < KCH / 16; ++s)
-                                mma_bf16(d, umma_desc_sw128(sA + 32 * s), umma_desc_sw128(sB + 32 * s), idesc,
-                                         (kb0 | s) != 0);
-                        } else {
-                            for (int j = 0; j < kc; ++j, ++ac) {
-                                const int ab = ac % C::NA;
-                                mbar_wait(&aready[ab], (ac / C::NA) & 1);
-                                tc_fence_after();
-                                const uint32_t at = tmem_a + 32 * ab, bj = sB + j * rb * 128;
+                            for (int s = 0; s < KCH / 16; ++s) mma_bf16(d, da + 2 * s, db + 2 * s, idesc, (kb0 | s) != 0);
+                        }
+                        __syncwarp();
+                    } else {
+                        const uint64_t db = umma_desc_sw128(sB);
+                        const uint32_t bstep = (rb * 128) >> 4;            // B sub-tile stride in descriptor units
+                        for (int j0 = 0; j0 < kc; j0 += C::ACH) {         // one TMEM A buffer = ACH chunks
+                            mbar_wait(&aready[ab], aph);
+                            tc_fence_after();
+                            const int jn = min(C::ACH, kc - j0);
+                            const uint32_t at = tmem_a + ab * 32 * C::ACH;
+                            const uint64_t bj = db + j0 * bstep;
+                            const bool first = (kb0 | j0) == 0;
+                            if (lane == 0) {
+                                if (a.dbg != 4 && a.dbg != 6) {
+                                    if (jn == C::ACH) {
 #pragma unroll
-                                for (int s = 0; s < KCH / 16; ++s)
-                                    mma_bf16_ts(d, at + 8 * s, umma_desc_sw128(bj + 32 * s), idesc,
-                                                ((kb0 + j) | s) != 0);
+                                        for (int q = 0; q < 4 * C::ACH; ++q)
+                                            mma_bf16_ts(d, at + 8 * q, bj + (q >> 2) * bstep + 2 * (q & 3), idesc, !first || q);
+                                    } else {
+                                        for (int j = 0; j < jn; ++j)
+#pragma unroll
+                                            for (int s = 0; s < 4; ++s)
+                                                mma_bf16_ts(d, at + 32 * j + 8 * s, bj + j * bstep + 2 * s, idesc,
+                                                            !first || j || s);
+                                    }
+                                }
                                 mma_commit(&aempty[ab]);
                             }
+                            __syncwarp();
+                            if (++ab == C::NA) { ab = 0; aph ^= 1; }
                         }
-                        mma_commit(&empty[st]);
                     }
-                    mma_commit(&tfull[buf]);
+                    if (lane == 0) mma_commit(&empty[st]);
+                    __syncwarp();
+                    if (++st == STAGES) { st = 0; ph ^= 1; }
                 }
+                if (lane == 0) mma_commit(&tfull[buf]);
+                __syncwarp();
             }
         }
     } else if (warp < 10) {
-        // ------------------------------------------------ dequant transform: two 4-warp groups take
-        // alternate K chunks of the quantised stages; thread = A row = TMEM lane
+        // ------------------------------------------------ dequant transform (8 warps, thread = A row =
+        // TMEM lane).  Decode: every TMEM A buffer holds ACH = 4 chunks, group g dequantises chunks 2g and
+        // 2g+1 of each; prefill: one chunk per buffer, the two groups take alternate buffers.
         const int grp = (warp - 2) >> 2;
         const int qa = warp & 3;
         const int r = 32 * qa + lane;
-        const int rows_total = PHASE == 0 ? 2 * a.I : a.H;
-        const int mat = PHASE == 0 ? 0 : 2;
-        const int G = K / a.g;
-        int it = 0, ac = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-            const Item w = decode(a, item, nmb);
+        // row r of the item's A block: matrix mat (gate 0 / up 1 / down 2), row mrow of it
+        const int mat_rows = PHASE == 0 ? a.I : a.H;
+        const uint32_t lane_base = tmem_a + ((uint32_t)(32 * qa) << 16);
+        const int gsh = 31 - __clz(a.g);                  // g is a power of two (checked at pool creation)
+        uint32_t magic = 0x43004300u;                     // bf16x2 (128, 128): kept in a register for LOP3
+        asm volatile("" : "+r"(magic));
+        int st = 0, ab = 0, tc = 0, nbuf = 0;
+        uint32_t ph = 0, aph = 0;
+        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
+            const Item w = get_item(a, itab, ii, item, nmb);
             const int nb = C::nb(w.bits), ks = C::ks(w.bits);
-            const int mat_row = PHASE == 0 ? (r < 64 ? 0 : a.I) + w.mb * 64 + (r & 63) : w.mb * 128 + r;
+            const int mat = PHASE == 0 ? (r >> 6) : 2;
+            const int mrow = PHASE == 0 ? w.mb * 64 + (r & 63) : w.mb * 128 + r;
             const SlotLayout& L = w.ti ? a.hi : a.lo;
             const uint8_t* slot_base =
                 a.layer + (w.ti ? a.hi_base + (int64_t)w.slot * a.hi.bytes : (int64_t)w.slot * a.lo.bytes);
             const uint16_t* scales = reinterpret_cast<const uint16_t*>(slot_base + L.scales_off + mat * L.scales_stride);
             const uint8_t* zeros = slot_base + L.zeros_off + mat * L.zeros_stride;
-            const int rawc = 128 * KCH * w.bits / 8, rowb = KCH * w.bits / 8;
-            // this row's scales / zeros for the whole item, once (G <= 16: g = 128, K <= 2048), packed
-            // as (bf16 scale | bf16(128 + z) << 16); otherwise fetched per chunk
-            // thread-private row table in smem (only this thread writes and reads it)
-            uint32_t* sz = sz_tab + (grp * 128 + r) * 17;
-            const bool sz_reg = G <= 16 && w.bits != 16;
-            if (sz_reg) {
-                for (int gi = 0; gi < G; ++gi) {
-                    uint32_t v = 0x43003f80u;
-                    if (mat_row < rows_total)
-                        v = (uint32_t)scales[(int64_t)mat_row * G + gi] | ((0x4300u + zeros[(int64_t)mat_row * G + gi]) << 16);
-                    sz[gi] = v;
-                }
-            }
+            const int rowb = KCH * w.bits / 8;
+            // scales / zeros: this item's smem table (TMA'd by the producer) when G <= GTAB, else global
+            const bool use_tab = tab_ok && w.bits != 16;
+            const int tb = tc & 1;
+            const uint16_t* tsc = reinterpret_cast<const uint16_t*>(tabs + tb * TAB_BYTES) + r * G;
+            const uint8_t* tze = tabs + tb * TAB_BYTES + 128 * GTAB * 2 + r * G;
+            if (use_tab) mbar_wait(&tabfull[tb], (tc >> 1) & 1);
             for (int n0 = 0; n0 < w.m; n0 += nb) {
-                for (int kb0 = 0; kb0 < nk; kb0 += ks, ++it) {
-                    const int st = it % STAGES, ph = (it / STAGES) & 1;
+                for (int kb0 = 0; kb0 < nk; kb0 += ks) {
                     // every transform thread observes every phase of full[] (no phase aliasing)
                     mbar_wait(&full[st], ph);
+                    const uint32_t stage = smem_u32(sS + st * STAGE_BYTES);
+                    if (++st == STAGES) { st = 0; ph ^= 1; }
                     if (w.bits == 16) continue;                   // bf16 stages need no transform
                     const int kc = min(ks, nk - kb0);
-                    for (int j = 0; j < kc; ++j, ++ac) {
-                        if ((ac & 1) != grp) continue;
-                        const int kb = kb0 + j;
-                        uint32_t zz[2], ss[2];
+                    for (int j0 = 0; j0 < kc; j0 += C::ACH, ++nbuf) {
+                        const int cab = ab;
+                        const uint32_t caph = aph;
+                        if (++ab == C::NA) { ab = 0; aph ^= 1; }
+                        if (!DEC && (nbuf & 1) != grp) continue;   // prefill: the other group's buffer
+                        mbar_wait(&aempty[cab], caph ^ 1);
+                        if (a.dbg != 5 && a.dbg != 6 && a.dbg != 8) {
 #pragma unroll
-                        for (int h2 = 0; h2 < 2; ++h2) {           // one or two groups per 64-element chunk
-                            const int gi = (kb * KCH + h2 * 32) / a.g;
-                            uint32_t v = 0x43003f80u;
-                            if (sz_reg) {
-                                v = sz[gi];
-                            } else if (mat_row < rows_total) {
-                                v = (uint32_t)scales[(int64_t)mat_row * G + gi] |
-                                    ((0x4300u + zeros[(int64_t)mat_row * G + gi]) << 16);
+                            for (int h = 0; h < (DEC ? 2 : 1); ++h) {
+                                const int jj = DEC ? 2 * grp + h : 0;    // chunk within the buffer
+                                const int j = j0 + jj;                    // chunk within the stage
+                                if (j >= kc) break;
+                                const int kb = kb0 + j;
+                                uint32_t zz[2], ss[2];
+#pragma unroll
+                                for (int h2 = 0; h2 < 2; ++h2) {   // one or two groups per 64-element chunk
+                                    const int gi = (kb * KCH + h2 * 32) >> gsh;
+                                    // packed (bf16 scale | bf16(128 + z) << 16); rows past the matrix: s = 1, z = 0
+                                    uint32_t v = 0x43003f80u;
+                                    if (mrow < mat_rows) {
+                                        if (use_tab) v = (uint32_t)tsc[gi] | ((0x4300u + tze[gi]) << 16);
+                                        else v = (uint32_t)scales[(int64_t)mrow * G + gi] | ((0x4300u + zeros[(int64_t)mrow * G + gi]) << 16);
+                                    }
+                                    zz[h2] = (v >> 16) * 0x10001u;
+                                    ss[h2] = (v & 0xFFFFu) * 0x10001u;
+                                }
+                                // raw codes of (row r, chunk j): decode stages hold one 128 B-swizzled row of
+                                // 16/bits chunks (16 B unit c of row r at unit c ^ (r & 7)); prefill one chunk
+                                uint32_t ra0, ra1;
+                                if (DEC) {
+                                    const uint32_t row = stage + r * 128;
+                                    const int c = j * rowb / 16;
+                                    ra0 = row + ((c ^ (r & 7)) << 4);
+                                    ra1 = row + (((c + 1) ^ (r & 7)) << 4);
+                                } else {
+                                    ra0 = stage + r * rowb;
+                                    ra1 = ra0 + 16;
+                                }
+                                uint32_t wv[KCH / 2];              // 32 bf16x2 words = 64 elements
+                                dequant_chunk(w.bits, ra0, ra1, zz, ss, wv, magic);
+                                tc_fence_after();
+                                tmem_st32(lane_base + cab * 32 * C::ACH + 32 * jj, wv);
                             }
-                            zz[h2] = (v >> 16) * 0x10001u;
-                            ss[h2] = (v & 0xFFFFu) * 0x10001u;
-                        }
-                        const int ab = ac % C::NA;
-                        mbar_wait(&aempty[ab], ((ac / C::NA) & 1) ^ 1);
-                        const uint32_t raw_addr = smem_u32(sS + st * STAGE_BYTES + j * rawc + r * rowb);
-                        uint32_t wv[KCH / 2];                      // 32 bf16x2 words = 64 elements
-                        if (a.dbg == 1) {                          // perf experiment: no dequant
-#pragma unroll
-                            for (int b = 0; b < 32; ++b) wv[b] = zz[0] ^ b;
-                        } else if (w.bits == 4) {
-                            uint32_t s0, s1, s2, s3, s4, s5, s6, s7;
-                            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(raw_addr));
-                            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s4), "=r"(s5), "=r"(s6), "=r"(s7) : "r"(raw_addr + 16));
-                            const uint32_t src[8] = {s0, s1, s2, s3, s4, s5, s6, s7};
-#pragma unroll
-                            for (int b = 0; b < 32; ++b) {      // pair-interleaved: pair j at bits 4j, 16+4j
-                                const uint32_t x = src[b >> 2] >> (4 * (b & 3));
-                                wv[b] = bf2_sub_mul((x & 0x000F000Fu) | 0x43004300u, zz[b >> 4], ss[b >> 4]);
-                            }
-                        } else {
-                            uint32_t s0, s1, s2, s3;
-                            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(raw_addr));
-                            const uint32_t src[4] = {s0, s1, s2, s3};
-#pragma unroll
-                            for (int b = 0; b < 32; ++b) {      // pair-interleaved: pair j at bits 2j, 16+2j
-                                const uint32_t x = src[b >> 3] >> (2 * (b & 7));
-                                wv[b] = bf2_sub_mul((x & 0x00030003u) | 0x43004300u, zz[b >> 4], ss[b >> 4]);
-                            }
-                        }
-                        tc_fence_after();
-                        if (a.dbg != 2) {                          // dbg 2: perf experiment, no TMEM store
-                            tmem_st32(tmem_a + ((uint32_t)(32 * qa) << 16) + 32 * ab, wv);
                             tmem_st_wait();
-                        } else if (wv[lane] == 0x12345678u) {
-                            a.act[0] = __float2bfloat16_rn(0.0f);
                         }
                         tc_fence_before();
-                        mbar_arrive(&aready[ab]);
+                        mbar_arrive(&aready[cab]);
                     }
                 }
+            }
+            if (use_tab) {                                        // table buffer back to the producer
+                mbar_arrive(&tabempty[tb]);
+                ++tc;
             }
         }
     } else {
@@ -305,8 +417,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         const int q = warp & 3;                         // TMEM lane quarter this warp may access
         const int et = threadIdx.x - 320;               // 0..127
         int cc = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-            const Item w = decode(a, item, nmb);
+        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
+            const Item w = get_item(a, itab, ii, item, nmb);
             const int nb = C::nb(w.bits);
             for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
                 const int buf = cc & 1;
