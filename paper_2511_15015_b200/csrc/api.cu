@@ -23,6 +23,8 @@ void dx_set_error(const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+    const size_t len = strlen(g_err);
+    gemm_trap_report(g_err + len, sizeof(g_err) - len);
 }
 extern "C" const char* dx_last_error(void) { return g_err; }
 extern "C" const char* dx_version(void) { return "dynaexq-b200 0.1 (sm_100a)"; }
@@ -492,6 +494,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     const i64 n3 = (i64)3 * p->I * p->H;
     inf.export_bytes_hi = cfg->high_bits == 16 ? n3 * 2 : n3 + n3 / p->g * 3;
     inf.export_bytes_lo = n3 + n3 / p->g * 3;
+    gemm_trap_init();
     st = build_maps(p);
     if (st != DX_OK) return fail(st);
     *out = p;

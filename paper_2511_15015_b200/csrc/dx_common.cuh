@@ -238,6 +238,8 @@ struct GemmArgs {
                                     // 5 skip the dequant transform, 6 both
 };
 bool gemm_decode_cfg(int T);
+void gemm_trap_init();                            // host-mapped watchdog record (once per process)
+int gemm_trap_report(char* buf, size_t n);        // appends the record, if a k_gemm wait timed out
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
 
 // k_ctrl.cu

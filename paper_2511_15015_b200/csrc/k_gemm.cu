@@ -18,6 +18,9 @@
 // Warp roles (448 threads): 0 TMA producer, 1 TMEM owner + MMA issuer, 2-9 transform, 10-13 epilogue.
 #include "dx_common.cuh"
 #include "dx_sm100.cuh"
+#include <cstdio>
+#include <cstring>
+#include <type_traits>
 
 using namespace sm100;
 
@@ -82,6 +85,28 @@ __device__ __forceinline__ void dequant_chunk(int bits, uint32_t ra0, uint32_t r
             wv[b] = bf2_sub_mul(and_or(x, 0x00030003u, magic), zz[b >> 4], ss[b >> 4]);
         }
     }
+}
+
+// Protocol watchdog: a wait that never completes records which barrier (tag), parity, block and thread in a
+// host-mapped word array and traps, so a hang surfaces as a launch error with a readable diagnosis
+// (gemm_trap_report) instead of a stuck GPU.
+__device__ uint32_t* g_gemm_trap = nullptr;
+__device__ __noinline__ void gemm_trap(uint32_t tag, uint32_t parity) {
+    uint32_t* r = g_gemm_trap;
+    if (r && atomicCAS(r, 0u, 0xDEAD0000u | tag) == 0u) {
+        r[1] = parity;
+        r[2] = blockIdx.x;
+        r[3] = threadIdx.x;
+        __threadfence_system();
+    }
+    __trap();
+}
+__device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, uint32_t tag) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait_sleep(a, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try_wait_sleep(a, parity))
+        if (globaltimer_ns() - t0 > 2000000000ull) gemm_trap(tag, parity);   // 2 s: a protocol bug
 }
 
 // Decoded work item: 128-row block mb of an active expert, its token rows [r0, r0+m), tier / slot / bits.
@@ -198,9 +223,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             if (qt && tab_ok) {
                 // this item's scales / zeros: contiguous row spans of the slot's [rows][G] tables
                 const int tb = tc & 1;
-                mbar_wait(&tabempty[tb], ((tc >> 1) & 1) ^ 1);
+                gwait(&tabempty[tb], ((tc >> 1) & 1) ^ 1, 1);
                 ++tc;
-                if (lane == 0) {
+                if (elect_one()) {
                     const SlotLayout& L = w.ti ? a.hi : a.lo;
                     const uint8_t* sb = a.layer + (w.ti ? a.hi_base + (int64_t)w.slot * a.hi.bytes : (int64_t)w.slot * a.lo.bytes);
                     uint8_t* ts = tabs + tb * TAB_BYTES;
@@ -238,8 +263,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 const CUtensorMap* bmap = multi ? &maps.xk[w.bits == 2 ? 2 : ri] : &maps.xb[ri];
                 const uint32_t bytes = multi ? A_BYTES + ks * rb * 128 : (qt ? 128 * kunit : A_BYTES) + rb * 128;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
-                    mbar_wait(&empty[st], ph ^ 1);
-                    if (lane == 0) {
+                    gwait(&empty[st], ph ^ 1, 2);
+                    if (elect_one()) {
                         uint8_t* sA = sS + st * STAGE_BYTES;
                         mbar_arrive_expect_tx(&full[st], bytes);
                         if (PHASE == 0) tma_load_4d(sA, amap, &full[st], kb0 * kunit, arow, 0, w.slot);
@@ -264,17 +289,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 const int rb = box_rows(min(nb, w.m - n0));
                 const uint32_t idesc = idesc_bf16(128, rb);
                 const int buf = cc & 1;
-                mbar_wait(&tempty[buf], ((cc >> 1) & 1) ^ 1);
+                gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * C::NBMAX;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
                     const int kc = min(ks, nk - kb0);
-                    mbar_wait(&full[st], ph);
+                    gwait(&full[st], ph, 4);
                     tc_fence_after();
                     const uint32_t sA = smem_u32(sS + st * STAGE_BYTES), sB = sA + A_BYTES;
                     if (w.bits == 16) {
                         const uint64_t da = umma_desc_sw128(sA), db = umma_desc_sw128(sB);
-                        if (lane == 0) {
+                        if (elect_one()) {
 #pragma unroll
                             for (int s = 0; s < KCH / 16; ++s) mma_bf16(d, da + 2 * s, db + 2 * s, idesc, (kb0 | s) != 0);
                         }
@@ -283,13 +308,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         const uint64_t db = umma_desc_sw128(sB);
                         const uint32_t bstep = (rb * 128) >> 4;            // B sub-tile stride in descriptor units
                         for (int j0 = 0; j0 < kc; j0 += C::ACH) {         // one TMEM A buffer = ACH chunks
-                            mbar_wait(&aready[ab], aph);
+                            gwait(&aready[ab], aph, 5);
                             tc_fence_after();
                             const int jn = min(C::ACH, kc - j0);
                             const uint32_t at = tmem_a + ab * 32 * C::ACH;
                             const uint64_t bj = db + j0 * bstep;
                             const bool first = (kb0 | j0) == 0;
-                            if (lane == 0) {
+                            if (elect_one()) {
                                 if (a.dbg != 4 && a.dbg != 6) {
                                     if (jn == C::ACH) {
 #pragma unroll
@@ -309,11 +334,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                             if (++ab == C::NA) { ab = 0; aph ^= 1; }
                         }
                     }
-                    if (lane == 0) mma_commit(&empty[st]);
+                    if (elect_one()) mma_commit(&empty[st]);
                     __syncwarp();
                     if (++st == STAGES) { st = 0; ph ^= 1; }
                 }
-                if (lane == 0) mma_commit(&tfull[buf]);
+                if (elect_one()) mma_commit(&tfull[buf]);
                 __syncwarp();
             }
         }
@@ -324,9 +349,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         const int grp = (warp - 2) >> 2;
         const int qa = warp & 3;
         const int r = 32 * qa + lane;
-        // row r of the item's A block: matrix mat (gate 0 / up 1 / down 2), row mrow of it
+        const uint32_t rsw = r & 7;                        // 128 B swizzle phase of this row
         const int mat_rows = PHASE == 0 ? a.I : a.H;
         const uint32_t lane_base = tmem_a + ((uint32_t)(32 * qa) << 16);
+        const uint32_t stages_u32 = smem_u32(sS);
         const int gsh = 31 - __clz(a.g);                  // g is a power of two (checked at pool creation)
         uint32_t magic = 0x43004300u;                     // bf16x2 (128, 128): kept in a register for LOP3
         asm volatile("" : "+r"(magic));
@@ -334,80 +360,97 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         uint32_t ph = 0, aph = 0;
         for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
             const Item w = get_item(a, itab, ii, item, nmb);
-            const int nb = C::nb(w.bits), ks = C::ks(w.bits);
+            if (w.bits == 16) {                           // bf16 stages need no transform: observe their phases
+                const int nst = ((w.m + C::nb(16) - 1) / C::nb(16)) * nk;
+                for (int s = 0; s < nst; ++s) {
+                    gwait(&full[st], ph, 7);
+                    if (++st == STAGES) { st = 0; ph ^= 1; }
+                }
+                continue;
+            }
+            // row r of the item's A block: matrix mat (gate 0 / up 1 / down 2), row mrow of it
             const int mat = PHASE == 0 ? (r >> 6) : 2;
             const int mrow = PHASE == 0 ? w.mb * 64 + (r & 63) : w.mb * 128 + r;
+            const bool valid = mrow < mat_rows;
             const SlotLayout& L = w.ti ? a.hi : a.lo;
             const uint8_t* slot_base =
                 a.layer + (w.ti ? a.hi_base + (int64_t)w.slot * a.hi.bytes : (int64_t)w.slot * a.lo.bytes);
-            const uint16_t* scales = reinterpret_cast<const uint16_t*>(slot_base + L.scales_off + mat * L.scales_stride);
-            const uint8_t* zeros = slot_base + L.zeros_off + mat * L.zeros_stride;
-            const int rowb = KCH * w.bits / 8;
+            const uint16_t* scales =
+                reinterpret_cast<const uint16_t*>(slot_base + L.scales_off + mat * L.scales_stride) + (int64_t)mrow * G;
+            const uint8_t* zeros = slot_base + L.zeros_off + mat * L.zeros_stride + (int64_t)mrow * G;
             // scales / zeros: this item's smem table (TMA'd by the producer) when G <= GTAB, else global
-            const bool use_tab = tab_ok && w.bits != 16;
             const int tb = tc & 1;
             const uint16_t* tsc = reinterpret_cast<const uint16_t*>(tabs + tb * TAB_BYTES) + r * G;
             const uint8_t* tze = tabs + tb * TAB_BYTES + 128 * GTAB * 2 + r * G;
-            if (use_tab) mbar_wait(&tabfull[tb], (tc >> 1) & 1);
-            for (int n0 = 0; n0 < w.m; n0 += nb) {
-                for (int kb0 = 0; kb0 < nk; kb0 += ks) {
-                    // every transform thread observes every phase of full[] (no phase aliasing)
-                    mbar_wait(&full[st], ph);
-                    const uint32_t stage = smem_u32(sS + st * STAGE_BYTES);
-                    if (++st == STAGES) { st = 0; ph ^= 1; }
-                    if (w.bits == 16) continue;                   // bf16 stages need no transform
-                    const int kc = min(ks, nk - kb0);
-                    for (int j0 = 0; j0 < kc; j0 += C::ACH, ++nbuf) {
-                        const int cab = ab;
-                        const uint32_t caph = aph;
-                        if (++ab == C::NA) { ab = 0; aph ^= 1; }
-                        if (!DEC && (nbuf & 1) != grp) continue;   // prefill: the other group's buffer
-                        mbar_wait(&aempty[cab], caph ^ 1);
-                        if (a.dbg != 5 && a.dbg != 6 && a.dbg != 8) {
+            if (tab_ok) gwait(&tabfull[tb], (tc >> 1) & 1, 6);
+            // packed (bf16 scale | bf16(128 + z) << 16) of group gi; rows past the matrix: s = 1, z = 0
+            auto group_sz = [&](int gi) -> uint32_t {
+                if (!valid) return 0x43003f80u;
+                return tab_ok ? (uint32_t)tsc[gi] | ((0x4300u + tze[gi]) << 16)
+                              : (uint32_t)scales[gi] | ((0x4300u + zeros[gi]) << 16);
+            };
+            auto body = [&](auto bits_c) {
+                constexpr int BITS = decltype(bits_c)::value;
+                constexpr int KS = DEC ? 16 / BITS : 1;     // K chunks per stage
+                constexpr int ROWB = KCH * BITS / 8;        // code bytes per row per chunk
+                constexpr int NBB = DEC ? (BITS == 4 ? 32 : 16) : 128;
+                for (int n0 = 0; n0 < w.m; n0 += NBB) {
+                    for (int kb0 = 0; kb0 < nk; kb0 += KS) {
+                        // every transform thread observes every phase of full[] (no phase aliasing)
+                        gwait(&full[st], ph, 7);
+                        const uint32_t stage = stages_u32 + st * STAGE_BYTES;
+                        if (++st == STAGES) { st = 0; ph ^= 1; }
+                        const int kc = min(KS, nk - kb0);
+                        for (int j0 = 0; j0 < kc; j0 += C::ACH, ++nbuf) {
+                            const int cab = ab;
+                            const uint32_t caph = aph;
+                            if (++ab == C::NA) { ab = 0; aph ^= 1; }
+                            if (!DEC && (nbuf & 1) != grp) continue;   // prefill: the other group's buffer
+                            gwait(&aempty[cab], caph ^ 1, 8);
+                            if (a.dbg != 5 && a.dbg != 6) {
 #pragma unroll
-                            for (int h = 0; h < (DEC ? 2 : 1); ++h) {
-                                const int jj = DEC ? 2 * grp + h : 0;    // chunk within the buffer
-                                const int j = j0 + jj;                    // chunk within the stage
-                                if (j >= kc) break;
-                                const int kb = kb0 + j;
-                                uint32_t zz[2], ss[2];
-#pragma unroll
-                                for (int h2 = 0; h2 < 2; ++h2) {   // one or two groups per 64-element chunk
-                                    const int gi = (kb * KCH + h2 * 32) >> gsh;
-                                    // packed (bf16 scale | bf16(128 + z) << 16); rows past the matrix: s = 1, z = 0
-                                    uint32_t v = 0x43003f80u;
-                                    if (mrow < mat_rows) {
-                                        if (use_tab) v = (uint32_t)tsc[gi] | ((0x4300u + tze[gi]) << 16);
-                                        else v = (uint32_t)scales[(int64_t)mrow * G + gi] | ((0x4300u + zeros[(int64_t)mrow * G + gi]) << 16);
+                                for (int h = 0; h < (DEC ? 2 : 1); ++h) {
+                                    const int jj = DEC ? 2 * grp + h : 0;   // chunk within the buffer
+                                    const int j = j0 + jj;                   // chunk within the stage
+                                    if (j < kc) {
+                                        const int k0 = (kb0 + j) * KCH;
+                                        uint32_t zz[2], ss[2];
+                                        const uint32_t v0 = group_sz(k0 >> gsh);
+                                        const uint32_t v1 = a.g >= 64 ? v0 : group_sz((k0 + 32) >> gsh);
+                                        zz[0] = (v0 >> 16) * 0x10001u;
+                                        ss[0] = (v0 & 0xFFFFu) * 0x10001u;
+                                        zz[1] = (v1 >> 16) * 0x10001u;
+                                        ss[1] = (v1 & 0xFFFFu) * 0x10001u;
+                                        // raw codes of (row r, chunk j): decode stages hold one 128 B-swizzled
+                                        // row of KS chunks (16 B unit c of row r at unit c ^ (r & 7)); prefill
+                                        // stages one chunk
+                                        uint32_t ra0, ra1;
+                                        if (DEC) {
+                                            const uint32_t row = stage + r * 128;
+                                            const uint32_t c = j * ROWB / 16;
+                                            ra0 = row + ((c ^ rsw) << 4);
+                                            ra1 = row + (((c + 1) ^ rsw) << 4);
+                                        } else {
+                                            ra0 = stage + r * ROWB;
+                                            ra1 = ra0 + 16;
+                                        }
+                                        uint32_t wv[KCH / 2];      // 32 bf16x2 words = 64 elements
+                                        dequant_chunk(BITS, ra0, ra1, zz, ss, wv, magic);
+                                        tc_fence_after();
+                                        tmem_st32(lane_base + cab * 32 * C::ACH + 32 * jj, wv);
                                     }
-                                    zz[h2] = (v >> 16) * 0x10001u;
-                                    ss[h2] = (v & 0xFFFFu) * 0x10001u;
                                 }
-                                // raw codes of (row r, chunk j): decode stages hold one 128 B-swizzled row of
-                                // 16/bits chunks (16 B unit c of row r at unit c ^ (r & 7)); prefill one chunk
-                                uint32_t ra0, ra1;
-                                if (DEC) {
-                                    const uint32_t row = stage + r * 128;
-                                    const int c = j * rowb / 16;
-                                    ra0 = row + ((c ^ (r & 7)) << 4);
-                                    ra1 = row + (((c + 1) ^ (r & 7)) << 4);
-                                } else {
-                                    ra0 = stage + r * rowb;
-                                    ra1 = ra0 + 16;
-                                }
-                                uint32_t wv[KCH / 2];              // 32 bf16x2 words = 64 elements
-                                dequant_chunk(w.bits, ra0, ra1, zz, ss, wv, magic);
-                                tc_fence_after();
-                                tmem_st32(lane_base + cab * 32 * C::ACH + 32 * jj, wv);
+                                tmem_st_wait();
                             }
-                            tmem_st_wait();
+                            tc_fence_before();
+                            mbar_arrive(&aready[cab]);
                         }
-                        tc_fence_before();
-                        mbar_arrive(&aready[cab]);
                     }
                 }
-            }
-            if (use_tab) {                                        // table buffer back to the producer
+            };
+            if (w.bits == 4) body(std::integral_constant<int, 4>{});
+            else body(std::integral_constant<int, 2>{});
+            if (tab_ok) {                                 // table buffer back to the producer
                 mbar_arrive(&tabempty[tb]);
                 ++tc;
             }
@@ -430,7 +473,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         gate_s[i] = a.gate[ent];
                     }
                 }
-                mbar_wait(&tfull[buf], (cc >> 1) & 1);
+                gwait(&tfull[buf], (cc >> 1) & 1, 9);
                 tc_fence_after();
                 named_bar(1, 128);
                 for (int col = 0; col < nvalid; col += 32) {
@@ -496,6 +539,28 @@ void launch_one(const GemmMaps& maps, const GemmArgs& a, int items, cudaStream_t
 }  // namespace
 
 bool gemm_decode_cfg(int T) { return T <= 64; }
+
+static uint32_t* g_trap_host = nullptr;
+void gemm_trap_init() {
+    if (g_trap_host) return;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&g_trap_host), 64, cudaHostAllocMapped) != cudaSuccess) {
+        g_trap_host = nullptr;
+        return;
+    }
+    memset(g_trap_host, 0, 64);
+    uint32_t* dptr = nullptr;
+    cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), g_trap_host, 0);
+    cudaMemcpyToSymbol(g_gemm_trap, &dptr, sizeof(dptr));
+}
+static const char* const k_trap_names[] = {"?", "tabempty (producer)", "empty (producer)", "tempty (MMA)", "full (MMA)",
+                                           "aready (MMA)", "tabfull (transform)", "full (transform)",
+                                           "aempty (transform)", "tfull (epilogue)"};
+int gemm_trap_report(char* buf, size_t n) {
+    if (!g_trap_host || (g_trap_host[0] >> 16) != 0xDEADu) return 0;
+    const uint32_t tag = g_trap_host[0] & 0xFFFFu;
+    return snprintf(buf, n, " [k_gemm watchdog: wait on %s, parity %u, block %u, thread %u]",
+                    tag < 10 ? k_trap_names[tag] : "?", g_trap_host[1], g_trap_host[2], g_trap_host[3]);
+}
 
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st) {
     if (max_items <= 0) return;
