@@ -288,10 +288,11 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         const size_t LE = (size_t)L * Ek, LO = (size_t)L * (Ek + s);
         ctrl_bytes = LE * (4 + 4 + 4 + 8 + 4 + 8 + 8 + 4 + 4 + 8 + 16) + LO * 8 + L * (8 + 8 + 4 * 3) + 64 * 256;
     }
-    size_t ws_bytes = (size_t)T * p->E * 4 + n_ent * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
+    const size_t lg_rows = (size_t)T;
+    size_t ws_bytes = lg_rows * p->E * 4 + n_ent * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
                       (size_t)(p->E + 1) * 8 + n_ent * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8;
     if (G > 1)   // dispatch-side routing workspace (global experts, local tokens)
-        ws_bytes += (size_t)T * p->E * 4 + (size_t)T * k * 16 + (size_t)route_blocks(T) * p->E * 8 +
+        ws_bytes += lg_rows * p->E * 4 + (size_t)T * k * 16 + (size_t)route_blocks(T) * p->E * 8 +
                     (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
     const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
@@ -329,7 +330,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     c.E = E; c.s = s; c.n_hot = (int)n_hot; c.W = cfg->warmup_steps; c.Tp = cfg->period;
     c.dwell = cfg->dwell_min; c.lag = cfg->publish_lag; c.alpha = cfg->ema_alpha;
     RouteWs& w = p->ws;
-    w.logits = carve<float>(q, (size_t)T * p->E);
+    w.logits = carve<float>(q, lg_rows * p->E);
     w.idx = carve<int32_t>(q, n_ent);
     w.gate = carve<float>(q, n_ent);
     w.hist = carve<int32_t>(q, (size_t)nblk * p->E);
@@ -343,7 +344,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     w.done = carve<unsigned>(q, 1);
     if (G > 1) {
         RouteWs& v = p->ws_src;
-        v.logits = carve<float>(q, (size_t)T * p->E);
+        v.logits = carve<float>(q, lg_rows * p->E);
         v.idx = carve<int32_t>(q, (size_t)T * k);
         v.gate = carve<float>(q, (size_t)T * k);
         v.hist = carve<int32_t>(q, (size_t)route_blocks(T) * p->E);
@@ -614,17 +615,25 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
     if (topk_gate) ws.gate = topk_gate;
     const float* lg = logits;
     if (router_w) {
-        launch_router((const __nv_bfloat16*)x, (const __nv_bfloat16*)router_w, router_bias, T, p->E, p->H,
-                      ws.logits, p->cs);
+        launch_router((const __nv_bfloat16*)x, (const __nv_bfloat16*)router_w, router_bias, T, p->E, p->H, ws.logits,
+                      p->cs);
         lg = ws.logits;
         p->launches += 1;
     }
     const size_t base = (size_t)layer * p->E_loc;
     // a2+a3 (+ the a4 offset scan in the last block), then a4 placement (+ x gather for tcgen05)
-    launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->ctrl.tier + base,
-                 p->wbytes, p->cs);
-    launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
-    p->launches += 2;
+    __nv_bfloat16* Xp = p->ffn_path == 1 ? nullptr : p->Xp;
+    if (route1_ok(T, p->E, p->k)) {
+        launch_route1(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base,
+                      p->ctrl.mass + base, p->ctrl.tier + base, p->wbytes, p->cs);
+        launch_gather(T, p->k, ws, (const __nv_bfloat16*)x, p->H, Xp, p->cs);
+        p->launches += Xp ? 2 : 1;
+    } else {
+        launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base,
+                     p->ctrl.mass + base, p->ctrl.tier + base, p->wbytes, p->cs);
+        launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, Xp, p->cs);
+        p->launches += 2;
+    }
     dx_status st = expert_ffn(p, layer, ws, x, T, p->k, y, ev);
     if (st != DX_OK) return st;
     p->pend_tokens[layer] += (u64)T;

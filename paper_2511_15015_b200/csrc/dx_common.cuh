@@ -176,11 +176,18 @@ struct RouteStats {       // profiling: algorithmic weight bytes per touched exp
     u64* stats;
 };
 int route_blocks(int T);
-void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E,
-                   int H, float* logits, cudaStream_t st);
+// logits[t][e] = x[t] . W_r[e] (+ bias[e]), fp32 (tensor-core products, deterministic sum order)
+void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E, int H,
+                   float* logits, cudaStream_t st);
 // tier: layer table (or NULL); bytes[tier][phase]: algorithmic weight bytes of one expert
 void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
                   uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st);
+// decode batches (route1_ok): a2-a4 in one single-block launch (top-k, gates, counters, offsets, active
+// list, perm / inv), then the x gather
+bool route1_ok(int T, int E, int k);
+void launch_route1(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
+                   uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st);
+void launch_gather(int T, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp, cudaStream_t st);
 // stable placement of every (t, j) entry; Xp != NULL also gathers x rows in permuted order
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
                   cudaStream_t st);

@@ -13,65 +13,108 @@
 namespace {
 
 // ------------------------------------------------------------------ a1: logits = x Wr^T (+b), fp32
-template <int TT>
-__global__ void __launch_bounds__(256) k_router(const __nv_bfloat16* __restrict__ x,
-                                                const __nv_bfloat16* __restrict__ wr,
+// Tensor-core router (mma.sync m16n8k16, bf16 products exact, fp32 accumulate): block = 8 experts x 16
+// tokens, 16 warps each taking every 16th K step (short per-warp load chains, all fragment loads of a warp
+// in flight at once; x is L2-resident).  The 16 warp partials are summed in smem in warp order, so the
+// logits are deterministic.
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__global__ void __launch_bounds__(512) k_router(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr,
                                                 const float* __restrict__ bias, int T, int E, int H,
                                                 float* __restrict__ logits) {
-    extern __shared__ float xs[];   // [TT][H]
+    __shared__ float red[16][16][9];                      // [warp][token][expert] partials
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
-    const int t0 = blockIdx.y * TT;
-    const int nt = min(TT, T - t0);
-    for (int i = threadIdx.x; i < TT * H / 8; i += blockDim.x) {
-        const int t = (i * 8) / H, h = (i * 8) % H;
-        float* d = xs + t * H + h;
-        if (t < nt) {
-            uint4 v = *reinterpret_cast<const uint4*>(x + (size_t)(t0 + t) * H + h);
-            const uint16_t* b = reinterpret_cast<const uint16_t*>(&v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    const int e0 = blockIdx.x * 8, t0 = blockIdx.y * 16;
+    const int ta = t0 + g, tb = t0 + g + 8, e = e0 + g;
+    const uint32_t* xa = reinterpret_cast<const uint32_t*>(x + (size_t)min(ta, T - 1) * H) + q;
+    const uint32_t* xb = reinterpret_cast<const uint32_t*>(x + (size_t)min(tb, T - 1) * H) + q;
+    const uint32_t* we = reinterpret_cast<const uint32_t*>(wr + (size_t)min(e, E - 1) * H) + q;
+    const int nsteps = H / 16;
+    float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    constexpr int U = 8;
+    for (int s0 = warp; s0 < nsteps; s0 += 16 * U) {
+        uint32_t f[U][6];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) d[j] = dx_bf2f(b[j]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) d[j] = 0.0f;
+        for (int u = 0; u < U; ++u) {                      // all loads of the batch first
+            const int s = s0 + 16 * u;
+            if (s < nsteps) {
+                const int k = s * 8;                       // 16 elements = 8 words per step
+                f[u][0] = __ldg(xa + k); f[u][1] = __ldg(xb + k);
+                f[u][2] = __ldg(xa + k + 4); f[u][3] = __ldg(xb + k + 4);
+                f[u][4] = __ldg(we + k); f[u][5] = __ldg(we + k + 4);
+            }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (s0 + 16 * u < nsteps) mma16816(c, f[u][0], f[u][1], f[u][2], f[u][3], f[u][4], f[u][5]);
     }
+    red[warp][g][2 * q] = c[0];
+    red[warp][g][2 * q + 1] = c[1];
+    red[warp][g + 8][2 * q] = c[2];
+    red[warp][g + 8][2 * q + 1] = c[3];
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (e >= E) return;
-    const __nv_bfloat16* row = wr + (size_t)e * H;
-    float acc[TT];
+    if (threadIdx.x < 128) {
+        const int tl = threadIdx.x >> 3, el = threadIdx.x & 7;   // 16 tokens x 8 experts
+        const int t = t0 + tl, ee = e0 + el;
+        if (t < T && ee < E) {
+            float v = red[0][tl][el];
 #pragma unroll
-    for (int t = 0; t < TT; ++t) acc[t] = 0.0f;
-#pragma unroll 8
-    for (int k = lane * 8; k < H; k += 256) {
-        uint4 v = __ldg(reinterpret_cast<const uint4*>(row + k));
-        const uint16_t* b = reinterpret_cast<const uint16_t*>(&v);
-        float w[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) w[j] = dx_bf2f(b[j]);
-#pragma unroll
-        for (int t = 0; t < TT; ++t) {
-            const float4 a = *reinterpret_cast<const float4*>(xs + t * H + k);
-            const float4 c = *reinterpret_cast<const float4*>(xs + t * H + k + 4);
-            acc[t] = fmaf(w[0], a.x, acc[t]); acc[t] = fmaf(w[1], a.y, acc[t]);
-            acc[t] = fmaf(w[2], a.z, acc[t]); acc[t] = fmaf(w[3], a.w, acc[t]);
-            acc[t] = fmaf(w[4], c.x, acc[t]); acc[t] = fmaf(w[5], c.y, acc[t]);
-            acc[t] = fmaf(w[6], c.z, acc[t]); acc[t] = fmaf(w[7], c.w, acc[t]);
+            for (int w = 1; w < 16; ++w) v += red[w][tl][el];
+            logits[(size_t)t * E + ee] = bias ? v + bias[ee] : v;
         }
-    }
-#pragma unroll
-    for (int t = 0; t < TT; ++t) {
-        float v = acc[t];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && t < nt) logits[(size_t)(t0 + t) * E + e] = v + (bias ? bias[e] : 0.0f);
     }
 }
 
 __device__ __forceinline__ bool better(float a, int ea, float b, int eb) {
     return a > b || (a == b && ea < eb);
+}
+
+// Order-preserving u32 key of a float (larger float -> larger key); 0 = excluded (below every value).
+__device__ __forceinline__ uint32_t fkey(float f) {
+    uint32_t u = __float_as_uint(f);
+    if (u == 0x80000000u) u = 0u;                          // -0 ties with +0 (float compare)
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+// k rounds of warp arg-max over E = 32 * NVT values (lane holds experts lane + 32 i): per round the best
+// value by a max-reduction of order-preserving keys, ties to the lower expert id by a min-reduction
+// (R-G1); sel_* in rank order.
+template <int NVT>
+__device__ __forceinline__ void topk_warp(const float (&v)[NVT], uint32_t taken, int k, int lane,
+                                          float (&sel_v)[ROUTE_MAX_K], int (&sel_e)[ROUTE_MAX_K]) {
+    uint32_t key[NVT];
+#pragma unroll
+    for (int i = 0; i < NVT; ++i) key[i] = ((taken >> i) & 1u) ? 0u : fkey(v[i]);
+#pragma unroll
+    for (int j = 0; j < ROUTE_MAX_K; ++j) {
+        if (j >= k) break;
+        uint32_t bk = 0u;
+        int bi = 0;
+#pragma unroll
+        for (int i = 0; i < NVT; ++i)
+            if (key[i] > bk) { bk = key[i]; bi = i; }          // ascending i: lowest expert on ties
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, bk);
+        const uint32_t mine = (bk == kmax && kmax != 0u) ? (uint32_t)(lane + 32 * bi) : 0xffffffffu;
+        const uint32_t emin = __reduce_min_sync(0xffffffffu, mine);
+        if (mine == emin) {
+#pragma unroll
+            for (int i = 0; i < NVT; ++i)
+                if (i == bi) key[i] = 0u;
+        }
+        sel_v[j] = fkey_inv(kmax);
+        sel_e[j] = (int)emin;
+    }
 }
 
 // ------------------------------------------------------------------ a2 + a3: top-k, gates, counters
@@ -112,26 +155,7 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
         }
         float sel_v[ROUTE_MAX_K];
         int sel_e[ROUTE_MAX_K];
-#pragma unroll
-        for (int j = 0; j < ROUTE_MAX_K; ++j) {
-            if (j >= k) break;
-            float bv = -INFINITY;
-            int be = 0x7fffffff;
-#pragma unroll
-            for (int i = 0; i < NVT; ++i) {
-                const int e = lane + 32 * i;
-                if (!((taken >> i) & 1u) && better(v[i], e, bv, be)) { bv = v[i]; be = e; }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-                if (better(ov, oe, bv, be)) { bv = ov; be = oe; }
-            }
-            if ((be & 31) == lane) taken |= 1u << (be >> 5);
-            sel_v[j] = bv;
-            sel_e[j] = be;
-        }
+        topk_warp<NVT>(v, taken, k, lane, sel_v, sel_e);
         // gates: softmax over the selected logits, sequential fp32 sum in rank order (R-G2)
         float ev[ROUTE_MAX_K];
         float sum = 0.0f;
@@ -141,16 +165,17 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
             ev[j] = dx_expf(__fsub_rn(sel_v[j], sel_v[0]));
             sum = (j == 0) ? ev[0] : __fadd_rn(sum, ev[j]);
         }
+        float my_ev = 0.0f;                             // lane j < k handles rank j (no divergent loop)
+        int my_e = 0;
 #pragma unroll
-        for (int j = 0; j < ROUTE_MAX_K; ++j) {
-            if (j >= k) break;
-            if (lane == j) {
-                const float gte = __fdiv_rn(ev[j], sum);
-                idx_out[(size_t)t * k + j] = sel_e[j];
-                gate_out[(size_t)t * k + j] = gte;
-                atomicAdd(&cnt_s[sel_e[j]], 1u);
-                atomicAdd(&mass_s[sel_e[j]], (u64)rintf(__fmul_rn(gte, 16777216.0f)));
-            }
+        for (int j = 0; j < ROUTE_MAX_K; ++j)
+            if (j == lane) { my_ev = ev[j]; my_e = sel_e[j]; }
+        if (lane < k) {
+            const float gte = __fdiv_rn(my_ev, sum);
+            idx_out[(size_t)t * k + lane] = my_e;
+            gate_out[(size_t)t * k + lane] = gte;
+            atomicAdd(&cnt_s[my_e], 1u);
+            atomicAdd(&mass_s[my_e], (u64)rintf(__fmul_rn(gte, 16777216.0f)));
         }
     }
     __syncthreads();
@@ -172,6 +197,157 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
     __threadfence();
     scan_tail(hist, gridDim.x, E, base, off, act_e, n_act, rs);
     if (threadIdx.x == 0) *done = 0;
+}
+
+// ------------------------------------------------------------------ a2-a4 in ONE block (decode batches)
+// T*k <= ROUTE1_MAX_ENT: top-k + gates + counters (as k_route), then the offsets scan, the active list and
+// the stable placement (entry i's row = off[e] + #{i' < i : e_i' = e}) all in shared memory -- no
+// cross-block completion counter, no second launch for the ranks.
+#define ROUTE1_MAX_ENT 512
+#define ROUTE1_CHUNKS 16
+template <typename Tv>
+__device__ Tv block_excl_scan(Tv v, Tv* tmp, Tv* total);
+template <int NVT>
+__global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits, int T, int E, int k, int e_lo,
+                                                int e_cnt, int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
+                                                uint32_t* __restrict__ cnt_acc, u64* __restrict__ mass_acc,
+                                                int32_t* __restrict__ off, int32_t* __restrict__ act_e,
+                                                int32_t* __restrict__ n_act, int32_t* __restrict__ perm,
+                                                int32_t* __restrict__ inv, RouteStats rs) {
+    __shared__ int16_t ent_s[ROUTE1_MAX_ENT];                // expert of every entry (t*k + j)
+    __shared__ uint32_t gm_s[ROUTE1_MAX_ENT];                // rint(gate * 2^24) of every entry (R-H1)
+    __shared__ int32_t tmp[32];
+    __shared__ int32_t total_s, na_s;
+    extern __shared__ __align__(16) uint8_t dyn_s[];
+    float* lg_s = reinterpret_cast<float*>(dyn_s);                              // [T][E] logits of the batch
+    uint32_t* cmass = reinterpret_cast<uint32_t*>(lg_s + (size_t)T * E);        // [chunk][expert] mass
+    int16_t* chist = reinterpret_cast<int16_t*>(cmass + ROUTE1_CHUNKS * E);     // [chunk][expert] counts, bases
+    for (int i = threadIdx.x; i < ROUTE1_CHUNKS * E; i += blockDim.x) { chist[i] = 0; cmass[i] = 0; }
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    {
+        const int n4 = T * E / 4;                            // E % 4 == 0 (route1_ok)
+        const float4* src = reinterpret_cast<const float4*>(logits);
+        float4* dst = reinterpret_cast<float4*>(lg_s);
+#pragma unroll 4
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    // a2 + a3: one warp per token, k rounds of (value desc, id asc) warp arg-max, gates (R-G1, R-G2)
+    for (int t = warp; t < T; t += nwarps) {
+        float v[NVT];
+        uint32_t taken = 0;
+        const float* lrow = lg_s + (size_t)t * E;
+#pragma unroll
+        for (int i = 0; i < NVT; ++i) {
+            const int e = lane + 32 * i;
+            v[i] = e < E ? lrow[e] : -INFINITY;
+            if (e >= E) taken |= 1u << i;
+        }
+        float sel_v[ROUTE_MAX_K];
+        int sel_e[ROUTE_MAX_K];
+        topk_warp<NVT>(v, taken, k, lane, sel_v, sel_e);
+        float ev[ROUTE_MAX_K];
+        float sum = 0.0f;
+#pragma unroll
+        for (int j = 0; j < ROUTE_MAX_K; ++j) {
+            if (j >= k) break;
+            ev[j] = dx_expf(__fsub_rn(sel_v[j], sel_v[0]));
+            sum = (j == 0) ? ev[0] : __fadd_rn(sum, ev[j]);
+        }
+        float my_ev = 0.0f;                             // lane j < k handles rank j (no divergent loop)
+        int my_e = 0;
+#pragma unroll
+        for (int j = 0; j < ROUTE_MAX_K; ++j)
+            if (j == lane) { my_ev = ev[j]; my_e = sel_e[j]; }
+        if (lane < k) {
+            const float gte = __fdiv_rn(my_ev, sum);
+            idx_out[(size_t)t * k + lane] = my_e;
+            gate_out[(size_t)t * k + lane] = gte;
+            ent_s[t * k + lane] = (int16_t)my_e;
+            gm_s[t * k + lane] = (uint32_t)rintf(__fmul_rn(gte, 16777216.0f));
+        }
+    }
+    __syncthreads();
+    // per 32-entry chunk (one warp each): same-expert groups by match_any -> in-chunk rank, count, mass
+    const int n = T * k;
+    const int ci = warp, i = warp * 32 + lane;               // n <= 512 = 16 warps x 32 entries
+    const bool have = i < n;
+    const int ei = have ? ent_s[i] : -1 - lane;
+    const unsigned same = __match_any_sync(0xffffffffu, ei);
+    const int rk = __popc(same & ((1u << lane) - 1u));
+    const uint32_t gsum = __reduce_add_sync(same, have ? gm_s[i] : 0u);
+    if (have && rk == 0) {
+        chist[ci * E + ei] = (int16_t)__popc(same);
+        cmass[ci * E + ei] = gsum;
+    }
+    __syncthreads();
+    // per expert (thread e): totals in chunk order (integer sums: order-free), offsets scan, active list,
+    // hotness accumulators, chunk bases
+    const int e = threadIdx.x;
+    uint32_t c = 0;
+    u64 m = 0;
+    if (e < E) {
+#pragma unroll
+        for (int c2 = 0; c2 < ROUTE1_CHUNKS; ++c2) {
+            c += (uint32_t)chist[c2 * E + e];
+            m += cmass[c2 * E + e];
+        }
+        if (c) {
+            const int le = e - e_lo;
+            if (le >= 0 && le < e_cnt && cnt_acc) {
+                atomicAdd(&cnt_acc[le], c);
+                atomicAdd(&mass_acc[le], m);
+            }
+        }
+    }
+    const int32_t o = block_excl_scan<int32_t>((int32_t)c, tmp, &total_s);
+    const int32_t a = block_excl_scan<int32_t>(c > 0 ? 1 : 0, tmp, &na_s);
+    if (e < E) {
+        off[e] = o;
+        if (c) act_e[a] = e;
+        int run = o;
+#pragma unroll
+        for (int c2 = 0; c2 < ROUTE1_CHUNKS; ++c2) {
+            const int b = chist[c2 * E + e];
+            chist[c2 * E + e] = (int16_t)run;
+            run += b;
+        }
+    }
+    if (rs.stats && rs.tier) {                               // algorithmic weight bytes of this forward
+        __shared__ int32_t nhi_s;                             // (profiling): 3 atomics per forward
+        const int32_t hi = (e < E && c && rs.tier[e]) ? 1 : 0;
+        block_excl_scan<int32_t>(hi, tmp, &nhi_s);
+        if (threadIdx.x == 0) {
+            const u64 nh = (u64)nhi_s, nl = (u64)na_s - nh;
+            atomicAdd(&rs.stats[0], nh * rs.b10 + nl * rs.b00);
+            atomicAdd(&rs.stats[1], nh * rs.b11 + nl * rs.b01);
+            atomicAdd(&rs.stats[2], (u64)na_s);
+        }
+    }
+    if (threadIdx.x == 0) { off[E] = total_s; *n_act = na_s; }
+    __syncthreads();
+    // a4: stable placement (entry order t asc, j asc): pos = off[e] + earlier chunks + in-chunk rank
+    if (have) {
+        const int pos = chist[ci * E + ei] + rk;
+        perm[pos] = i;
+        inv[i] = pos;
+    }
+}
+
+// x rows gathered into the permuted order (B operand of the gate/up GEMM): Xp[inv[i]] = x[i / k]; one
+// warp per entry, 16 B per lane per step
+__global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ inv, int n, int k, const __nv_bfloat16* __restrict__ x,
+                                                int H, __nv_bfloat16* __restrict__ Xp) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int pos = inv[i];
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(i / k) * H);
+    uint4* dst = reinterpret_cast<uint4*>(Xp + (size_t)pos * H);
+    for (int h = lane; h < H / 8; h += 32) dst[h] = src[h];
 }
 
 // ------------------------------------------------------------------ a4: offsets + stable scatter
@@ -226,19 +402,22 @@ __device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int
         if (e >= E) continue;
         const int32_t oe = h ? o + t0 : o;
         off[e] = oe;
-        if (tot > 0) {
-            act_e[ai++] = e;
-            if (rs.stats && rs.tier) {          // algorithmic weight bytes of this forward (profiling)
-                const int ti = rs.tier[e];
-                atomicAdd(&rs.stats[0], ti ? rs.b10 : rs.b00);
-                atomicAdd(&rs.stats[1], ti ? rs.b11 : rs.b01);
-                atomicAdd(&rs.stats[2], 1ull);
-            }
-        }
+        if (tot > 0) act_e[ai++] = e;
         int32_t run = oe;
         for (int b = 0; b < nblk; ++b) {
             base[(size_t)b * E + e] = run;
             run += __ldcg(hist + (size_t)b * E + e);
+        }
+    }
+    if (rs.stats && rs.tier) {                  // algorithmic weight bytes of this forward (profiling)
+        __shared__ int32_t nhi_s;
+        const int32_t hi = (e0 < E && t0 > 0 && rs.tier[e0] ? 1 : 0) + (e1 < E && t1 > 0 && rs.tier[e1] ? 1 : 0);
+        block_excl_scan<int32_t>(hi, tmp, &nhi_s);
+        if (threadIdx.x == 0) {
+            const u64 nh = (u64)nhi_s, nl = (u64)na_s - nh;
+            atomicAdd(&rs.stats[0], nh * rs.b10 + nl * rs.b00);
+            atomicAdd(&rs.stats[1], nh * rs.b11 + nl * rs.b01);
+            atomicAdd(&rs.stats[2], (u64)na_s);
         }
     }
     if (threadIdx.x == 0) { off[E] = total_s; *n_act = na_s; }
@@ -392,23 +571,11 @@ __global__ void k_counts_from(const int32_t* __restrict__ idx, const float* __re
 
 int route_blocks(int T) { return (T + ROUTE_TOK_PER_BLK - 1) / ROUTE_TOK_PER_BLK; }
 
-void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E,
-                   int H, float* logits, cudaStream_t st) {
+void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E, int H,
+                   float* logits, cudaStream_t st) {
     if (T <= 0) return;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_router<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_router<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    // 4 warps (experts) per block: decode batches still spread the 4 KB router rows over >= 32 blocks
-    if (T <= 4) {
-        dim3 grid((E + 3) / 4, (T + 3) / 4);
-        dx_launch(k_router<4>, grid, dim3(128), 4 * H * sizeof(float), st, g_dx_pdl, x, wr, bias, T, E, H, logits);
-    } else {
-        dim3 grid((E + 3) / 4, (T + 7) / 8);
-        dx_launch(k_router<8>, grid, dim3(128), 8 * H * sizeof(float), st, g_dx_pdl, x, wr, bias, T, E, H, logits);
-    }
+    dim3 grid((E + 7) / 8, (T + 15) / 16);
+    dx_launch(k_router, grid, dim3(512), 0, st, g_dx_pdl, x, wr, bias, T, E, H, logits);
 }
 
 void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
@@ -422,6 +589,36 @@ void launch_route(const float* logits, int T, int E, int k, int e_lo, const Rout
     else if (E <= 256) dx_launch(k_route<8>, dim3(nb), dim3(256), 0, st, g_dx_pdl, DX_ROUTE_ARGS);
     else               dx_launch(k_route<16>, dim3(nb), dim3(256), 0, st, g_dx_pdl, DX_ROUTE_ARGS);
 #undef DX_ROUTE_ARGS
+}
+
+bool route1_ok(int T, int E, int k) { return T * k <= ROUTE1_MAX_ENT && E <= 512 && E % 4 == 0 && T * E <= 32768; }
+
+void launch_route1(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
+                   uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st) {
+    if (T <= 0) return;
+    const int ec = cnt_acc ? E : 0;
+    RouteStats rs{tier, bytes[0][0], bytes[0][1], bytes[1][0], bytes[1][1], ws.stats};
+#define DX_R1_ARGS logits, T, E, k, e_lo, ec, ws.idx, ws.gate, cnt_acc, mass_acc, ws.off, ws.act_e, ws.n_act, \
+                   ws.perm, ws.inv, rs
+    static bool attr = false;
+    if (!attr) {
+        const int mx = 32768 * 4 + ROUTE1_CHUNKS * ROUTE_MAX_E * 6;
+        cudaFuncSetAttribute(k_route1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_route1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_route1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        attr = true;
+    }
+    const size_t sm = (size_t)T * E * 4 + (size_t)ROUTE1_CHUNKS * E * 6;
+    if (E <= 128)      dx_launch(k_route1<4>, dim3(1), dim3(512), sm, st, g_dx_pdl, DX_R1_ARGS);
+    else if (E <= 256) dx_launch(k_route1<8>, dim3(1), dim3(512), sm, st, g_dx_pdl, DX_R1_ARGS);
+    else               dx_launch(k_route1<16>, dim3(1), dim3(512), sm, st, g_dx_pdl, DX_R1_ARGS);
+#undef DX_R1_ARGS
+}
+
+void launch_gather(int T, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp, cudaStream_t st) {
+    const int n = T * k;
+    if (n <= 0 || !Xp) return;
+    dx_launch(k_gather, dim3((n + 7) / 8), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.inv, n, k, x, H, Xp);
 }
 
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
