@@ -30,7 +30,7 @@ UNIT = "layer-tokens/s"
 
 # C2: Qwen3-30B-A3B expert geometry, 24e9 B expert budget per GPU, bf16/int4.
 C2 = dict(L=48, E=128, k=8, H=2048, I=768, g=128, high=16, low=4, budget=24 * 10**9, s=1,
-          alpha=0.95, Tp=16, W=32, dwell=32, lag=4, zipf=1.2, drift=32, frac=0.25, n_top=24)
+          alpha=0.95, Tp=16, W=32, dwell=16, lag=4, zipf=1.2, drift=32, frac=0.25, n_top=24)
 
 
 def parse():

@@ -13,7 +13,7 @@ LIB = os.path.join(HERE, "libdx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
-         "--expt-relaxed-constexpr", "-I", INCLUDE]
+         "--expt-relaxed-constexpr", "-I", INCLUDE] + os.environ.get("DX_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -54,6 +54,7 @@ struct dx_pool_s {
     __nv_bfloat16* act = nullptr;
     __nv_bfloat16* Y = nullptr;
     int32_t* err_flag = nullptr;
+    int32_t* gemm_sched = nullptr;      // [phase][ticket counter, CTAs done] of the grouped GEMMs (self-resetting)
     int2* manual_cmds = nullptr;
     int32_t* manual_status = nullptr;
     const uint8_t** hi_img_dev = nullptr;   // [L * E_loc]
@@ -290,7 +291,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     }
     const size_t lg_rows = (size_t)T;
     size_t ws_bytes = lg_rows * p->E * 4 + n_ent * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
-                      (size_t)(p->E + 1) * 8 + n_ent * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8;
+                      (size_t)(p->E + 1) * 8 + n_ent * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8 + 256;
     if (G > 1)   // dispatch-side routing workspace (global experts, local tokens)
         ws_bytes += lg_rows * p->E * 4 + (size_t)T * k * 16 + (size_t)route_blocks(T) * p->E * 8 +
                     (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
@@ -361,6 +362,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     p->Y = carve<__nv_bfloat16>(q, n_ent * p->H);
     p->Xp = carve<__nv_bfloat16>(q, n_ent * p->H);
     p->err_flag = carve<int32_t>(q, 1);
+    p->gemm_sched = carve<int32_t>(q, 4);
     p->manual_cmds = carve<int2>(q, 1024);
     p->manual_status = carve<int32_t>(q, 1024);
     uint8_t* stage_master = carve<uint8_t>(q, (size_t)3 * p->I * p->H * 2);
@@ -450,6 +452,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         DX_CUDA(cudaMemcpyAsync(c.cap_hi, chi.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
         DX_CUDA(cudaMemcpyAsync(c.plan_n, pn.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
         DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
+        DX_CUDA(cudaMemsetAsync(p->gemm_sched, 0, 16, p->cs));
         DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
         DX_CUDA(cudaMemsetAsync(w.done, 0, 4, p->cs));
         if (G > 1) DX_CUDA(cudaMemsetAsync(p->ws_src.done, 0, 4, p->cs));
@@ -666,7 +669,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         ga.layer = a.arena_layer; ga.hi_base = p->hi_base; ga.hi = p->hi; ga.lo = p->lo;
         ga.tier = a.tier; ga.slot = a.slot; ga.off = ws.off; ga.act_e = ws.act_e; ga.n_act = ws.n_act;
         ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = k;
-        ga.act = p->act; ga.Y = p->Y;
+        ga.act = p->act; ga.Y = p->Y; ga.sched = p->gemm_sched;
         static const int dbg = [] { const char* s = getenv("DX_GEMM_DBG"); return s ? atoi(s) : 0; }();
         ga.dbg = dbg;
         GemmMaps gm = p->gmaps[layer];

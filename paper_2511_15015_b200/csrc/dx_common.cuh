@@ -163,7 +163,7 @@ struct RouteWs {
     int32_t* hist;        // [nblk][E]
     int32_t* base;        // [nblk][E]
     int32_t* off;         // [E+1]
-    int32_t* act_e;       // [E] active experts (ascending)
+    int32_t* act_e;       // [E] active experts: HIGH tier first, each tier ascending
     int32_t* n_act;       // [1]
     int32_t* perm;        // [T*k] entry (t*k+j) at each permuted row
     int32_t* inv;         // [T*k] permuted row of entry
@@ -241,6 +241,8 @@ struct GemmArgs {
     int H, I, g, k;
     __nv_bfloat16* act;
     __nv_bfloat16* Y;
+    int* sched;                     // [phase][ticket counter, CTAs done]: dynamic work-item hand-out, zero
+                                    // between launches (the last CTA of a launch resets it)
     int dbg;                        // performance experiments only (DX_GEMM_DBG): 4 skip the A-in-TMEM MMAs,
                                     // 5 skip the dequant transform, 6 both
 };

@@ -15,7 +15,11 @@
 // 32-column TMEM A buffers (lane = weight row) that feeds tcgen05.mma with A in tensor memory.
 // Gate/up items take 64 gate rows (A rows 0-63) and the matching 64 up rows (64-127); the SwiGLU pairs
 // meet through a small smem exchange in the epilogue.
-// Warp roles (448 threads): 0 TMA producer, 1 TMEM owner + MMA issuer, 2-9 transform, 10-13 epilogue.
+// Warp roles (480 threads): 0 TMA producer, 1 TMEM owner + MMA issuer, 2-9 transform, 10-13 epilogue,
+// 14 scheduler.  Work items are handed out dynamically (one global ticket counter per launch, items in
+// the routing kernel's HIGH-tier-first order, so the heavy items go first and the tail is a light one):
+// the scheduler warp claims a ticket, decodes it and publishes it through a 2-entry smem ring that every
+// other role walks in the same order.
 #include "dx_common.cuh"
 #include "dx_sm100.cuh"
 #include <cstdio>
@@ -26,14 +30,22 @@ using namespace sm100;
 
 namespace {
 
-constexpr int GEMM_THREADS = 448;
+#ifndef DX_GEMM_NTW
+#define DX_GEMM_NTW 16
+#endif
+constexpr int NTW = DX_GEMM_NTW;              // dequant transform warps (groups of 4: one per TMEM lane quarter)
+constexpr int NG = NTW / 4;                   // transform groups
+constexpr int W_EPI = 2 + NTW;                // first epilogue warp
+constexpr int W_SCHED = W_EPI + 4;            // scheduler warp
+constexpr int GEMM_THREADS = 32 * (W_SCHED + 1);
 constexpr int KCH = 64;                       // K elements per chunk (128 B of bf16 per row)
 constexpr int STAGES = 6;
 constexpr int A_BYTES = 128 * 128;            // A / raw region per stage
 constexpr int B_REGION = 16384;               // B region per stage
 constexpr int STAGE_BYTES = A_BYTES + B_REGION;
 constexpr int XCH_BYTES = 64 * 32 * 4;        // epilogue SwiGLU exchange: 64 rows x 32 columns fp32
-constexpr int MAXIT = 64;                     // work items per CTA decoded once into smem (rest: on the fly)
+constexpr int RING = 2;                       // claimed work items in flight per CTA (small: balance)
+constexpr int N_CONSUMERS = W_SCHED;          // warps that read the item ring (all but the scheduler)
 constexpr int GTAB = 16;                      // scale/zero groups per row staged in smem per item (G <= 16)
 constexpr int TAB_BYTES = 128 * GTAB * 3;     // one item's table: [128 rows][G] bf16 scales, then u8 zeros
 
@@ -44,7 +56,7 @@ struct Cfg {
     static constexpr int NBMAX = DEC ? 64 : 128;
     static constexpr int ACH = DEC ? 4 : 1;                    // K chunks per TMEM A buffer (32 columns each)
     static constexpr int NA = (512 - 2 * NBMAX) / (32 * ACH);  // TMEM A buffers: 3 (decode) / 8 (prefill)
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + MAXIT * 16 + 2 * TAB_BYTES;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES;
     __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : 128; }
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
@@ -118,34 +130,35 @@ __device__ __forceinline__ int4 decode_raw(const GemmArgs& a, int item, int nmb)
     const int r0 = a.off[e];
     return make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
 }
-// the i-th item of this CTA (item = blockIdx.x + i * gridDim.x): from the smem table when i < MAXIT
-__device__ __forceinline__ Item get_item(const GemmArgs& a, const int4* itab, int i, int item, int nmb) {
-    const int4 v = i < MAXIT ? itab[i] : decode_raw(a, item, nmb);
-    Item it;
-    it.mb = item % nmb;
-    it.r0 = v.x;
-    it.m = v.y;
-    it.slot = v.z;
-    it.ti = v.w;
-    it.bits = it.ti ? a.hi.bits : a.lo.bits;
-    return it;
-}
+// One published work item of the ring: decoded fields + the ticket (>= n_items: no more work).
+struct Tick {
+    int4 v;            // {r0, m, slot, tier}
+    int item, pad[3];
+};
 
-// the same, with every field made warp-uniform (producer / MMA warps)
-__device__ __forceinline__ Item get_item_u(const GemmArgs& a, const int4* itab, int i, int item, int nmb) {
-    int4 v = i < MAXIT ? itab[i] : decode_raw(a, item, nmb);
+// The ii-th item of this CTA, from the ring (every field warp-uniform: read by lane 0, broadcast).  The
+// warp then releases the ring entry.  Returns false after the last item.
+__device__ __forceinline__ bool take_item(const GemmArgs& a, const Tick* ring, uint64_t* tkfull, uint64_t* tkempty,
+                                          int ii, int n_items, int nmb, Item& it) {
+    const int sl = ii % RING;
+    gwait(&tkfull[sl], (ii / RING) & 1, 10);
+    int4 v = ring[sl].v;
+    int item = ring[sl].item;
     v.x = __shfl_sync(0xffffffffu, v.x, 0);
     v.y = __shfl_sync(0xffffffffu, v.y, 0);
     v.z = __shfl_sync(0xffffffffu, v.z, 0);
     v.w = __shfl_sync(0xffffffffu, v.w, 0);
-    Item it;
+    item = __shfl_sync(0xffffffffu, item, 0);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&tkempty[sl]);
+    if (item >= n_items) return false;
     it.mb = item % nmb;
     it.r0 = v.x;
     it.m = v.y;
     it.slot = v.z;
     it.ti = v.w;
     it.bits = it.ti ? a.hi.bits : a.lo.bits;
-    return it;
+    return true;
 }
 
 __device__ __forceinline__ int box_rows(int nvalid) {        // B tile rows: power of two in [16, 128]
@@ -170,11 +183,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     uint64_t* tempty = tfull + 2;                         // [2] accumulator drained
     uint64_t* tabfull = tempty + 2;                       // [2] scale/zero table of an item landed
     uint64_t* tabempty = tabfull + 2;                     // [2] transform finished with the table
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tabempty + 2);
+    uint64_t* tkfull = tabempty + 2;                      // [RING] item published by the scheduler
+    uint64_t* tkempty = tkfull + RING;                    // [RING] every consumer warp read the item
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tkempty + RING);
     int32_t* ent_s = reinterpret_cast<int32_t*>(tmem_slot + 4);     // [128] epilogue: entry ids
     float* gate_s = reinterpret_cast<float*>(ent_s + 128);           // [128] epilogue: gates
-    int4* itab = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(bars) + 2048);   // [MAXIT] items
-    uint8_t* tabs = reinterpret_cast<uint8_t*>(itab + MAXIT);        // [2][TAB_BYTES]
+    Tick* ring = reinterpret_cast<Tick*>(reinterpret_cast<uint8_t*>(bars) + 2048);   // [RING] items
+    uint8_t* tabs = reinterpret_cast<uint8_t*>(ring + RING);         // [2][TAB_BYTES]
 
     const int K = PHASE == 0 ? a.H : a.I;
     const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
@@ -188,11 +203,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     // prologue independent of the predecessor kernels (overlaps their tail under PDL)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? 256 : 128); mbar_init(&aempty[b], 1); }
+        for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? 32 * NTW : 128); mbar_init(&aempty[b], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128);
-            mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], 256);
+            mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], 32 * NTW);
         }
+        for (int b = 0; b < RING; ++b) { mbar_init(&tkfull[b], 1); mbar_init(&tkempty[b], N_CONSUMERS); }
         fence_mbar_init();
         for (int i = 0; i < 4; ++i) tma_prefetch(&maps.xb[i]);
     }
@@ -200,12 +216,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
     const int n_items = a.n_act[0] * nmb;
-    // this CTA's items, decoded once by all threads (the per-item dependent loads leave every role's
-    // critical path)
-    for (int i = threadIdx.x; i < MAXIT; i += GEMM_THREADS) {
-        const int item = blockIdx.x + i * gridDim.x;
-        if (item < n_items) itab[i] = decode_raw(a, item, nmb);
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -217,8 +227,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         // with warp-uniform values (uniform registers, no per-lane serialisation); lane 0 issues
         int st = 0, tc = 0;
         uint32_t ph = 0;
-        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
-            const Item w = get_item_u(a, itab, ii, item, nmb);
+        Item w;
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
             const bool qt = w.bits != 16;
             if (qt && tab_ok) {
                 // this item's scales / zeros: contiguous row spans of the slot's [rows][G] tables
@@ -282,8 +292,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         // (tcgen05.mma / commit are single-thread instructions; commits must come from the issuing thread)
         int st = 0, ab = 0, cc = 0;
         uint32_t ph = 0, aph = 0;
-        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
-            const Item w = get_item_u(a, itab, ii, item, nmb);
+        Item w;
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
             const int nb = C::nb(w.bits), ks = C::ks(w.bits);
             for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
                 const int rb = box_rows(min(nb, w.m - n0));
@@ -342,11 +352,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 __syncwarp();
             }
         }
-    } else if (warp < 10) {
+    } else if (warp < W_EPI) {
         // ------------------------------------------------ dequant transform (8 warps, thread = A row =
         // TMEM lane).  Decode: every TMEM A buffer holds ACH = 4 chunks, group g dequantises chunks 2g and
         // 2g+1 of each; prefill: one chunk per buffer, the two groups take alternate buffers.
-        const int grp = (warp - 2) >> 2;
+        const int grp = (warp - 2) >> 2;              // 0..NG-1
         const int qa = warp & 3;
         const int r = 32 * qa + lane;
         const uint32_t rsw = r & 7;                        // 128 B swizzle phase of this row
@@ -358,8 +368,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         asm volatile("" : "+r"(magic));
         int st = 0, ab = 0, tc = 0, nbuf = 0;
         uint32_t ph = 0, aph = 0;
-        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
-            const Item w = get_item(a, itab, ii, item, nmb);
+        Item w;
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
             if (w.bits == 16) {                           // bf16 stages need no transform: observe their phases
                 const int nst = ((w.m + C::nb(16) - 1) / C::nb(16)) * nk;
                 for (int s = 0; s < nst; ++s) {
@@ -405,12 +415,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                             const int cab = ab;
                             const uint32_t caph = aph;
                             if (++ab == C::NA) { ab = 0; aph ^= 1; }
-                            if (!DEC && (nbuf & 1) != grp) continue;   // prefill: the other group's buffer
+                            if (!DEC && (nbuf % NG) != grp) continue;  // prefill: another group's buffer
                             gwait(&aempty[cab], caph ^ 1, 8);
                             if (a.dbg != 5 && a.dbg != 6) {
 #pragma unroll
-                                for (int h = 0; h < (DEC ? 2 : 1); ++h) {
-                                    const int jj = DEC ? 2 * grp + h : 0;   // chunk within the buffer
+                                for (int h = 0; h < (DEC ? C::ACH / NG : 1); ++h) {
+                                    const int jj = DEC ? (C::ACH / NG) * grp + h : 0;   // chunk within the buffer
                                     const int j = j0 + jj;                   // chunk within the stage
                                     if (j < kc) {
                                         const int k0 = (kb0 + j) * KCH;
@@ -455,13 +465,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 ++tc;
             }
         }
+    } else if (warp == W_SCHED) {
+        // ------------------------------------------------ scheduler: claim a ticket, decode it, publish it
+        // (the ring is only RING deep, so a CTA never hoards work another SM could start sooner)
+        int* ctr = a.sched + 2 * PHASE;
+        for (int ii = 0;; ++ii) {
+            const int sl = ii % RING;
+            gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11);
+            int item = 0;
+            if (lane == 0) {
+                item = atomicAdd(ctr, 1);
+                ring[sl].v = item < n_items ? decode_raw(a, item, nmb) : make_int4(0, 0, 0, 0);
+                ring[sl].item = item;
+                mbar_arrive(&tkfull[sl]);
+            }
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= n_items) break;
+        }
     } else {
-        // ------------------------------------------------ epilogue (128 threads, warps 10-13)
+        // ------------------------------------------------ epilogue (128 threads, warps W_EPI..W_EPI+3)
         const int q = warp & 3;                         // TMEM lane quarter this warp may access
-        const int et = threadIdx.x - 320;               // 0..127
+        const int et = threadIdx.x - 32 * W_EPI;        // 0..127
         int cc = 0;
-        for (int item = blockIdx.x, ii = 0; item < n_items; item += gridDim.x, ++ii) {
-            const Item w = get_item(a, itab, ii, item, nmb);
+        Item w;
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
             const int nb = C::nb(w.bits);
             for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
                 const int buf = cc & 1;
@@ -522,6 +549,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
+    if (threadIdx.x == 0) {                           // the last CTA out resets the ticket counter for the
+        int* ctr = a.sched + 2 * PHASE;                // next launch (which reads it only after griddepcontrol.wait)
+        __threadfence();
+        if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+            atomicExch(ctr, 0);
+            atomicExch(ctr + 1, 0);
+        }
+    }
 }
 
 template <int PHASE, bool DEC>
@@ -554,12 +589,13 @@ void gemm_trap_init() {
 }
 static const char* const k_trap_names[] = {"?", "tabempty (producer)", "empty (producer)", "tempty (MMA)", "full (MMA)",
                                            "aready (MMA)", "tabfull (transform)", "full (transform)",
-                                           "aempty (transform)", "tfull (epilogue)"};
+                                           "aempty (transform)", "tfull (epilogue)", "tkfull (item ring)",
+                                           "tkempty (scheduler)"};
 int gemm_trap_report(char* buf, size_t n) {
     if (!g_trap_host || (g_trap_host[0] >> 16) != 0xDEADu) return 0;
     const uint32_t tag = g_trap_host[0] & 0xFFFFu;
     return snprintf(buf, n, " [k_gemm watchdog: wait on %s, parity %u, block %u, thread %u]",
-                    tag < 10 ? k_trap_names[tag] : "?", g_trap_host[1], g_trap_host[2], g_trap_host[3]);
+                    tag < 12 ? k_trap_names[tag] : "?", g_trap_host[1], g_trap_host[2], g_trap_host[3]);
 }
 
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st) {

@@ -304,9 +304,13 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
     }
     const int32_t o = block_excl_scan<int32_t>((int32_t)c, tmp, &total_s);
     const int32_t a = block_excl_scan<int32_t>(c > 0 ? 1 : 0, tmp, &na_s);
+    // active list HIGH tier first (the grouped GEMMs hand out work items in this order, heaviest first)
+    __shared__ int32_t nhi_s;
+    const int32_t hi = (e < E && c && rs.tier && rs.tier[e]) ? 1 : 0;
+    const int32_t ah = block_excl_scan<int32_t>(hi, tmp, &nhi_s);
     if (e < E) {
         off[e] = o;
-        if (c) act_e[a] = e;
+        if (c) act_e[hi ? ah : nhi_s + (a - ah)] = e;
         int run = o;
 #pragma unroll
         for (int c2 = 0; c2 < ROUTE1_CHUNKS; ++c2) {
@@ -316,10 +320,7 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
         }
     }
     if (rs.stats && rs.tier) {                               // algorithmic weight bytes of this forward
-        __shared__ int32_t nhi_s;                             // (profiling): 3 atomics per forward
-        const int32_t hi = (e < E && c && rs.tier[e]) ? 1 : 0;
-        block_excl_scan<int32_t>(hi, tmp, &nhi_s);
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0) {                               // (profiling): 3 atomics per forward
             const u64 nh = (u64)nhi_s, nl = (u64)na_s - nh;
             atomicAdd(&rs.stats[0], nh * rs.b10 + nl * rs.b00);
             atomicAdd(&rs.stats[1], nh * rs.b11 + nl * rs.b01);
@@ -394,7 +395,11 @@ __device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int
     }
     const int32_t o = block_excl_scan<int32_t>(t0 + t1, tmp, &total_s);
     const int32_t a = block_excl_scan<int32_t>((t0 > 0) + (t1 > 0), tmp, &na_s);
-    int32_t ai = a;
+    // active list HIGH tier first (the grouped GEMMs hand out work items in this order, heaviest first)
+    __shared__ int32_t nhi_s;
+    const bool h0 = e0 < E && t0 > 0 && rs.tier && rs.tier[e0], h1 = e1 < E && t1 > 0 && rs.tier && rs.tier[e1];
+    const int32_t ah = block_excl_scan<int32_t>((int32_t)h0 + (int32_t)h1, tmp, &nhi_s);
+    int32_t ahi = ah, alo = nhi_s + (a - ah);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int e = h ? e1 : e0;
@@ -402,7 +407,7 @@ __device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int
         if (e >= E) continue;
         const int32_t oe = h ? o + t0 : o;
         off[e] = oe;
-        if (tot > 0) act_e[ai++] = e;
+        if (tot > 0) act_e[(h ? h1 : h0) ? ahi++ : alo++] = e;
         int32_t run = oe;
         for (int b = 0; b < nblk; ++b) {
             base[(size_t)b * E + e] = run;
@@ -410,9 +415,6 @@ __device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int
         }
     }
     if (rs.stats && rs.tier) {                  // algorithmic weight bytes of this forward (profiling)
-        __shared__ int32_t nhi_s;
-        const int32_t hi = (e0 < E && t0 > 0 && rs.tier[e0] ? 1 : 0) + (e1 < E && t1 > 0 && rs.tier[e1] ? 1 : 0);
-        block_excl_scan<int32_t>(hi, tmp, &nhi_s);
         if (threadIdx.x == 0) {
             const u64 nh = (u64)nhi_s, nl = (u64)na_s - nh;
             atomicAdd(&rs.stats[0], nh * rs.b10 + nl * rs.b00);

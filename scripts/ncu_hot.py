@@ -1,18 +1,20 @@
-"""Top SASS lines by warp-stall samples from an ncu report: python scripts/ncu_hot.py rep.ncu-rep [kernel-regex] [n]"""
+"""Top SASS lines by warp-stall samples from an ncu report:
+python scripts/ncu_hot.py rep.ncu-rep [kernel-block-index] [n]   (block = n-th profiled kernel in the report)"""
 import csv
 import io
 import subprocess
 import sys
 
 rep = sys.argv[1]
-kr = sys.argv[2] if len(sys.argv) > 2 else "k_gemm"   # e.g. "k_gemm<\\(int\\)1"
+kb = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name",
-                      "regex:" + kr, "--launch-count", "1"], capture_output=True, text=True).stdout
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
 lines = out.splitlines()
-start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
-end = next((i for i in range(start + 1, len(lines)) if lines[i].startswith('"Kernel Name"')), len(lines))
-rows = list(csv.reader(io.StringIO("\n".join(lines[start:end]))))
+heads = [i for i, l in enumerate(lines) if l.startswith('"Kernel Name"')] + [len(lines)]
+print(lines[heads[kb]][:120])
+block = lines[heads[kb] + 1:heads[kb + 1]]
+rows = list(csv.reader(io.StringIO("\n".join(block))))
 h = rows[0]
 S = h.index("Warp Stall Sampling (All Samples)")
 stalls = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
