@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--prefill-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--switch-stress", action="store_true",
+                    help="C5 (SURVEY 8(d)): one Q30B layer, n_hot swept 10%%..100%%, drift 0.5 every period; "
+                         "prints the C5 JSON line instead of the main one")
     return ap.parse_args()
 
 
@@ -379,6 +382,82 @@ def prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream):
             "weight_bytes_per_layer": sum(prof["weight_bytes"]) / max(prof["forwards"], 1)}
 
 
+def switch_stress(a):
+    """C5: one Qwen3-30B-A3B-shaped layer (E=128, bf16/int4, s=2 spares per tier) at
+    n_hot = 10 %..100 % of E, with the hot set drifting (half of the top-n_hot set rotates every period),
+    so the controller promotes and demotes every period.  Per n_hot and per workload (decode B=16,
+    prefill T=4096): device ms per step, transitions, side-stream switch latency (plan issue -> ready,
+    CUDA events on the side stream) and EXPOSED switch time = compute-stream stall at publication
+    (events around the cross-stream wait), as a fraction of the step time."""
+    import torch
+    import synth
+    from paper_2511_15015_b200 import dx
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    E, k, H, I, g, s_sp = 128, 8, 2048, 768, 128, 2
+    Tp, W, lag, alpha = 8, 16, 2, 0.9
+    arr, ptrs = host_masters(a.seed, 1, E, H, I, 0, 1)
+    S_h, S_l = dx.dx_slot_bytes(H, I, g, 16), dx.dx_slot_bytes(H, I, g, 4)
+    wr = torch.from_numpy(router_weights(a.seed, 0, E, H, a.router_scale).view(np.int16)).to(dev).view(torch.bfloat16)
+    stream = torch.cuda.current_stream()
+    rows = []
+    for n_hot in (13, 26, 38, 51, 64, 77, 90, 102, 115, 128):
+        budget = n_hot * S_h + (E - n_hot) * S_l + s_sp * (S_h + S_l)
+        for mode, T, steps in (("decode", 16, 48), ("prefill", 4096, 24)):
+            cfg = dx.dx_config()
+            cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = 1, E, k, H, I, g
+            cfg.high_bits, cfg.low_bits = 16, 4
+            cfg.expert_budget_bytes = budget
+            cfg.n_spare, cfg.ema_alpha = s_sp, alpha
+            cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = Tp, W, Tp, lag
+            cfg.max_tokens, cfg.ep_rank, cfg.ep_size = T, 0, 1
+            pool = dx.Pool(cfg, ptrs, stream)
+            assert pool.info.n_hot == n_hot, (pool.info.n_hot, n_hot)
+            total = W + Tp + steps + 1
+            bias = torch.stack([torch.from_numpy(synth.zipf_logp(
+                synth.rank_perm(a.seed, 0, ep, E, max(n_hot, 1), 0.5), 1.2)) for ep in range(total // Tp + 2)]).to(dev)
+            xs = [torch.from_numpy(synth.normal_bf16(a.seed, 700, i, 0, (T, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+                  for i in range(2)]
+            y = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+
+            def one(t):
+                pool.dx_moe_forward(0, xs[t & 1], T, y, router_w=wr, router_bias=bias[t // Tp])
+                pool.dx_hotness_update(0)
+                pool.dx_plan_precision(0)
+
+            for t in range(W):
+                one(t)
+            pool.dx_plan_precision(0)
+            for t in range(W, W + Tp):
+                one(t)
+            pool.dx_sync()
+            pool.dx_profile_read()
+            pool.dx_profile_enable(True)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for t in range(W + Tp, W + Tp + steps):
+                one(t)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            pr = pool.dx_profile_read()
+            pool.dx_profile_enable(False)
+            pool.close()
+            rows.append({"n_hot": n_hot, "hot_frac": n_hot / E, "mode": mode, "tokens": T, "steps": steps,
+                         "ms_per_step": ms / steps, "promotions": pr["promotions"], "demotions": pr["demotions"],
+                         "plans": pr["plans"], "switch_ms_mean": pr["xfer_ms"] / max(pr["plans"], 1),
+                         "switch_ms_max": pr["xfer_max_ms"], "exposed_ms": pr["exposed_ms"],
+                         "exposed_frac": pr["exposed_ms"] / ms if ms > 0 else None})
+    torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
+    return {"metric": "C5 precision-switch stress: exposed switch time / step time", "unit": "fraction",
+            "higher_is_better": False, "n_gpus": 1, "data": "synthetic",
+            "config": {"workload": "C5: one Q30B-shaped layer (E=128, k=8, H=2048, I=768, bf16/int4 g=128), "
+                                   "s=2 spares per tier, Tp=8, W=16, dwell=8, L=2, alpha=0.9, Zipf(1.2) router bias "
+                                   "with half of the top-n_hot set rotating every period"},
+            "value": max(r["exposed_frac"] for r in rows), "rows": rows}
+
+
 # ---------------------------------------------------------------------------------------- oracle arm
 def oracle_layer_sample(a, seconds=15.0, max_steps=None):
     """The CPU oracle (as it stands) on a bounded sample of the same workload: one layer of the stack
@@ -460,6 +539,10 @@ def main():
     import __graft_entry__
     if rank == 0:
         __graft_entry__.build()
+    if a.switch_stress:
+        if rank == 0:
+            print(json.dumps(switch_stress(a)), flush=True)
+        return
     out = run_ours(a, rank, world, local_rank)
     if rank == 0:
         if not a.no_cpu_baseline:

@@ -113,11 +113,17 @@ __device__ __noinline__ void gemm_trap(uint32_t tag, uint32_t parity) {
     }
     __trap();
 }
+#ifndef DX_GEMM_SPIN
+#define DX_GEMM_SPIN 0
+#endif
+__device__ __forceinline__ bool gtry(uint32_t a, uint32_t parity) {
+    return DX_GEMM_SPIN ? mbar_try_wait(a, parity) : mbar_try_wait_sleep(a, parity);
+}
 __device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, uint32_t tag) {
     const uint32_t a = smem_u32(bar);
-    if (mbar_try_wait_sleep(a, parity)) return;
+    if (gtry(a, parity)) return;
     const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try_wait_sleep(a, parity))
+    while (!gtry(a, parity))
         if (globaltimer_ns() - t0 > 2000000000ull) gemm_trap(tag, parity);   // 2 s: a protocol bug
 }
 
@@ -203,10 +209,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     // prologue independent of the predecessor kernels (overlaps their tail under PDL)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? 32 * NTW : 128); mbar_init(&aempty[b], 1); }
+        for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? NTW : 4); mbar_init(&aempty[b], 1); }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128);
-            mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], 32 * NTW);
+            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4);
+            mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], NTW);
         }
         for (int b = 0; b < RING; ++b) { mbar_init(&tkfull[b], 1); mbar_init(&tkempty[b], N_CONSUMERS); }
         fence_mbar_init();
@@ -453,7 +459,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                                 tmem_st_wait();
                             }
                             tc_fence_before();
-                            mbar_arrive(&aready[cab]);
+                            __syncwarp();                 // one arrival per warp (arrivals serialise)
+                            if (lane == 0) mbar_arrive(&aready[cab]);
                         }
                     }
                 }
@@ -461,7 +468,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             if (w.bits == 4) body(std::integral_constant<int, 4>{});
             else body(std::integral_constant<int, 2>{});
             if (tab_ok) {                                 // table buffer back to the producer
-                mbar_arrive(&tabempty[tb]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tabempty[tb]);
                 ++tc;
             }
         }
@@ -539,7 +547,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(&tempty[buf]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[buf]);
                 named_bar(1, 128);                      // ent_s / gate_s / xch reused by the next chunk
             }
         }
