@@ -24,6 +24,7 @@
 #include "dx_sm100.cuh"
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <type_traits>
 
 using namespace sm100;
@@ -44,6 +45,7 @@ constexpr int A_BYTES = 128 * 128;            // A / raw region per stage
 constexpr int B_REGION = 16384;               // B region per stage
 constexpr int STAGE_BYTES = A_BYTES + B_REGION;
 constexpr int XCH_BYTES = 64 * 32 * 4;        // epilogue SwiGLU exchange: 64 rows x 32 columns fp32
+constexpr int TPRE_BYTES = (512 + 1) * 4 + 12;   // prefill: per-active-expert N-tile prefix
 constexpr int RING = 2;                       // claimed work items in flight per CTA (small: balance)
 constexpr int N_CONSUMERS = W_SCHED;          // warps that read the item ring (all but the scheduler)
 constexpr int GTAB = 16;                      // scale/zero groups per row staged in smem per item (G <= 16)
@@ -56,7 +58,7 @@ struct Cfg {
     static constexpr int NBMAX = DEC ? 64 : 128;
     static constexpr int ACH = DEC ? 4 : 1;                    // K chunks per TMEM A buffer (32 columns each)
     static constexpr int NA = (512 - 2 * NBMAX) / (32 * ACH);  // TMEM A buffers: 3 (decode) / 8 (prefill)
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES + TPRE_BYTES;
     __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : 128; }
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
@@ -103,6 +105,7 @@ __device__ __forceinline__ void dequant_chunk(int bits, uint32_t ra0, uint32_t r
 // host-mapped word array and traps, so a hang surfaces as a launch error with a readable diagnosis
 // (gemm_trap_report) instead of a stuck GPU.
 __device__ uint32_t* g_gemm_trap = nullptr;
+__device__ uint64_t g_gemm_watchdog_ns = 2000000000ull;   // DX_WATCHDOG_S (ncu's instrumented replays need more)
 __device__ __noinline__ void gemm_trap(uint32_t tag, uint32_t parity) {
     uint32_t* r = g_gemm_trap;
     if (r && atomicCAS(r, 0u, 0xDEAD0000u | tag) == 0u) {
@@ -119,18 +122,47 @@ __device__ __noinline__ void gemm_trap(uint32_t tag, uint32_t parity) {
 __device__ __forceinline__ bool gtry(uint32_t a, uint32_t parity) {
     return DX_GEMM_SPIN ? mbar_try_wait(a, parity) : mbar_try_wait_sleep(a, parity);
 }
-__device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, uint32_t tag) {
+// Slow path of a barrier wait, out of line: polls (the watchdog clock is read once per 256 polls) and
+// sleeps backoff_ns between polls.  Waiting warps share their sub-partition's issue slots with the dequant
+// warps, so every role except the dequant workers backs off.
+__device__ __noinline__ void gwait_slow(uint32_t a, uint32_t parity, uint32_t tag, uint32_t backoff_ns) {
+    const uint64_t lim = g_gemm_watchdog_ns;
+    const uint64_t t0 = globaltimer_ns();
+    for (;;) {
+#pragma unroll 1
+        for (int i = 0; i < 256; ++i) {
+            if (mbar_try_wait(a, parity)) return;
+            if (backoff_ns) __nanosleep(backoff_ns);
+        }
+        if (globaltimer_ns() - t0 > lim) gemm_trap(tag, parity);   // default 2 s: a protocol bug
+    }
+}
+__device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, uint32_t tag, uint32_t backoff_ns = 0) {
     const uint32_t a = smem_u32(bar);
     if (gtry(a, parity)) return;
-    const uint64_t t0 = globaltimer_ns();
-    while (!gtry(a, parity))
-        if (globaltimer_ns() - t0 > 2000000000ull) gemm_trap(tag, parity);   // 2 s: a protocol bug
+    gwait_slow(a, parity, tag, backoff_ns);
 }
 
 // Decoded work item: 128-row block mb of an active expert, its token rows [r0, r0+m), tier / slot / bits.
 struct Item {
     int mb, r0, m, ti, slot, bits;
 };
+// Prefill work items are (expert, N tile of NT token rows, row block): the N tiles of every active expert
+// are numbered by the prefix tpre[] (so a hot expert's thousands of rows spread over many SMs instead of
+// one CTA walking all of them); decode items are (expert, row block) with all of its rows.
+__device__ __forceinline__ int4 decode_tiled(const GemmArgs& a, const int32_t* tpre, int n_act, int item, int nmb,
+                                             int NT) {
+    const int q = item / nmb;
+    int lo = 0, hi = n_act - 1;                        // largest a with tpre[a] <= q
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tpre[mid] <= q) lo = mid; else hi = mid - 1;
+    }
+    const int e = a.act_e[lo];
+    const int r0 = a.off[e] + (q - tpre[lo]) * NT;
+    const int m = min(NT, a.off[e + 1] - r0);
+    return make_int4(r0, m, a.slot[e], a.tier[e]);
+}
 __device__ __forceinline__ int4 decode_raw(const GemmArgs& a, int item, int nmb) {   // {r0, m, slot, ti}
     const int e = a.act_e[item / nmb];
     const int r0 = a.off[e];
@@ -147,7 +179,7 @@ struct Tick {
 __device__ __forceinline__ bool take_item(const GemmArgs& a, const Tick* ring, uint64_t* tkfull, uint64_t* tkempty,
                                           int ii, int n_items, int nmb, Item& it) {
     const int sl = ii % RING;
-    gwait(&tkfull[sl], (ii / RING) & 1, 10);
+    gwait(&tkfull[sl], (ii / RING) & 1, 10, 128);
     int4 v = ring[sl].v;
     int item = ring[sl].item;
     v.x = __shfl_sync(0xffffffffu, v.x, 0);
@@ -196,6 +228,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     float* gate_s = reinterpret_cast<float*>(ent_s + 128);           // [128] epilogue: gates
     Tick* ring = reinterpret_cast<Tick*>(reinterpret_cast<uint8_t*>(bars) + 2048);   // [RING] items
     uint8_t* tabs = reinterpret_cast<uint8_t*>(ring + RING);         // [2][TAB_BYTES]
+    int32_t* tpre = reinterpret_cast<int32_t*>(tabs + 2 * TAB_BYTES); // [n_act + 1] prefill N-tile prefix
 
     const int K = PHASE == 0 ? a.H : a.I;
     const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
@@ -208,7 +241,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
 
     // prologue independent of the predecessor kernels (overlaps their tail under PDL)
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1 + NTW); }
         for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? NTW : 4); mbar_init(&aempty[b], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4);
@@ -221,7 +254,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
-    const int n_items = a.n_act[0] * nmb;
+    const int n_act = a.n_act[0];
+    int n_items = n_act * nmb;
+    if (!DEC) {
+        // N tiles per active expert, exclusive prefix over the active list (n_act <= 512 < blockDim)
+        __shared__ int32_t wsum[32];
+        const int t = threadIdx.x;
+        int v = 0;
+        if (t < n_act) {
+            const int e = a.act_e[t];
+            v = (a.off[e + 1] - a.off[e] + C::NBMAX - 1) / C::NBMAX;
+        }
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        int base = 0;
+        for (int w2 = 0; w2 < warp; ++w2) base += wsum[w2];
+        if (t <= n_act) tpre[t] = base + x - v;
+        __syncthreads();
+        n_items = tpre[n_act] * nmb;
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -239,7 +296,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             if (qt && tab_ok) {
                 // this item's scales / zeros: contiguous row spans of the slot's [rows][G] tables
                 const int tb = tc & 1;
-                gwait(&tabempty[tb], ((tc >> 1) & 1) ^ 1, 1);
+                gwait(&tabempty[tb], ((tc >> 1) & 1) ^ 1, 1, 128);
                 ++tc;
                 if (elect_one()) {
                     const SlotLayout& L = w.ti ? a.hi : a.lo;
@@ -279,7 +336,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 const CUtensorMap* bmap = multi ? &maps.xk[w.bits == 2 ? 2 : ri] : &maps.xb[ri];
                 const uint32_t bytes = multi ? A_BYTES + ks * rb * 128 : (qt ? 128 * kunit : A_BYTES) + rb * 128;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
-                    gwait(&empty[st], ph ^ 1, 2);
+                    gwait(&empty[st], ph ^ 1, 2, 128);
                     if (elect_one()) {
                         uint8_t* sA = sS + st * STAGE_BYTES;
                         mbar_arrive_expect_tx(&full[st], bytes);
@@ -305,12 +362,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 const int rb = box_rows(min(nb, w.m - n0));
                 const uint32_t idesc = idesc_bf16(128, rb);
                 const int buf = cc & 1;
-                gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3);
+                gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, 128);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * C::NBMAX;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
                     const int kc = min(ks, nk - kb0);
-                    gwait(&full[st], ph, 4);
+                    gwait(&full[st], ph, 4, 64);
                     tc_fence_after();
                     const uint32_t sA = smem_u32(sS + st * STAGE_BYTES), sB = sA + A_BYTES;
                     if (w.bits == 16) {
@@ -324,7 +381,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         const uint64_t db = umma_desc_sw128(sB);
                         const uint32_t bstep = (rb * 128) >> 4;            // B sub-tile stride in descriptor units
                         for (int j0 = 0; j0 < kc; j0 += C::ACH) {         // one TMEM A buffer = ACH chunks
-                            gwait(&aready[ab], aph, 5);
+                            gwait(&aready[ab], aph, 5, 64);
                             tc_fence_after();
                             const int jn = min(C::ACH, kc - j0);
                             const uint32_t at = tmem_a + ab * 32 * C::ACH;
@@ -359,9 +416,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             }
         }
     } else if (warp < W_EPI) {
-        // ------------------------------------------------ dequant transform (8 warps, thread = A row =
-        // TMEM lane).  Decode: every TMEM A buffer holds ACH = 4 chunks, group g dequantises chunks 2g and
-        // 2g+1 of each; prefill: one chunk per buffer, the two groups take alternate buffers.
+        // ------------------------------------------------ dequant transform (NTW warps, thread = A row =
+        // TMEM lane).  Decode: every TMEM A buffer holds ACH = 4 chunks, group g dequantises chunk(s)
+        // ACH/NG*g.. of each; prefill: one chunk per buffer, the NG groups take the buffers in turn.  Every
+        // transform warp also releases every stage (empty[] counts 1 MMA commit + NTW warps), so the
+        // producer can never lap a warp that is still to observe a stage's phase.
         const int grp = (warp - 2) >> 2;              // 0..NG-1
         const int qa = warp & 3;
         const int r = 32 * qa + lane;
@@ -379,7 +438,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             if (w.bits == 16) {                           // bf16 stages need no transform: observe their phases
                 const int nst = ((w.m + C::nb(16) - 1) / C::nb(16)) * nk;
                 for (int s = 0; s < nst; ++s) {
-                    gwait(&full[st], ph, 7);
+                    gwait(&full[st], ph, 7, 64);         // idle: poll gently
+                    __syncwarp();                        // released by every transform warp too, so the
+                    if (lane == 0) mbar_arrive(&empty[st]);   // producer can never lap an observer
                     if (++st == STAGES) { st = 0; ph ^= 1; }
                 }
                 continue;
@@ -414,6 +475,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                     for (int kb0 = 0; kb0 < nk; kb0 += KS) {
                         // every transform thread observes every phase of full[] (no phase aliasing)
                         gwait(&full[st], ph, 7);
+                        const int cst = st;
                         const uint32_t stage = stages_u32 + st * STAGE_BYTES;
                         if (++st == STAGES) { st = 0; ph ^= 1; }
                         const int kc = min(KS, nk - kb0);
@@ -462,6 +524,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                             __syncwarp();                 // one arrival per warp (arrivals serialise)
                             if (lane == 0) mbar_arrive(&aready[cab]);
                         }
+                        __syncwarp();                     // this warp is done reading the stage's codes
+                        if (lane == 0) mbar_arrive(&empty[cst]);
                     }
                 }
             };
@@ -479,11 +543,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         int* ctr = a.sched + 2 * PHASE;
         for (int ii = 0;; ++ii) {
             const int sl = ii % RING;
-            gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11);
+            gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11, 256);
             int item = 0;
             if (lane == 0) {
                 item = atomicAdd(ctr, 1);
-                ring[sl].v = item < n_items ? decode_raw(a, item, nmb) : make_int4(0, 0, 0, 0);
+                ring[sl].v = item >= n_items ? make_int4(0, 0, 0, 0)
+                           : DEC ? decode_raw(a, item, nmb) : decode_tiled(a, tpre, n_act, item, nmb, C::NBMAX);
                 ring[sl].item = item;
                 mbar_arrive(&tkfull[sl]);
             }
@@ -508,7 +573,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         gate_s[i] = a.gate[ent];
                     }
                 }
-                gwait(&tfull[buf], (cc >> 1) & 1, 9);
+                gwait(&tfull[buf], (cc >> 1) & 1, 9, 256);
                 tc_fence_after();
                 named_bar(1, 128);
                 for (int col = 0; col < nvalid; col += 32) {
@@ -595,6 +660,10 @@ void gemm_trap_init() {
     uint32_t* dptr = nullptr;
     cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), g_trap_host, 0);
     cudaMemcpyToSymbol(g_gemm_trap, &dptr, sizeof(dptr));
+    if (const char* w = getenv("DX_WATCHDOG_S")) {
+        const uint64_t ns = (uint64_t)(atof(w) * 1e9);
+        if (ns > 0) cudaMemcpyToSymbol(g_gemm_watchdog_ns, &ns, sizeof(ns));
+    }
 }
 static const char* const k_trap_names[] = {"?", "tabempty (producer)", "empty (producer)", "tempty (MMA)", "full (MMA)",
                                            "aready (MMA)", "tabfull (transform)", "full (transform)",
