@@ -303,7 +303,7 @@ def run_ours(a, rank, world, local_rank):
                                "touched per layer), controller Tp=16 L=4 with drift",
                    "global_batch": B * world, "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "l2": "no flush: each step streams >=48 distinct layers of weights (> 126 MB L2)"},
-        "roofline": {"bound": "hbm", "kernel": "k_ffn gate/up (phase 0)", "achieved": ach0, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_gemm<0> decode gate/up + SwiGLU (tcgen05)", "achieved": ach0, "peak": peak,
                      "unit": "GB/s", "frac": ach0 / peak, "traffic": traffic, "peak_source": peak_src,
                      "ffn_both_phases_gbs": ach_all, "ffn_both_frac": ach_all / peak,
                      "algorithmic_bytes_per_launch": wb[0] / max(prof["forwards"], 1)},

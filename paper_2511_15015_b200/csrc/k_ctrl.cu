@@ -236,7 +236,10 @@ __global__ void k_manual(Ctrl c, int layer, const int2* __restrict__ cmds, int n
 #define XFER_CHUNKS 64
 // mode: 0 = regular plan (promotions + demotions), 1 = finalize moves only, 2 = finalize promotions
 // only (the second finalize pass runs after every move has left the future HIGH region).
-__global__ void __launch_bounds__(256) k_xfer(Ctrl c, int layer, XferArgs x, int mode) {
+// Side-stream transitions run as a few small, register-lean blocks (128 threads, <= 48 registers) so
+// that each fits on an SM next to a resident persistent k_gemm CTA (736 threads x 80 registers): the
+// transfer then overlaps the expert GEMMs instead of holding SMs they are waiting for.
+__global__ void __launch_bounds__(128, 10) k_xfer(Ctrl c, int layer, XferArgs x, int mode) {
     const int n = c.plan_n[layer];
     const int E = c.E;
     const int total = n * XFER_CHUNKS;
@@ -313,7 +316,11 @@ void launch_manual(const Ctrl& c, int layer, const int2* cmds, int n, int32_t* s
 void launch_transitions(const Ctrl& c, int layer, const XferArgs& x, int max_cmds, int mode,
                         cudaStream_t st) {
     int grid = max_cmds * XFER_CHUNKS;
-    if (grid > 2 * DX_NUM_SMS) grid = 2 * DX_NUM_SMS;
+    // finalize (modes 1, 2: synchronous on the compute stream, nothing to overlap) may take the whole GPU;
+    // runtime transitions (mode 0, side stream) use at most one lean block per SM, which fits beside the
+    // SM's persistent GEMM CTA, so the GEMMs keep every SM while the transfer runs
+    const int cap = mode == 0 ? DX_NUM_SMS : 4 * DX_NUM_SMS;
+    if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    k_xfer<<<grid, 256, 0, st>>>(c, layer, x, mode);
+    k_xfer<<<grid, 128, 0, st>>>(c, layer, x, mode);
 }

@@ -46,7 +46,10 @@ constexpr int B_REGION = 16384;               // B region per stage
 constexpr int STAGE_BYTES = A_BYTES + B_REGION;
 constexpr int XCH_BYTES = 64 * 32 * 4;        // epilogue SwiGLU exchange: 64 rows x 32 columns fp32
 constexpr int TPRE_BYTES = (512 + 1) * 4 + 12;   // prefill: per-active-expert N-tile prefix
-constexpr int RING = 2;                       // claimed work items in flight per CTA (small: balance)
+#ifndef DX_GEMM_RING
+#define DX_GEMM_RING 2
+#endif
+constexpr int RING = DX_GEMM_RING;                       // claimed work items in flight per CTA (small: balance)
 constexpr int N_CONSUMERS = W_SCHED;          // warps that read the item ring (all but the scheduler)
 constexpr int GTAB = 16;                      // scale/zero groups per row staged in smem per item (G <= 16)
 constexpr int TAB_BYTES = 128 * GTAB * 3;     // one item's table: [128 rows][G] bf16 scales, then u8 zeros
@@ -63,6 +66,20 @@ struct Cfg {
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
 
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+// (bf16 scale | bf16(128 + z) << 16) of group gi from the slot in global memory (tables too wide for smem)
+__device__ __noinline__ uint32_t group_sz_global(const uint16_t* scales, const uint8_t* zeros, int gi) {
+    return (uint32_t)scales[gi] | ((0x4300u + zeros[gi]) << 16);
+}
 __device__ __forceinline__ uint32_t bf2_sub_mul(uint32_t v, uint32_t zz, uint32_t ss) {
     __nv_bfloat162 r = __hmul2(__hsub2(*reinterpret_cast<__nv_bfloat162*>(&v), *reinterpret_cast<__nv_bfloat162*>(&zz)),
                                *reinterpret_cast<__nv_bfloat162*>(&ss));
@@ -457,14 +474,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             const uint8_t* zeros = slot_base + L.zeros_off + mat * L.zeros_stride + (int64_t)mrow * G;
             // scales / zeros: this item's smem table (TMA'd by the producer) when G <= GTAB, else global
             const int tb = tc & 1;
-            const uint16_t* tsc = reinterpret_cast<const uint16_t*>(tabs + tb * TAB_BYTES) + r * G;
-            const uint8_t* tze = tabs + tb * TAB_BYTES + 128 * GTAB * 2 + r * G;
+            const uint32_t tsc = smem_u32(tabs + tb * TAB_BYTES) + r * G * 2;             // shared addresses
+            const uint32_t tze = smem_u32(tabs + tb * TAB_BYTES + 128 * GTAB * 2) + r * G;
             if (tab_ok) gwait(&tabfull[tb], (tc >> 1) & 1, 6);
             // packed (bf16 scale | bf16(128 + z) << 16) of group gi; rows past the matrix: s = 1, z = 0
             auto group_sz = [&](int gi) -> uint32_t {
                 if (!valid) return 0x43003f80u;
-                return tab_ok ? (uint32_t)tsc[gi] | ((0x4300u + tze[gi]) << 16)
-                              : (uint32_t)scales[gi] | ((0x4300u + zeros[gi]) << 16);
+                return tab_ok ? lds_u16(tsc + 2 * gi) | ((0x4300u + lds_u8(tze + gi)) << 16)
+                              : group_sz_global(scales, zeros, gi);
             };
             auto body = [&](auto bits_c) {
                 constexpr int BITS = decltype(bits_c)::value;
