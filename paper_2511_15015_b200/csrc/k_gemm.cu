@@ -50,7 +50,6 @@ constexpr int TPRE_BYTES = (512 + 1) * 4 + 12;   // prefill: per-active-expert N
 #define DX_GEMM_RING 2
 #endif
 constexpr int RING = DX_GEMM_RING;                       // claimed work items in flight per CTA (small: balance)
-constexpr int GR = 2;                         // factored path: group accumulator slots (32 TMEM columns each)
 constexpr int N_CONSUMERS = W_SCHED;          // warps that read the item ring (all but the scheduler)
 constexpr int GTAB = 16;                      // scale/zero groups per row staged in smem per item (G <= 16)
 constexpr int TAB_BYTES = 128 * GTAB * 3;     // one item's table: [128 rows][G] bf16 scales, then u8 zeros
@@ -116,26 +115,6 @@ __device__ __forceinline__ void dequant_chunk(int bits, uint32_t ra0, uint32_t r
             const uint32_t x = src[b >> 3] >> (2 * (b & 7));
             wv[b] = bf2_sub_mul(and_or(x, 0x00030003u, magic), zz[b >> 4], ss[b >> 4]);
         }
-    }
-}
-
-// Factored decode path (int tiers, g >= 64): A = bf16(128 + q) straight from the codes (one LOP3, plus a
-// shift for three of every four pairs); the zero point and the scale are applied per quantisation group
-// by the tensor cores and the epilogue instead (see the MMA and epilogue roles).
-__device__ __forceinline__ void raw_chunk(int bits, uint32_t ra0, uint32_t ra1, uint32_t (&wv)[KCH / 2], uint32_t magic) {
-    if (bits == 4) {
-        uint32_t s0, s1, s2, s3, s4, s5, s6, s7;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(ra0));
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s4), "=r"(s5), "=r"(s6), "=r"(s7) : "r"(ra1));
-        const uint32_t src[8] = {s0, s1, s2, s3, s4, s5, s6, s7};
-#pragma unroll
-        for (int b = 0; b < 32; ++b) wv[b] = and_or(src[b >> 2] >> (4 * (b & 3)), 0x000F000Fu, magic);
-    } else {
-        uint32_t s0, s1, s2, s3;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(s0), "=r"(s1), "=r"(s2), "=r"(s3) : "r"(ra0));
-        const uint32_t src[4] = {s0, s1, s2, s3};
-#pragma unroll
-        for (int b = 0; b < 32; ++b) wv[b] = and_or(src[b >> 3] >> (2 * (b & 7)), 0x00030003u, magic);
     }
 }
 
@@ -261,9 +240,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     uint64_t* tabempty = tabfull + 2;                     // [2] transform finished with the table
     uint64_t* tkfull = tabempty + 2;                      // [RING] item published by the scheduler
     uint64_t* tkempty = tkfull + RING;                    // [RING] every consumer warp read the item
-    uint64_t* gfull = tkempty + RING;                     // [GR] factored path: group accumulator ready
-    uint64_t* gempty = gfull + GR;                        // [GR] factored path: group accumulator drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + GR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tkempty + RING);
     int32_t* ent_s = reinterpret_cast<int32_t*>(tmem_slot + 4);     // [128] epilogue: entry ids
     float* gate_s = reinterpret_cast<float*>(ent_s + 128);           // [128] epilogue: gates
     Tick* ring = reinterpret_cast<Tick*>(reinterpret_cast<uint8_t*>(bars) + 2048);   // [RING] items
@@ -275,16 +252,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     const int nk = K / KCH;
     const int G = K / a.g;                                // quantisation groups per weight row
     const bool tab_ok = G <= GTAB;                        // per-item scale/zero tables staged by TMA
-    // Factored decode path for the int tiers (launch-uniform): per quantisation group g the tensor cores
-    // accumulate sum_k (128+q_k) x_k + sum_k (-(128+z)) x_k = sum_k (q_k - z) x_k into a group accumulator
-    // (the second term from a TMEM block of -(128+z) rows), and the epilogue adds s * that to its register
-    // accumulator.  The dequant transform is then one LOP3 (+ shift) per element pair instead of four
-    // instructions.  Needs whole groups per 4-chunk A buffer (64 <= g <= 256) and the smem tables.
-    // TMEM: [0,128) bf16 accumulators, [128,192) GR group slots, [192,512) two A buffers of 128 code
-    // columns + 32 columns of z rows (8 per group).  DX_GEMM_DBG=7 forces the exact-dequant path.
-    const bool fact = DEC && a.g >= 64 && a.g <= 256 && tab_ok && a.dbg != 7;
-    const int NAe = fact ? 2 : C::NA;                     // TMEM A buffers in use
-    const uint32_t a_stride = fact ? 160u : 32u * C::ACH; // TMEM columns per A buffer
     // warp index made provably warp-uniform: role branches are uniform and the single-thread issue paths
     // keep their operands in uniform registers
     const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
@@ -295,10 +262,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? NTW : 4); mbar_init(&aempty[b], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4);
-            mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], NTW + 4);   // transform + epilogue warps
+            mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], NTW);
         }
         for (int b = 0; b < RING; ++b) { mbar_init(&tkfull[b], 1); mbar_init(&tkempty[b], N_CONSUMERS); }
-        for (int b = 0; b < GR; ++b) { mbar_init(&gfull[b], 1); mbar_init(&gempty[b], 4); }
         fence_mbar_init();
         for (int i = 0; i < 4; ++i) tma_prefetch(&maps.xb[i]);
     }
@@ -334,8 +300,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-    const uint32_t tmem_a = tmem + (fact ? 192u : 2u * C::NBMAX);   // first TMEM A buffer column
-    const uint32_t tmem_g = tmem + 128u;                  // factored path: group accumulator slots
+    const uint32_t tmem_a = tmem + 2 * C::NBMAX;          // first TMEM A buffer column
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer: the whole warp walks the stages
@@ -405,20 +370,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer: warp-uniform walk, lane 0 issues
         // (tcgen05.mma / commit are single-thread instructions; commits must come from the issuing thread)
-        int st = 0, ab = 0, cc = 0, gc = 0;
+        int st = 0, ab = 0, cc = 0;
         uint32_t ph = 0, aph = 0;
         Item w;
         for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
             const int nb = C::nb(w.bits), ks = C::ks(w.bits);
-            const bool fi = fact && w.bits != 16;           // this item takes the factored path
-            for (int n0 = 0; n0 < w.m; n0 += nb) {
+            for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
                 const int rb = box_rows(min(nb, w.m - n0));
                 const uint32_t idesc = idesc_bf16(128, rb);
                 const int buf = cc & 1;
-                if (!fi) {
-                    gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, 128);
-                    tc_fence_after();
-                }
+                gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, 128);
+                tc_fence_after();
                 const uint32_t d = tmem + buf * C::NBMAX;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
                     const int kc = min(ks, nk - kb0);
@@ -439,37 +401,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                             gwait(&aready[ab], aph, 5, 64);
                             tc_fence_after();
                             const int jn = min(C::ACH, kc - j0);
-                            const uint32_t at = tmem_a + ab * a_stride;
+                            const uint32_t at = tmem_a + ab * 32 * C::ACH;
                             const uint64_t bj = db + j0 * bstep;
                             const bool first = (kb0 | j0) == 0;
-                            if (fi) {
-                                // whole quantisation groups of this buffer, each into the next group slot:
-                                // per K16 step the code MMA (A = bf16(128+q)) and the z-row MMA (A = -(128+z))
-                                const int spg = a.g >> 4;            // K16 steps per group
-                                const int ngb = (jn * KCH) / a.g;    // groups in this buffer
-                                for (int gb = 0; gb < ngb; ++gb, ++gc) {
-                                    const int sl = gc % GR;
-                                    gwait(&gempty[sl], ((gc / GR) & 1) ^ 1, 12, 32);
-                                    tc_fence_after();
-                                    const uint32_t dg = tmem_g + sl * 32;
-                                    if (elect_one()) {
-                                        if (a.dbg != 4 && a.dbg != 6) {
-                                            for (int q = 0; q < spg; ++q) {
-                                                const int kq = gb * spg + q;          // K16 step in the buffer
-                                                const uint64_t bq = bj + (kq >> 2) * bstep + 2 * (kq & 3);
-                                                mma_bf16_ts(dg, at + 8 * kq, bq, idesc, q != 0);
-                                                mma_bf16_ts(dg, at + 128 + 8 * gb, bq, idesc, true);
-                                            }
-                                        }
-                                        mma_commit(&gfull[sl]);
-                                    }
-                                    __syncwarp();
-                                }
-                                if (elect_one()) mma_commit(&aempty[ab]);
-                                __syncwarp();
-                                if (++ab == NAe) { ab = 0; aph ^= 1; }
-                                continue;
-                            }
                             if (elect_one()) {
                                 if (a.dbg != 4 && a.dbg != 6) {
                                     if (jn == C::ACH) {
@@ -487,18 +421,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                                 mma_commit(&aempty[ab]);
                             }
                             __syncwarp();
-                            if (++ab == NAe) { ab = 0; aph ^= 1; }
+                            if (++ab == C::NA) { ab = 0; aph ^= 1; }
                         }
                     }
                     if (elect_one()) mma_commit(&empty[st]);
                     __syncwarp();
                     if (++st == STAGES) { st = 0; ph ^= 1; }
                 }
-                if (!fi) {
-                    if (elect_one()) mma_commit(&tfull[buf]);
-                    __syncwarp();
-                    ++cc;
-                }
+                if (elect_one()) mma_commit(&tfull[buf]);
+                __syncwarp();
             }
         }
     } else if (warp < W_EPI) {
@@ -568,7 +499,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         for (int j0 = 0; j0 < kc; j0 += C::ACH, ++nbuf) {
                             const int cab = ab;
                             const uint32_t caph = aph;
-                            if (++ab == NAe) { ab = 0; aph ^= 1; }
+                            if (++ab == C::NA) { ab = 0; aph ^= 1; }
                             if (!DEC && (nbuf % NG) != grp) continue;  // prefill: another group's buffer
                             gwait(&aempty[cab], caph ^ 1, 8);
                             if (a.dbg != 5 && a.dbg != 6) {
@@ -578,6 +509,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                                     const int j = j0 + jj;                   // chunk within the stage
                                     if (j < kc) {
                                         const int k0 = (kb0 + j) * KCH;
+                                        uint32_t zz[2], ss[2];
+                                        const uint32_t v0 = group_sz(k0 >> gsh);
+                                        const uint32_t v1 = a.g >= 64 ? v0 : group_sz((k0 + 32) >> gsh);
+                                        zz[0] = (v0 >> 16) * 0x10001u;
+                                        ss[0] = (v0 & 0xFFFFu) * 0x10001u;
+                                        zz[1] = (v1 >> 16) * 0x10001u;
+                                        ss[1] = (v1 & 0xFFFFu) * 0x10001u;
                                         // raw codes of (row r, chunk j): decode stages hold one 128 B-swizzled
                                         // row of KS chunks (16 B unit c of row r at unit c ^ (r & 7)); prefill
                                         // stages one chunk
@@ -592,28 +530,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                                             ra1 = ra0 + 16;
                                         }
                                         uint32_t wv[KCH / 2];      // 32 bf16x2 words = 64 elements
-                                        const uint32_t tcol = lane_base + cab * a_stride + 32 * jj;
-                                        if (fact) {
-                                            raw_chunk(BITS, ra0, ra1, wv, magic);
-                                            tc_fence_after();
-                                            tmem_st32(tcol, wv);
-                                            if ((k0 & (a.g - 1)) == 0) {     // first chunk of its group: z rows
-                                                const uint32_t zr = valid ? 0xC300u + lds_u8(tze + (k0 >> gsh)) : 0xC300u;
-                                                tmem_st8_splat(lane_base + cab * a_stride + 128 + 8 * ((jj * KCH) / a.g),
-                                                               zr * 0x10001u);
-                                            }
-                                        } else {
-                                            uint32_t zz[2], ss[2];
-                                            const uint32_t v0 = group_sz(k0 >> gsh);
-                                            const uint32_t v1 = a.g >= 64 ? v0 : group_sz((k0 + 32) >> gsh);
-                                            zz[0] = (v0 >> 16) * 0x10001u;
-                                            ss[0] = (v0 & 0xFFFFu) * 0x10001u;
-                                            zz[1] = (v1 >> 16) * 0x10001u;
-                                            ss[1] = (v1 & 0xFFFFu) * 0x10001u;
-                                            dequant_chunk(BITS, ra0, ra1, zz, ss, wv, magic);
-                                            tc_fence_after();
-                                            tmem_st32(tcol, wv);
-                                        }
+                                        dequant_chunk(BITS, ra0, ra1, zz, ss, wv, magic);
+                                        tc_fence_after();
+                                        tmem_st32(lane_base + cab * 32 * C::ACH + 32 * jj, wv);
                                     }
                                 }
                                 tmem_st_wait();
@@ -657,50 +576,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
         // ------------------------------------------------ epilogue (128 threads, warps W_EPI..W_EPI+3)
         const int q = warp & 3;                         // TMEM lane quarter this warp may access
         const int et = threadIdx.x - 32 * W_EPI;        // 0..127
-        const int row = 32 * q + lane;                  // A row = TMEM lane of this thread
-        int cc = 0, gc = 0, tc = 0;
-        // one 32-column block of results (bit patterns of fp32) for token columns col.. of this chunk
-        auto emit = [&](const uint32_t (&v)[32], const Item& w, int n0, int col, int nvalid) {
-            if (PHASE == 0) {
-                // rows 64-127 (up) -> smem; rows 0-63 (gate) combine: act = silu(g) * u
-                if (q >= 2) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) xch[j * 64 + 32 * (q - 2) + lane] = __uint_as_float(v[j]);
-                }
-                named_bar(1, 128);
-                if (q < 2) {
-                    const int f = w.mb * 64 + 32 * q + lane;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {           // fully unrolled: v[] stays in registers
-                        if (col + j < nvalid) {
-                            const float gv = __uint_as_float(v[j]);
-                            const float uv = xch[j * 64 + 32 * q + lane];
-                            const float sg = gv / (1.0f + __expf(-gv));
-                            a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
-                        }
-                    }
-                }
-                named_bar(1, 128);
-            } else {
-                const int h = w.mb * 128 + 32 * q + lane;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {               // fully unrolled: v[] stays in registers
-                    if (col + j < nvalid && h < a.H) {
-                        const int ent = ent_s[col + j];
-                        a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(gate_s[col + j] * __uint_as_float(v[j]));
-                    }
-                }
-            }
-        };
+        int cc = 0;
         Item w;
         for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
             const int nb = C::nb(w.bits);
-            const bool qt = w.bits != 16;
-            const bool fi = fact && qt;
-            const int tb = tc & 1;
-            const uint32_t tscale = smem_u32(tabs + tb * TAB_BYTES) + row * G * 2;
-            if (fi) gwait(&tabfull[tb], (tc >> 1) & 1, 6, 64);
-            for (int n0 = 0; n0 < w.m; n0 += nb) {
+            for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
+                const int buf = cc & 1;
                 const int nvalid = min(nb, w.m - n0);
                 if (PHASE == 1) {                       // entry ids and gates of this chunk's tokens -> smem
                     for (int i = et; i < nvalid; i += 128) {
@@ -709,41 +590,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         gate_s[i] = a.gate[ent];
                     }
                 }
-                if (fi) {
-                    // factored path: y = sum over groups of s_g * (group accumulator), in registers
-                    float acc[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-                    for (int gi = 0; gi < G; ++gi, ++gc) {
-                        const int sl = gc % GR;
-                        gwait(&gfull[sl], (gc / GR) & 1, 13, 32);
-                        tc_fence_after();
-                        const float sc = __uint_as_float(lds_u16(tscale + 2 * gi) << 16);
-                        const uint32_t taddr = tmem_g + sl * 32 + ((uint32_t)(32 * q) << 16);
-                        uint32_t v16[16];
-                        tmem_ld16(taddr, v16);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) acc[j] = fmaf(sc, __uint_as_float(v16[j]), acc[j]);
-                        if (nb > 16) {
-                            tmem_ld16(taddr + 16, v16);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) acc[16 + j] = fmaf(sc, __uint_as_float(v16[j]), acc[16 + j]);
-                        }
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&gempty[sl]);
-                    }
-                    named_bar(1, 128);
-                    uint32_t v[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc[j]);
-                    emit(v, w, n0, 0, nvalid);
-                    named_bar(1, 128);                  // ent_s / gate_s / xch reused by the next chunk
-                    continue;
-                }
-                const int buf = cc & 1;
                 gwait(&tfull[buf], (cc >> 1) & 1, 9, 256);
                 tc_fence_after();
                 named_bar(1, 128);
@@ -751,18 +597,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                     uint32_t v[32];
                     tmem_ld32(tmem + buf * C::NBMAX + ((uint32_t)(32 * q) << 16) + col, v);
                     tmem_ld_wait();
-                    emit(v, w, n0, col, nvalid);
+                    if (PHASE == 0) {
+                        // rows 64-127 (up) -> smem; rows 0-63 (gate) combine: act = silu(g) * u
+                        if (q >= 2) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) xch[j * 64 + 32 * (q - 2) + lane] = __uint_as_float(v[j]);
+                        }
+                        named_bar(1, 128);
+                        if (q < 2) {
+                            const int f = w.mb * 64 + 32 * q + lane;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {           // fully unrolled: v[] stays in registers
+                                if (col + j < nvalid) {
+                                    const float gv = __uint_as_float(v[j]);
+                                    const float uv = xch[j * 64 + 32 * q + lane];
+                                    const float sg = gv / (1.0f + __expf(-gv));
+                                    a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
+                                }
+                            }
+                        }
+                        named_bar(1, 128);
+                    } else {
+                        const int h = w.mb * 128 + 32 * q + lane;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {           // fully unrolled: v[] stays in registers
+                            if (col + j < nvalid && h < a.H) {
+                                const int ent = ent_s[col + j];
+                                a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(gate_s[col + j] * __uint_as_float(v[j]));
+                            }
+                        }
+                    }
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[buf]);
                 named_bar(1, 128);                      // ent_s / gate_s / xch reused by the next chunk
-                ++cc;
-            }
-            if (qt && tab_ok) {                         // scale/zero table back to the producer
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tabempty[tb]);
-                ++tc;
             }
         }
     }
