@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--prefill-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-batch-sweep", action="store_true")
     ap.add_argument("--switch-stress", action="store_true",
                     help="C5 (SURVEY 8(d)): one Q30B layer, n_hot swept 10%%..100%%, drift 0.5 every period; "
                          "prints the C5 JSON line instead of the main one")
@@ -325,10 +326,59 @@ def run_ours(a, rank, world, local_rank):
     clock = clk.summary()
     if clock:
         out["clocks"] = clock
+    if not a.no_batch_sweep:
+        out["extra"]["decode_batch_sweep"] = batch_sweep(a, pool, wr, bias, step_counter, L, H, dev, stream, peak)
     if a.prefill_tokens > 0:
         out["extra"]["prefill"] = prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream)
     pool.close()
     return out
+
+
+def batch_sweep(a, pool, wr, bias, step_counter, L, H, dev, stream, peak):
+    """C2's decode batch range (B in 1..64) on the same stack and pool: per B, 5 timed
+    stack steps (after 2 untimed) -> layer-tokens/s, and the expert GEMMs' algorithmic weight bytes /
+    their device time (both phases) against the HBM peak."""
+    import torch
+    import synth
+    c = C2
+    rows = []
+    for B in (1, 4, 16, 64):
+        xs = [torch.from_numpy(synth.normal_bf16(a.seed, 800 + B, i, 0, (B, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+              for i in range(2)]
+        y = torch.empty(B, H, dtype=torch.bfloat16, device=dev)
+
+        def bstep(x):
+            ep = min(step_counter[0] // c["drift"], bias.shape[1] - 1)
+            for l in range(L):
+                pool.dx_moe_forward(l, x, B, y, router_w=wr[l], router_bias=bias[l, ep])
+                pool.dx_hotness_update(l)
+                pool.dx_plan_precision(l)
+            step_counter[0] += 1
+
+        for i in range(2):
+            bstep(xs[i % 2])
+        pool.dx_sync()
+        pool.dx_profile_read()
+        pool.dx_profile_enable(True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n = 5
+        for i in range(n):
+            bstep(xs[i % 2])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        prof = pool.dx_profile_read()
+        pool.dx_profile_enable(False)
+        wb = prof["weight_bytes"][0] + prof["weight_bytes"][1]
+        ffn_s = (prof["ffn_ms"][0] + prof["ffn_ms"][1]) / 1e3
+        gbs = wb / ffn_s / 1e9 if ffn_s > 0 else 0.0
+        rows.append({"batch": B, "value": B * L * n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / n,
+                     "active_experts_per_layer": prof["active_experts"] / max(prof["forwards"], 1),
+                     "weight_bytes_per_layer": wb / max(prof["forwards"], 1), "ffn_weight_gbs": gbs,
+                     "ffn_hbm_frac": gbs / peak})
+    return rows
 
 
 def prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream):

@@ -319,7 +319,10 @@ void launch_transitions(const Ctrl& c, int layer, const XferArgs& x, int max_cmd
     // finalize (modes 1, 2: synchronous on the compute stream, nothing to overlap) may take the whole GPU;
     // runtime transitions (mode 0, side stream) use at most one lean block per SM, which fits beside the
     // SM's persistent GEMM CTA, so the GEMMs keep every SM while the transfer runs
-    const int cap = mode == 0 ? DX_NUM_SMS : 4 * DX_NUM_SMS;
+#ifndef DX_XFER_BLOCKS
+#define DX_XFER_BLOCKS DX_NUM_SMS
+#endif
+    const int cap = mode == 0 ? DX_XFER_BLOCKS : 4 * DX_NUM_SMS;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     k_xfer<<<grid, 128, 0, st>>>(c, layer, x, mode);
