@@ -66,20 +66,54 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and throttle reasons sampled every 10 ms DURING the timed region through NVML (pynvml,
+    nvidia_ml_py); falls back to `nvidia-smi -lms 100` when NVML is unavailable.  At least one sample is
+    always taken (on entry)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+    NAMES = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.samples = []            # (sm_mhz, max_mhz, set(reasons))
+        self.nv = None
+        self.stop = threading.Event()
+
+    def _nvml_sample(self):
+        nv, h = self.nv, self.h
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = {"sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap, "hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown}
+        self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                             float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                             {k for k, v in bits.items() if r & v}))
+
+    def _nvml_loop(self):
+        while not self.stop.wait(0.01):
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
 
     def __enter__(self):
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            self._nvml_sample()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nv = None
+        try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.idx), "-lms", "200"], stdout=subprocess.PIPE,
+                                          "-i", str(self.idx), "-lms", "100"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -92,6 +126,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nv is not None:
+            self.stop.set()
+            self.t.join(timeout=1)
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -101,7 +142,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
-        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for a, b, r in self.samples:
+            sm.append(a)
+            mx.append(b)
+            reasons |= r
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 6:
@@ -111,13 +155,13 @@ class ClockSampler:
                 mx.append(float(p[1]))
             except ValueError:
                 continue
-            for n, v in zip(names, p[2:6]):
+            for n, v in zip(self.NAMES, p[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------------------- ours

@@ -133,6 +133,9 @@ __device__ __noinline__ void gemm_trap(uint32_t tag, uint32_t parity) {
     }
     __trap();
 }
+#ifndef DX_TBACK
+#define DX_TBACK 0             // backoff (ns) of the dequant warps' own waits
+#endif
 #ifndef DX_GEMM_SPIN
 #define DX_GEMM_SPIN 0
 #endif
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             const int tb = tc & 1;
             const uint32_t tsc = smem_u32(tabs + tb * TAB_BYTES) + r * G * 2;             // shared addresses
             const uint32_t tze = smem_u32(tabs + tb * TAB_BYTES + 128 * GTAB * 2) + r * G;
-            if (tab_ok) gwait(&tabfull[tb], (tc >> 1) & 1, 6);
+            if (tab_ok) gwait(&tabfull[tb], (tc >> 1) & 1, 6, DX_TBACK);
             // packed (bf16 scale | bf16(128 + z) << 16) of group gi; rows past the matrix: s = 1, z = 0
             auto group_sz = [&](int gi) -> uint32_t {
                 if (!valid) return 0x43003f80u;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 for (int n0 = 0; n0 < w.m; n0 += NBB) {
                     for (int kb0 = 0; kb0 < nk; kb0 += KS) {
                         // every transform thread observes every phase of full[] (no phase aliasing)
-                        gwait(&full[st], ph, 7);
+                        gwait(&full[st], ph, 7, DX_TBACK);
                         const int cst = st;
                         const uint32_t stage = stages_u32 + st * STAGE_BYTES;
                         if (++st == STAGES) { st = 0; ph ^= 1; }
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                             const uint32_t caph = aph;
                             if (++ab == C::NA) { ab = 0; aph ^= 1; }
                             if (!DEC && (nbuf % NG) != grp) continue;  // prefill: another group's buffer
-                            gwait(&aempty[cab], caph ^ 1, 8);
+                            gwait(&aempty[cab], caph ^ 1, 8, DX_TBACK);
                             if (a.dbg != 5 && a.dbg != 6) {
 #pragma unroll
                                 for (int h = 0; h < (DEC ? C::ACH / NG : 1); ++h) {
