@@ -11,3 +11,6 @@ import json; d=json.loads(open('gpurun_out/sweep.json').read()); r=d['roofline']
 print('value %.0f gateup %.0f GB/s both %.0f GB/s | prefill %.0f tok/s %.0f TF/s' % (d['value'], r['achieved'], r['ffn_both_phases_gbs'], p['value'], p['gemm_tflops']))" || tail -3 gpurun_out/sweep.err
   done
 done
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --prefill-tokens 0 --no-batch-sweep > gpurun_out/bench.json 2> gpurun_out/bench.err; python -c "
+import json; d=json.loads(open('gpurun_out/bench.json').read()); print('value %.0f clocks %s' % (d['value'], d.get('clocks')))" || tail -3 gpurun_out/bench.err
