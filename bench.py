@@ -172,7 +172,19 @@ def host_masters(seed, L, E, H, I, rank, world):
     import synth
     n = 3 * I * H
     total = L * E * n
+    shm_ok = False
     if world > 1:
+        import shutil
+        try:   # one shared copy only if /dev/shm can hold it (container /dev/shm is often small)
+            shm_ok = shutil.disk_usage("/dev/shm").free > total * 2 * 1.05 or \
+                os.path.exists(f"/dev/shm/dx_masters_{seed}_{L}_{E}_{H}_{I}.bin")
+        except OSError:
+            shm_ok = False
+        import torch.distributed as dist   # a collective decision: every rank takes the same branch
+        flag = torch.tensor([1 if shm_ok else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        shm_ok = bool(flag.item())
+    if shm_ok:
         path = f"/dev/shm/dx_masters_{seed}_{L}_{E}_{H}_{I}.bin"
         if rank == 0 and (not os.path.exists(path) or os.path.getsize(path) != total * 2):
             mm = np.memmap(path + ".tmp", dtype=np.uint16, mode="w+", shape=(total,))
