@@ -5,6 +5,7 @@
 // Readings: R-G1 (ties -> lower id, gates = softmax over the k selected logits), R-G2 (dx_expf),
 // R-H1 (cnt u32, mass = sum rint(g * 2^24) u64: integer sums are order-free => bit-exact).
 #include "dx_common.cuh"
+#include <cstdio>
 
 #define ROUTE_TOK_PER_BLK 8
 #define ROUTE_MAX_E 512
@@ -207,6 +208,12 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
 #define ROUTE1_CHUNKS 16
 template <typename Tv>
 __device__ Tv block_excl_scan(Tv v, Tv* tmp, Tv* total);
+#ifdef DX_ROUTE_PROF
+__device__ unsigned g_route1_calls = 0;
+#define R1P(i) do { if (threadIdx.x == 0) tp[i] = clock64(); } while (0)
+#else
+#define R1P(i) do {} while (0)
+#endif
 template <int NVT>
 __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits, int T, int E, int k, int e_lo,
                                                 int e_cnt, int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
@@ -214,6 +221,10 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
                                                 int32_t* __restrict__ off, int32_t* __restrict__ act_e,
                                                 int32_t* __restrict__ n_act, int32_t* __restrict__ perm,
                                                 int32_t* __restrict__ inv, RouteStats rs) {
+#ifdef DX_ROUTE_PROF
+    long long tp[8] = {0};
+#endif
+    R1P(0);
     __shared__ int16_t ent_s[ROUTE1_MAX_ENT];                // expert of every entry (t*k + j)
     __shared__ uint32_t gm_s[ROUTE1_MAX_ENT];                // rint(gate * 2^24) of every entry (R-H1)
     __shared__ int32_t tmp[32];
@@ -225,6 +236,7 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
     for (int i = threadIdx.x; i < ROUTE1_CHUNKS * E; i += blockDim.x) { chist[i] = 0; cmass[i] = 0; }
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
+    R1P(1);
     {
         const int n4 = T * E / 4;                            // E % 4 == 0 (route1_ok)
         const float4* src = reinterpret_cast<const float4*>(logits);
@@ -233,8 +245,11 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
         for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
+    R1P(2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    // a2 + a3: one warp per token, k rounds of (value desc, id asc) warp arg-max, gates (R-G1, R-G2)
+    // a2 + a3: one warp per token, k rounds of (value desc, id asc) warp arg-max, gates (R-G1, R-G2):
+    // lane j < k evaluates e_j = dx_expf(l_j - l_0) for its rank, lane 0 forms the sequential rank-order
+    // sum from shuffles (the same operations in the same order as one thread doing it all)
     for (int t = warp; t < T; t += nwarps) {
         float v[NVT];
         uint32_t taken = 0;
@@ -248,19 +263,19 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
         float sel_v[ROUTE_MAX_K];
         int sel_e[ROUTE_MAX_K];
         topk_warp<NVT>(v, taken, k, lane, sel_v, sel_e);
-        float ev[ROUTE_MAX_K];
-        float sum = 0.0f;
-#pragma unroll
-        for (int j = 0; j < ROUTE_MAX_K; ++j) {
-            if (j >= k) break;
-            ev[j] = dx_expf(__fsub_rn(sel_v[j], sel_v[0]));
-            sum = (j == 0) ? ev[0] : __fadd_rn(sum, ev[j]);
-        }
-        float my_ev = 0.0f;                             // lane j < k handles rank j (no divergent loop)
+        float my_v = sel_v[0];
         int my_e = 0;
 #pragma unroll
         for (int j = 0; j < ROUTE_MAX_K; ++j)
-            if (j == lane) { my_ev = ev[j]; my_e = sel_e[j]; }
+            if (j == lane) { my_v = sel_v[j]; my_e = sel_e[j]; }
+        const float my_ev = lane < k ? dx_expf(__fsub_rn(my_v, sel_v[0])) : 0.0f;
+        float part[ROUTE_MAX_K];
+#pragma unroll
+        for (int j = 0; j < ROUTE_MAX_K; ++j) part[j] = __shfl_sync(0xffffffffu, my_ev, j);
+        float sum = part[0];
+#pragma unroll
+        for (int j = 1; j < ROUTE_MAX_K; ++j)
+            if (j < k) sum = __fadd_rn(sum, part[j]);
         if (lane < k) {
             const float gte = __fdiv_rn(my_ev, sum);
             idx_out[(size_t)t * k + lane] = my_e;
@@ -270,6 +285,7 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
         }
     }
     __syncthreads();
+    R1P(3);
     // per 32-entry chunk (one warp each): same-expert groups by match_any -> in-chunk rank, count, mass
     const int n = T * k;
     const int ci = warp, i = warp * 32 + lane;               // n <= 512 = 16 warps x 32 entries
@@ -302,6 +318,7 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
             }
         }
     }
+    R1P(4);
     const int32_t o = block_excl_scan<int32_t>((int32_t)c, tmp, &total_s);
     const int32_t a = block_excl_scan<int32_t>(c > 0 ? 1 : 0, tmp, &na_s);
     // active list HIGH tier first (the grouped GEMMs hand out work items in this order, heaviest first)
@@ -329,12 +346,22 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
     }
     if (threadIdx.x == 0) { off[E] = total_s; *n_act = na_s; }
     __syncthreads();
+    R1P(5);
     // a4: stable placement (entry order t asc, j asc): pos = off[e] + earlier chunks + in-chunk rank
     if (have) {
         const int pos = chist[ci * E + ei] + rk;
         perm[pos] = i;
         inv[i] = pos;
     }
+#ifdef DX_ROUTE_PROF
+    R1P(6);
+    if (threadIdx.x == 0) {
+        const unsigned c = atomicAdd(&g_route1_calls, 1u);
+        if (c == 300)
+            printf("route1 T=%d clocks: wait %lld copy %lld topk %lld chunks %lld scans %lld place %lld total %lld\n", T,
+                   tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5], tp[6] - tp[0]);
+    }
+#endif
 }
 
 // x rows gathered into the permuted order (B operand of the gate/up GEMM): Xp[inv[i]] = x[i / k]; one
