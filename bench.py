@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-batch-sweep", action="store_true")
+    ap.add_argument("--no-q80b", action="store_true")
     ap.add_argument("--switch-stress", action="store_true",
                     help="C5 (SURVEY 8(d)): one Q30B layer, n_hot swept 10%%..100%%, drift 0.5 every period; "
                          "prints the C5 JSON line instead of the main one")
@@ -387,7 +388,96 @@ def run_ours(a, rank, world, local_rank):
     if a.prefill_tokens > 0:
         out["extra"]["prefill"] = prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream)
     pool.close()
+    torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
+    del arr
     return out
+
+
+def q80b_leg(a, peak, L=8):
+    """C4's layer shape on one GPU: a Qwen3-Next-80B-A3B-shaped stack (E=512, top-10,
+    H=2048, I=512, g=128) with the paper's int4 (HIGH) / int2 (LOW) pair, the per-GPU budget
+    of C4 at G=1 (n_hot = 25 % of E, s = 1 -> 543.6 MB per layer), router mode with a drifting Zipf(1.2)
+    bias.  Decode B=64 and prefill T=4096: layer-tokens/s, the expert GEMMs' weight GB/s (decode) and
+    TFLOP/s (prefill).  L=8 layers (per-layer numbers; 48 layers of bf16 masters would not fit host RAM
+    next to C2's)."""
+    import torch
+    import synth
+    from paper_2511_15015_b200 import dx
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    E, k, H, I, g, hb, lb, s_sp = 512, 10, 2048, 512, 128, 4, 2, 1
+    seed = a.seed + 1
+    arr, ptrs = host_masters(seed, L, E, H, I, 0, 1)
+    S_h, S_l = dx.dx_slot_bytes(H, I, g, hb), dx.dx_slot_bytes(H, I, g, lb)
+    n_hot = E // 4
+    M = n_hot * S_h + (E - n_hot) * S_l + s_sp * (S_h + S_l)
+    cfg = dx.dx_config()
+    cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = L, E, k, H, I, g
+    cfg.high_bits, cfg.low_bits = hb, lb
+    cfg.expert_budget_bytes = M * L
+    cfg.n_spare, cfg.ema_alpha = s_sp, 0.95
+    cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = 16, 32, 16, 4
+    cfg.max_tokens, cfg.ep_rank, cfg.ep_size = 4096, 0, 1
+    pool = dx.Pool(cfg, ptrs, stream)
+    assert pool.info.n_hot == n_hot, (pool.info.n_hot, n_hot)
+    wr = torch.empty(L, E, H, dtype=torch.bfloat16, device=dev)
+    for l in range(L):
+        wr[l].copy_(torch.from_numpy(router_weights(seed, l, E, H, a.router_scale).view(np.int16)).view(torch.bfloat16))
+    n_ep = 8
+    bias = torch.empty(L, n_ep, E, dtype=torch.float32, device=dev)
+    for l in range(L):
+        for ep in range(n_ep):
+            bias[l, ep].copy_(torch.from_numpy(synth.zipf_logp(synth.rank_perm(seed, l, ep, E, n_hot, 0.25), 1.2)))
+    res = {"workload": f"C4 shape at G=1: {L}-layer Qwen3-Next-80B-A3B-shaped stack (E=512, top-10, H=2048, I=512), "
+                       f"int4 HIGH / int2 LOW g=128, n_hot={n_hot} (25 %), s=1, {M / 1e6:.1f} MB per layer"}
+    cnt = [0]
+    for name, T, n_t in (("decode", 64, 10), ("prefill", 4096, 2)):
+        xs = [torch.from_numpy(synth.normal_bf16(seed, 600 + T, i, 0, (T, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+              for i in range(2)]
+        y = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+
+        def qstep(x):
+            ep = min(cnt[0] // 32, n_ep - 1)
+            for l in range(L):
+                pool.dx_moe_forward(l, x, T, y, router_w=wr[l], router_bias=bias[l, ep])
+                pool.dx_hotness_update(l)
+                pool.dx_plan_precision(l)
+            cnt[0] += 1
+
+        if name == "decode":
+            for i in range(32):
+                qstep(xs[i % 2])
+            for l in range(L):
+                pool.dx_plan_precision(l)
+        for i in range(3):
+            qstep(xs[i % 2])
+        pool.dx_sync()
+        pool.dx_profile_read()
+        pool.dx_profile_enable(True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(n_t):
+            qstep(xs[i % 2])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        prof = pool.dx_profile_read()
+        pool.dx_profile_enable(False)
+        ffn_s = (prof["ffn_ms"][0] + prof["ffn_ms"][1]) / 1e3
+        wb = prof["weight_bytes"][0] + prof["weight_bytes"][1]
+        r = {"value": T * L * n_t / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / n_t, "steps": n_t,
+             "active_experts_per_layer": prof["active_experts"] / max(prof["forwards"], 1),
+             "weight_bytes_per_layer": wb / max(prof["forwards"], 1)}
+        if name == "decode":
+            r["ffn_weight_gbs"] = wb / ffn_s / 1e9 if ffn_s > 0 else 0.0
+            r["ffn_hbm_frac"] = r["ffn_weight_gbs"] / peak
+        else:
+            r["gemm_tflops"] = 2.0 * T * k * 3 * I * H * prof["forwards"] / ffn_s / 1e12 if ffn_s > 0 else 0.0
+        res[name] = r
+    pool.close()
+    torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
+    return res
 
 
 def batch_sweep(a, pool, wr, bias, step_counter, L, H, dev, stream, peak):
@@ -650,6 +740,8 @@ def main():
             print(json.dumps(switch_stress(a)), flush=True)
         return
     out = run_ours(a, rank, world, local_rank)
+    if rank == 0 and world == 1 and not a.no_q80b:
+        out["extra"]["q80b"] = q80b_leg(a, out["roofline"]["peak"])
     if rank == 0:
         if not a.no_cpu_baseline:
             v, cores, nsteps, _ = oracle_layer_sample(a, seconds=15.0)
