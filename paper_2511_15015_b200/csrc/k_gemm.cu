@@ -596,27 +596,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 gwait(&tfull[buf], (cc >> 1) & 1, 9, 256);
                 tc_fence_after();
                 named_bar(1, 128);
-                for (int col = 0; col < nvalid; col += 32) {
+                for (int col = 0; col < (a.dbg == 8 ? 0 : nvalid); col += 32) {   // DX_GEMM_DBG=8: skip the epilogue math (timing only)
                     uint32_t v[32];
                     tmem_ld32(tmem + buf * C::NBMAX + ((uint32_t)(32 * q) << 16) + col, v);
                     tmem_ld_wait();
                     if (PHASE == 0) {
-                        // rows 64-127 (up) -> smem; rows 0-63 (gate) combine: act = silu(g) * u
+                        // gate rows 0-63 (warps q < 2) meet their up rows 64-127 (q >= 2) through smem, and all
+                        // four warps share the SwiGLU: the gate warps take token columns 0-15 of the block (up
+                        // values from smem), the up warps columns 16-31 (gate values from smem).
+                        // act = bf16(silu(g) * u), silu(g) = g / (1 + e^-g)
+                        float* xu = xch;                         // [16 cols][64 rows] up values, cols 0-15
+                        float* xg = xch + 16 * 64;               // [16 cols][64 rows] gate values, cols 16-31
+                        const int rr = 32 * (q & 1) + lane;      // row within the 64-row gate/up pair block
                         if (q >= 2) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) xch[j * 64 + 32 * (q - 2) + lane] = __uint_as_float(v[j]);
+                            for (int j = 0; j < 16; ++j) xu[j * 64 + rr] = __uint_as_float(v[j]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) xg[j * 64 + rr] = __uint_as_float(v[16 + j]);
                         }
                         named_bar(1, 128);
-                        if (q < 2) {
-                            const int f = w.mb * 64 + 32 * q + lane;
+                        const int f = w.mb * 64 + rr;
+                        const int j0 = q < 2 ? 0 : 16;
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {           // fully unrolled: v[] stays in registers
-                                if (col + j < nvalid) {
-                                    const float gv = __uint_as_float(v[j]);
-                                    const float uv = xch[j * 64 + 32 * q + lane];
-                                    const float sg = gv / (1.0f + __expf(-gv));
-                                    a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
-                                }
+                        for (int jj = 0; jj < 16; ++jj) {        // fully unrolled: v[] stays in registers
+                            const int j = j0 + jj;
+                            if (col + j < nvalid) {
+                                const float gv = q < 2 ? __uint_as_float(v[jj]) : xg[jj * 64 + rr];
+                                const float uv = q < 2 ? xu[jj * 64 + rr] : __uint_as_float(v[16 + jj]);
+                                const float sg = __fdividef(gv, 1.0f + __expf(-gv));
+                                a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
                             }
                         }
                         named_bar(1, 128);

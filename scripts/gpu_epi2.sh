@@ -1,0 +1,12 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python __graft_entry__.py > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+timeout 1200 python -m pytest tests -m gpu -x -q --timeout 900 -s > gpurun_out/gpu_tests.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/gpu_tests.log; grep -i "rel err\|C2 stack\|passed\|failed\|Error" gpurun_out/gpu_tests.log | tail -8
+for b in 60 24 16; do
+  echo "== budget $b"
+  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --prefill-tokens 4096 --prefill-steps 2 --no-batch-sweep --no-q80b --budget-gb $b > gpurun_out/sweep.json 2> gpurun_out/sweep.err
+  python -c "
+import json; d=json.loads(open('gpurun_out/sweep.json').read()); r=d['roofline']; x=d['extra']; p=x['prefill']
+print('value %.0f gateup %.0f GB/s | prefill %.0f tok/s %.0f TF/s' % (d['value'], r['achieved'], p['value'], p['gemm_tflops']))" || tail -3 gpurun_out/sweep.err
+done
