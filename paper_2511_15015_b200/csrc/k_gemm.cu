@@ -37,8 +37,16 @@ namespace {
 constexpr int NTW = DX_GEMM_NTW;              // dequant transform warps (groups of 4: one per TMEM lane quarter)
 constexpr int NG = NTW / 4;                   // transform groups
 constexpr int W_EPI = 2 + NTW;                // first epilogue warp
-constexpr int W_SCHED = W_EPI + 4;            // scheduler warp
-constexpr int GEMM_THREADS = 32 * (W_SCHED + 1);
+// Epilogue warpgroups ("teams", team t drains accumulator buffer t): one for decode (the dequant warps
+// need the registers: 80 at 736 threads), two for prefill (the SwiGLU/scatter epilogue was a limiter:
+// measured +4 % prefill TFLOP/s; the same layout costs decode 7-10 % through the 72-register cap).
+template <bool DEC>
+struct Roles {
+    static constexpr int EPI_TEAMS = DEC ? 1 : 2;
+    static constexpr int W_SCHED = W_EPI + 4 * EPI_TEAMS;     // scheduler warp
+    static constexpr int THREADS = 32 * (W_SCHED + 1);
+    static constexpr int N_CONSUMERS = W_SCHED;               // warps that read the item ring
+};
 constexpr int KCH = 64;                       // K elements per chunk (128 B of bf16 per row)
 constexpr int STAGES = 6;
 constexpr int A_BYTES = 128 * 128;            // A / raw region per stage
@@ -50,7 +58,6 @@ constexpr int TPRE_BYTES = (512 + 1) * 4 + 12;   // prefill: per-active-expert N
 #define DX_GEMM_RING 2
 #endif
 constexpr int RING = DX_GEMM_RING;                       // claimed work items in flight per CTA (small: balance)
-constexpr int N_CONSUMERS = W_SCHED;          // warps that read the item ring (all but the scheduler)
 constexpr int GTAB = 16;                      // scale/zero groups per row staged in smem per item (G <= 16)
 constexpr int TAB_BYTES = 128 * GTAB * 3;     // one item's table: [128 rows][G] bf16 scales, then u8 zeros
 
@@ -61,7 +68,8 @@ struct Cfg {
     static constexpr int NBMAX = DEC ? 64 : 128;
     static constexpr int ACH = DEC ? 4 : 1;                    // K chunks per TMEM A buffer (32 columns each)
     static constexpr int NA = (512 - 2 * NBMAX) / (32 * ACH);  // TMEM A buffers: 3 (decode) / 8 (prefill)
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES + TPRE_BYTES;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + Roles<DEC>::EPI_TEAMS * XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES +
+                                TPRE_BYTES;
     __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : 128; }
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
@@ -226,13 +234,14 @@ __device__ __forceinline__ int box_rows(int nvalid) {        // B tile rows: pow
 }
 
 template <int PHASE, bool DEC>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
+__global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
+    constexpr int EPI_TEAMS = Roles<DEC>::EPI_TEAMS, W_SCHED = Roles<DEC>::W_SCHED, N_CONSUMERS = Roles<DEC>::N_CONSUMERS;
     using C = Cfg<DEC>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sS = smem;                                   // [STAGES][A 16 KB | B 16 KB]
     float* xch = reinterpret_cast<float*>(sS + STAGES * STAGE_BYTES);            // [32 cols][64 rows]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + XCH_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + EPI_TEAMS * XCH_BYTES);
     uint64_t* full = bars;                                // [STAGES] TMA landed (A or raw, and B)
     uint64_t* empty = full + STAGES;                      // [STAGES] MMA finished with the stage
     uint64_t* aready = empty + STAGES;                    // [NA] transform wrote TMEM A buffer
@@ -576,26 +585,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
             if (item >= n_items) break;
         }
     } else {
-        // ------------------------------------------------ epilogue (128 threads, warps W_EPI..W_EPI+3)
+        // ------------------------------------------------ epilogue: EPI_TEAMS warpgroups of 128 threads; team t
+        // drains the chunks that land in accumulator buffer t (cc % 2 == t with two teams), so one team's
+        // SwiGLU / scatter overlaps the next chunk's drain by the other.  Each team has its own named
+        // barrier and exchange buffer (phase 1 keeps its entry ids / gates in that buffer).
+        const int team = (warp - W_EPI) >> 2;
         const int q = warp & 3;                         // TMEM lane quarter this warp may access
-        const int et = threadIdx.x - 32 * W_EPI;        // 0..127
+        const int et = threadIdx.x - 32 * (W_EPI + 4 * team);   // 0..127
+        const uint32_t nbar = 1 + team;
+        float* xch_t = xch + team * (XCH_BYTES / 4);
+        int32_t* ent_t = team == 0 ? ent_s : reinterpret_cast<int32_t*>(xch_t);
+        float* gate_t = team == 0 ? gate_s : xch_t + 128;
         int cc = 0;
         Item w;
         for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
             const int nb = C::nb(w.bits);
             for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
                 const int buf = cc & 1;
+                if (EPI_TEAMS == 2 && buf != team) continue;   // the other team's chunk
                 const int nvalid = min(nb, w.m - n0);
                 if (PHASE == 1) {                       // entry ids and gates of this chunk's tokens -> smem
                     for (int i = et; i < nvalid; i += 128) {
                         const int ent = a.perm[w.r0 + n0 + i];
-                        ent_s[i] = ent;
-                        gate_s[i] = a.gate[ent];
+                        ent_t[i] = ent;
+                        gate_t[i] = a.gate[ent];
                     }
                 }
                 gwait(&tfull[buf], (cc >> 1) & 1, 9, 256);
                 tc_fence_after();
-                named_bar(1, 128);
+                named_bar(nbar, 128);
                 for (int col = 0; col < (a.dbg == 8 ? 0 : nvalid); col += 32) {   // DX_GEMM_DBG=8: skip the epilogue math (timing only)
                     uint32_t v[32];
                     tmem_ld32(tmem + buf * C::NBMAX + ((uint32_t)(32 * q) << 16) + col, v);
@@ -605,8 +623,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                         // four warps share the SwiGLU: the gate warps take token columns 0-15 of the block (up
                         // values from smem), the up warps columns 16-31 (gate values from smem).
                         // act = bf16(silu(g) * u), silu(g) = g / (1 + e^-g)
-                        float* xu = xch;                         // [16 cols][64 rows] up values, cols 0-15
-                        float* xg = xch + 16 * 64;               // [16 cols][64 rows] gate values, cols 16-31
+                        float* xu = xch_t;                         // [16 cols][64 rows] up values, cols 0-15
+                        float* xg = xch_t + 16 * 64;               // [16 cols][64 rows] gate values, cols 16-31
                         const int rr = 32 * (q & 1) + lane;      // row within the 64-row gate/up pair block
                         if (q >= 2) {
 #pragma unroll
@@ -615,7 +633,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
 #pragma unroll
                             for (int j = 0; j < 16; ++j) xg[j * 64 + rr] = __uint_as_float(v[16 + j]);
                         }
-                        named_bar(1, 128);
+                        named_bar(nbar, 128);
                         const int f = w.mb * 64 + rr;
                         const int j0 = q < 2 ? 0 : 16;
 #pragma unroll
@@ -628,14 +646,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                                 a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
                             }
                         }
-                        named_bar(1, 128);
+                        named_bar(nbar, 128);
                     } else {
                         const int h = w.mb * 128 + 32 * q + lane;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {           // fully unrolled: v[] stays in registers
                             if (col + j < nvalid && h < a.H) {
-                                const int ent = ent_s[col + j];
-                                a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(gate_s[col + j] * __uint_as_float(v[j]));
+                                const int ent = ent_t[col + j];
+                                a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(gate_t[col + j] * __uint_as_float(v[j]));
                             }
                         }
                     }
@@ -643,7 +661,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_gemm(const __grid_constant_
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[buf]);
-                named_bar(1, 128);                      // ent_s / gate_s / xch reused by the next chunk
+                named_bar(nbar, 128);                      // ent_s / gate_s / xch reused by the next chunk
             }
         }
     }
@@ -671,7 +689,7 @@ void launch_one(const GemmMaps& maps, const GemmArgs& a, int items, cudaStream_t
         attr = true;
     }
     const int grid = items < DX_NUM_SMS ? items : DX_NUM_SMS;    // persistent: one CTA per SM
-    dx_launch(k_gemm<PHASE, DEC>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, st, g_dx_pdl, maps, a);
+    dx_launch(k_gemm<PHASE, DEC>, dim3(grid), dim3(Roles<DEC>::THREADS), C::SMEM, st, g_dx_pdl, maps, a);
 }
 
 }  // namespace
