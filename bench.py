@@ -301,8 +301,10 @@ def run_ours(a, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
+        h0 = time.perf_counter()
         for s_ in range(a.steps):
             step(xs[base + s_])
+        host_ms = (time.perf_counter() - h0) * 1e3      # host issue time of the timed steps (no sync inside)
         ev1.record(stream)
         torch.cuda.synchronize()
     if dist_on:
@@ -378,7 +380,8 @@ def run_ours(a, rank, world, local_rank):
                              "exposed_frac_of_step_time": prof["exposed_ms"] / ms if ms > 0 else None,
                              "xfer_ms_mean": prof["xfer_ms"] / max(prof["plans"], 1),
                              "xfer_ms_max": prof["xfer_max_ms"]},
-                  "setup_s": {"masters": t_gen, "pool_create": t_pool}},
+                  "setup_s": {"masters": t_gen, "pool_create": t_pool},
+                  "host_issue_ms_per_step": host_ms / a.steps},
     }
     clock = clk.summary()
     if clock:
