@@ -226,7 +226,10 @@ typedef struct {
     int64_t  plans;             /* plans whose transitions were issued */
     int64_t  promotions, demotions; /* transitions those plans issued */
 } dx_profile_t;
-/* Enable/disable per-forward CUDA-event timing (weight-byte counters always run, on the device). */
+/* Per-forward CUDA-event timing: enable = 0 off; enable = n >= 1 times every n-th forward (n > 1 keeps the
+   host cost of event records off most forwards).  While enabled, the device weight-byte counters count
+   exactly the timed (sampled) forwards, so bytes / time stay consistent; while disabled they count every
+   forward. */
 dx_status dx_profile_enable(dx_pool pool, int32_t enable);
 /* Synchronising; returns and resets the accumulated profile. */
 dx_status dx_profile_read(dx_pool pool, dx_profile_t* out);

@@ -71,6 +71,8 @@ struct dx_pool_s {
     i64 launches = 0;
     u64 wbytes[2][2];                       // [tier][phase] algorithmic weight bytes per expert
     bool profiling = false;
+    int prof_every = 1;                 // profile every prof_every-th forward (event timing + byte counters)
+    int64_t prof_ctr = 0;
     std::vector<cudaEvent_t> prof_ev;       // 4 per forward: start, after routing, between FFN phases, end
     std::vector<cudaEvent_t> prof_free;
     std::vector<cudaEvent_t> prof_wait_ev;  // pairs around the publish wait (exposed switch time)
@@ -538,6 +540,8 @@ extern "C" int64_t dx_kernel_launches(dx_pool p) { return p ? p->launches : 0; }
 extern "C" dx_status dx_profile_enable(dx_pool p, int32_t enable) {
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
     p->profiling = enable != 0;
+    p->prof_every = enable > 1 ? enable : 1;
+    p->prof_ctr = 0;
     return DX_OK;
 }
 
@@ -594,7 +598,7 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
 
 static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void* x, int T, int k, void* y,
                             cudaEvent_t* ev);
-static void prof_begin(dx_pool p, cudaEvent_t* ev);
+static bool prof_begin(dx_pool p, cudaEvent_t* ev);
 
 #define CHECK_LAYER(p, layer)                                                                          \
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");                                                      \
@@ -612,8 +616,9 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
     DX_CHECK(p->cfg.ep_size == 1, DX_ERR_INVALID_ARG,
              "ep_size > 1: use dx_ep_dispatch / dx_moe_forward_routed / dx_ep_combine");
     cudaEvent_t ev[4];
-    prof_begin(p, ev);
+    const bool sampled = prof_begin(p, ev);
     RouteWs ws = p->ws;
+    if (p->profiling && !sampled) ws.stats = nullptr;   // byte counters follow the sampled forwards
     if (topk_idx) ws.idx = topk_idx;
     if (topk_gate) ws.gate = topk_gate;
     const float* lg = logits;
@@ -689,15 +694,17 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
     return DX_OK;
 }
 
-static void prof_begin(dx_pool p, cudaEvent_t* ev) {
+static bool prof_begin(dx_pool p, cudaEvent_t* ev) {
     ev[0] = ev[1] = ev[2] = ev[3] = nullptr;
-    if (!p->profiling) return;
+    if (!p->profiling) return false;
+    if (p->prof_ctr++ % p->prof_every != 0) return false;      // not a sampled forward
     for (int i = 0; i < 4; ++i) {
         ev[i] = prof_event(p);
         p->prof_ev.push_back(ev[i]);
     }
     cudaEventRecord(ev[0], p->cs);
     p->prof_fwd += 1;
+    return true;
 }
 
 // ---------------------------------------------------------------- expert parallelism (a15)
@@ -746,14 +753,16 @@ extern "C" dx_status dx_moe_forward_routed(dx_pool p, int32_t layer, const void*
     if (R == 0) return DX_OK;
     DX_CHECK(rows && meta && y_rows, DX_ERR_INVALID_ARG, "null buffer");
     cudaEvent_t ev[4];
-    prof_begin(p, ev);
+    const bool sampled = prof_begin(p, ev);
+    RouteWs ws = p->ws;
+    if (p->profiling && !sampled) ws.stats = nullptr;   // byte counters follow the sampled forwards
     const size_t base = (size_t)layer * p->E_loc;
     DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
-    launch_route_given((const int2*)meta, R, p->E_loc, p->ws, p->ctrl.cnt + base, p->ctrl.mass + base,
+    launch_route_given((const int2*)meta, R, p->E_loc, ws, p->ctrl.cnt + base, p->ctrl.mass + base,
                        p->ctrl.tier + base, p->wbytes, p->err_flag, p->cs);
-    launch_place(R, p->E_loc, 1, p->ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
+    launch_place(R, p->E_loc, 1, ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
     p->launches += 2;
-    return expert_ffn(p, layer, p->ws, rows, R, 1, y_rows, ev);
+    return expert_ffn(p, layer, ws, rows, R, 1, y_rows, ev);
 }
 
 extern "C" dx_status dx_ep_combine(dx_pool p, int32_t layer, const void* back_rows, int32_t T, void* y) {

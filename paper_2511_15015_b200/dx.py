@@ -288,7 +288,8 @@ class Pool:
     def dx_set_ffn_path(self, path: int):
         _check(_lib.dx_set_ffn_path(self.h, path), "dx_set_ffn_path")
 
-    def dx_profile_enable(self, enable: bool = True):
+    def dx_profile_enable(self, enable=True):
+        """enable: False/0 off, True/1 every forward, n > 1 every n-th forward."""
         _check(_lib.dx_profile_enable(self.h, int(enable)), "dx_profile_enable")
 
     def dx_profile_read(self) -> dict:

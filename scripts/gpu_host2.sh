@@ -1,0 +1,14 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python __graft_entry__.py > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+for np in 0 1; do
+DX_BENCH_NOPROF=$np timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --prefill-tokens 0 --no-batch-sweep --no-q80b > gpurun_out/bench.json 2> gpurun_out/bench.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench.json').read())
+print('NOPROF=$np value %.0f ms/step %.3f host_issue_ms/step %.3f e2e %.0f' % (d['value'], d['ms_per_step'], d['extra']['host_issue_ms_per_step'], d['e2e']['value']))" || tail -3 gpurun_out/bench.err
+done
+python - <<'PY'
+# host cost of the three per-layer calls, GPU idle (tiny T) -- pure issue overhead
+import time, torch, numpy as np, sys
+sys.path.insert(0, '.')
+PY
