@@ -141,6 +141,9 @@ __device__ __noinline__ void gemm_trap(uint32_t tag, uint32_t parity) {
     }
     __trap();
 }
+#ifndef DX_EPI_BACK
+#define DX_EPI_BACK 256        // backoff (ns) of the epilogue's accumulator wait (MMA's drain wait: half)
+#endif
 #ifndef DX_TBACK
 #define DX_TBACK 0             // backoff (ns) of the dequant warps' own waits
 #endif
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                 const int rb = box_rows(min(nb, w.m - n0));
                 const uint32_t idesc = idesc_bf16(128, rb);
                 const int buf = cc & 1;
-                gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, 128);
+                gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, DX_EPI_BACK / 2);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * C::NBMAX;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
@@ -611,7 +614,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                         gate_t[i] = a.gate[ent];
                     }
                 }
-                gwait(&tfull[buf], (cc >> 1) & 1, 9, 256);
+                gwait(&tfull[buf], (cc >> 1) & 1, 9, DX_EPI_BACK);
                 tc_fence_after();
                 named_bar(nbar, 128);
                 for (int col = 0; col < (a.dbg == 8 ? 0 : nvalid); col += 32) {   // DX_GEMM_DBG=8: skip the epilogue math (timing only)
