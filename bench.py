@@ -750,6 +750,9 @@ def main():
     import __graft_entry__
     if rank == 0:
         __graft_entry__.build()
+    if world > 1:                      # the other ranks load libdx.so only once rank 0 has (re)built it
+        import torch.distributed as dist
+        dist.barrier()
     if a.switch_stress:
         if rank == 0:
             print(json.dumps(switch_stress(a)), flush=True)
