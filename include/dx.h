@@ -123,6 +123,19 @@ dx_status dx_moe_forward(dx_pool pool, int32_t layer, const void* x_bf16, int32_
                          const void* router_w_bf16, const float* router_bias, const float* logits,
                          void* y_bf16, int32_t* topk_idx, float* topk_gate);
 
+/* One serving step of one layer: dx_moe_forward + dx_hotness_update + dx_plan_precision, with the EMA fold
+ * and publication (a10, a14) fused into the combine launch (same results, bit for bit, as the three calls;
+ * the fold runs after the layer's GEMMs so the table flip never races them).  Arguments as dx_moe_forward;
+ * T = 0 folds an empty step (passive decay).  Asynchronous on the compute stream. */
+dx_status dx_moe_step(dx_pool pool, int32_t layer, const void* x_bf16, int32_t T,
+                      const void* router_w_bf16, const float* router_bias, const float* logits,
+                      void* y_bf16, int32_t* topk_idx, float* topk_gate);
+
+/* The fp32 router logits [T][E] of the last router-mode forward of this pool (exactly what its top-k
+ * consumed), into host memory of cap >= T*E floats.  Synchronising.  NOT_READY if the last forward was
+ * in trace mode. */
+dx_status dx_get_logits(dx_pool pool, float* host_out, int64_t cap);
+
 /* ---------------------------------------------------------------- expert parallelism
  * ep_size G > 1: GPU r owns experts [r*E/G, (r+1)*E/G) (its pool holds only those, master pointers
  * [L][E/G]); tokens are data-parallel.  One layer is dispatch -> all-to-all -> owner FFN ->
@@ -170,7 +183,9 @@ dx_status dx_plan_precision(dx_pool pool, int32_t layer, dx_plan* out);
 dx_status dx_promote(dx_pool pool, int32_t layer, const int32_t* experts, int32_t n);
 dx_status dx_demote(dx_pool pool, int32_t layer, const int32_t* experts, int32_t n);
 
-/* Wait for all compute- and side-stream work of the pool (does not move the publish schedule). */
+/* Wait for all compute- and side-stream work of the pool (does not move the publish schedule).
+ * Reports (and clears) the sticky device error: RANGE if dx_moe_forward_routed received an expert id
+ * outside [0, E_loc) since the last dx_sync (such rows were routed with gate 0, output 0). */
 dx_status dx_sync(dx_pool pool);
 
 /* ---------------------------------------------------------------- inspection (synchronising) */

@@ -83,7 +83,15 @@ int or_route(const float* logits, int32_t T, int32_t E, int32_t k, int32_t* idx,
     int rc = 0;
     for (int32_t t = 0; t < T && rc == 0; ++t) {
         const float* l = logits + (size_t)t * E;
-        for (int32_t e = 0; e < E; ++e) { if (!isfinite(l[e])) rc = -1; taken[e] = 0; }
+        /* R-G3: -inf marks a masked expert (ranked below every finite logit, gate 0 since
+         * or_expf(-inf) = 0); NaN / +inf, or a token with no finite logit, violate O-1's precondition. */
+        int32_t nfin = 0;
+        for (int32_t e = 0; e < E; ++e) {
+            if (isnan(l[e]) || (isinf(l[e]) && l[e] > 0)) rc = -1;
+            nfin += isfinite(l[e]) ? 1 : 0;
+            taken[e] = 0;
+        }
+        if (nfin == 0) rc = -1;
         if (rc) break;
         for (int32_t j = 0; j < k; ++j) {
             int32_t best = -1;

@@ -30,7 +30,7 @@ uint16_t or_f64_to_bf16_rn(double d);
 /* ---- O-1 router, top-k, gates (Eq.1 "K = topk({g_i(x)})") ---- */
 float or_expf(float x);                                   /* DESIGN.md R-G2 recipe, x <= 0 */
 int   or_route(const float* logits, int32_t T, int32_t E, int32_t k,
-               int32_t* idx, float* gate);                /* 0 ok, -1 non-finite input */
+               int32_t* idx, float* gate);                /* 0 ok, -1 NaN/+inf or no finite logit (R-G3) */
 void  or_router_logits(const uint16_t* x, const uint16_t* wr, const float* bias,
                        int32_t T, int32_t E, int32_t H, double* logits);
 
@@ -74,7 +74,8 @@ void     or_ctrl_fold(or_ctrl* c, const uint64_t* mass, uint64_t B_tot);
 /* returns number of commands written (>=0), or -1 when no plan is due at this step.
  * dir: +1 promote, -1 demote, 0 relayout move (finalize only).  *finalize set to 1 at t==W. */
 int32_t  or_ctrl_plan(or_ctrl* c, int32_t* expert, int32_t* dir, int32_t* dst, int32_t* finalize);
-/* manual command; returns 0 ok, 2 range, 4 pool exhausted, 5 busy, 3 wrong tier */
+/* manual command (Alg. 1 EnqueueUpgrade/EnqueueDowngrade for a given expert);
+ * returns 0 ok, 1 wrong tier or warm-up not finished, 2 range, 4 pool exhausted (deferred), 5 busy */
 int32_t  or_ctrl_command(or_ctrl* c, int32_t e, int32_t dir);
 void     or_ctrl_state(const or_ctrl* c, double* S, int32_t* tier, int32_t* slot, uint32_t* version,
                        int64_t* last, int32_t* in_flight, int64_t* t, double* tau,

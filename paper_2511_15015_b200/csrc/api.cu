@@ -54,6 +54,7 @@ struct dx_pool_s {
     __nv_bfloat16* act = nullptr;
     __nv_bfloat16* Y = nullptr;
     int32_t* err_flag = nullptr;
+    int32_t* dev_err = nullptr;             // sticky device-side error (EP routed rows), reported by dx_sync
     int32_t* gemm_sched = nullptr;      // [phase][ticket counter, CTAs done] of the grouped GEMMs (self-resetting)
     int2* manual_cmds = nullptr;
     int32_t* manual_status = nullptr;
@@ -79,6 +80,8 @@ struct dx_pool_s {
     std::vector<cudaEvent_t> prof_xfer_ev;  // pairs around side-stream transitions (switch latency)
     i64 prof_fwd = 0;
     int ffn_path = 0;                       // 0: tcgen05 grouped GEMM, 1: mma.sync decode kernel
+    bool last_logits_router = false;        // the last forward computed router logits into ws.logits
+    int last_T = 0;
     __nv_bfloat16* Xp = nullptr;            // x rows in permuted order (B operand of gate/up)
     std::vector<GemmMaps> gmaps;            // per layer (weights); xb filled per launch
     CUtensorMap xb0[4], xb1[4];             // B operand maps (Xp / act) for tiles of 16, 32, 64, 128 rows
@@ -292,10 +295,10 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         ctrl_bytes = LE * (4 + 4 + 4 + 8 + 4 + 8 + 8 + 4 + 4 + 8 + 16) + LO * 8 + L * (8 + 8 + 4 * 3) + 64 * 256;
     }
     const size_t lg_rows = (size_t)T;
-    size_t ws_bytes = lg_rows * p->E * 4 + n_ent * (4 + 4 + 4 + 4) + (size_t)nblk * p->E * 8 +
+    size_t ws_bytes = lg_rows * p->E * 4 + n_ent * (4 + 4 + 4 + 4 + 2 + 4) + 3 * 256 + (size_t)nblk * p->E * 8 +
                       (size_t)(p->E + 1) * 8 + n_ent * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8 + 256;
     if (G > 1)   // dispatch-side routing workspace (global experts, local tokens)
-        ws_bytes += lg_rows * p->E * 4 + (size_t)T * k * 16 + (size_t)route_blocks(T) * p->E * 8 +
+        ws_bytes += lg_rows * p->E * 4 + (size_t)T * k * 22 + 3 * 256 + (size_t)route_blocks(T) * p->E * 8 +
                     (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
     const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
@@ -345,6 +348,9 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     w.inv = carve<int32_t>(q, n_ent);
     w.stats = carve<u64>(q, 4);
     w.done = carve<unsigned>(q, 1);
+    w.ent = carve<int16_t>(q, n_ent);
+    w.gm = carve<uint32_t>(q, n_ent);
+    w.gbar = carve<unsigned>(q, 2);
     if (G > 1) {
         RouteWs& v = p->ws_src;
         v.logits = carve<float>(q, lg_rows * p->E);
@@ -359,11 +365,15 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         v.inv = carve<int32_t>(q, (size_t)T * k);
         v.stats = nullptr;
         v.done = carve<unsigned>(q, 1);
+        v.ent = carve<int16_t>(q, (size_t)T * k);
+        v.gm = carve<uint32_t>(q, (size_t)T * k);
+        v.gbar = carve<unsigned>(q, 2);
     }
     p->act = carve<__nv_bfloat16>(q, n_ent * p->I);
     p->Y = carve<__nv_bfloat16>(q, n_ent * p->H);
     p->Xp = carve<__nv_bfloat16>(q, n_ent * p->H);
     p->err_flag = carve<int32_t>(q, 1);
+    p->dev_err = carve<int32_t>(q, 1);
     p->gemm_sched = carve<int32_t>(q, 4);
     p->manual_cmds = carve<int2>(q, 1024);
     p->manual_status = carve<int32_t>(q, 1024);
@@ -454,10 +464,15 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         DX_CUDA(cudaMemcpyAsync(c.cap_hi, chi.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
         DX_CUDA(cudaMemcpyAsync(c.plan_n, pn.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
         DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
+        DX_CUDA(cudaMemsetAsync(p->dev_err, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(p->gemm_sched, 0, 16, p->cs));
         DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
         DX_CUDA(cudaMemsetAsync(w.done, 0, 4, p->cs));
-        if (G > 1) DX_CUDA(cudaMemsetAsync(p->ws_src.done, 0, 4, p->cs));
+        DX_CUDA(cudaMemsetAsync(w.gbar, 0, 8, p->cs));
+        if (G > 1) {
+            DX_CUDA(cudaMemsetAsync(p->ws_src.done, 0, 4, p->cs));
+            DX_CUDA(cudaMemsetAsync(p->ws_src.gbar, 0, 8, p->cs));
+        }
         DX_CUDA(cudaMemsetAsync(c.tstats, 0, 16, p->cs));
         DX_CUDA(cudaStreamSynchronize(p->cs));
     }
@@ -597,30 +612,29 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
 }
 
 static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void* x, int T, int k, void* y,
-                            cudaEvent_t* ev);
+                            cudaEvent_t* ev, bool fuse_fold = false);
 static bool prof_begin(dx_pool p, cudaEvent_t* ev);
+static dx_status fold(dx_pool p, int layer);
+static dx_status fold_prepare(dx_pool p, int layer, FoldReq* req);
 
 #define CHECK_LAYER(p, layer)                                                                          \
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");                                                      \
     DX_CHECK((layer) >= 0 && (layer) < (p)->L, DX_ERR_RANGE, "layer %d out of range [0,%d)", (int)(layer), (p)->L)
 
-extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
-                                    const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
-                                    float* topk_gate) {
-    CHECK_LAYER(p, layer);
-    DX_CHECK(T >= 0 && T <= p->cfg.max_tokens, DX_ERR_RANGE, "T=%d outside [0, max_tokens=%d]", T, p->cfg.max_tokens);
-    if (T == 0) return DX_OK;
-    DX_CHECK(x && y, DX_ERR_INVALID_ARG, "null x/y");
-    DX_CHECK((router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG,
-             "exactly one of router_w (router mode) and logits (trace mode) must be given");
-    DX_CHECK(p->cfg.ep_size == 1, DX_ERR_INVALID_ARG,
-             "ep_size > 1: use dx_ep_dispatch / dx_moe_forward_routed / dx_ep_combine");
-    cudaEvent_t ev[4];
-    const bool sampled = prof_begin(p, ev);
-    RouteWs ws = p->ws;
-    if (p->profiling && !sampled) ws.stats = nullptr;   // byte counters follow the sampled forwards
-    if (topk_idx) ws.idx = topk_idx;
-    if (topk_gate) ws.gate = topk_gate;
+// a1-a5: routing of T tokens over this pool's experts into `ws` (+ the x gather for the tcgen05 path).
+// Decode batches (T*k <= 512): one fused multi-CTA launch; larger batches: router, top-k/counters/scan,
+// placement.
+static void route_tokens(dx_pool p, int layer, const void* x, int T, const void* router_w, const float* router_bias,
+                         const float* logits, RouteWs& ws) {
+    const size_t base = (size_t)layer * p->E_loc;
+    __nv_bfloat16* Xp = p->ffn_path == 1 ? nullptr : p->Xp;
+    if (route_dec_ok(T, p->E, p->k)) {
+        launch_route_dec((const __nv_bfloat16*)x, (const __nv_bfloat16*)router_w, router_bias, router_w ? nullptr : logits,
+                         T, p->E, p->k, p->H, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->ctrl.tier + base,
+                         p->wbytes, Xp, p->cs);
+        p->launches += 1;
+        return;
+    }
     const float* lg = logits;
     if (router_w) {
         launch_router((const __nv_bfloat16*)x, (const __nv_bfloat16*)router_w, router_bias, T, p->E, p->H, ws.logits,
@@ -628,30 +642,64 @@ extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int
         lg = ws.logits;
         p->launches += 1;
     }
-    const size_t base = (size_t)layer * p->E_loc;
-    // a2+a3 (+ the a4 offset scan in the last block), then a4 placement (+ x gather for tcgen05)
-    __nv_bfloat16* Xp = p->ffn_path == 1 ? nullptr : p->Xp;
-    if (route1_ok(T, p->E, p->k)) {
-        launch_route1(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base,
-                      p->ctrl.mass + base, p->ctrl.tier + base, p->wbytes, p->cs);
-        launch_gather(T, p->k, ws, (const __nv_bfloat16*)x, p->H, Xp, p->cs);
-        p->launches += Xp ? 2 : 1;
-    } else {
-        launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base,
-                     p->ctrl.mass + base, p->ctrl.tier + base, p->wbytes, p->cs);
-        launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, Xp, p->cs);
-        p->launches += 2;
-    }
-    dx_status st = expert_ffn(p, layer, ws, x, T, p->k, y, ev);
-    if (st != DX_OK) return st;
+    launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->ctrl.tier + base,
+                 p->wbytes, p->cs);
+    launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, Xp, p->cs);
+    p->launches += 2;
+}
+
+static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
+                              const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
+                              float* topk_gate, bool fuse_fold) {
+    CHECK_LAYER(p, layer);
+    DX_CHECK(T >= 0 && T <= p->cfg.max_tokens, DX_ERR_RANGE, "T=%d outside [0, max_tokens=%d]", T, p->cfg.max_tokens);
+    DX_CHECK(T == 0 || (x && y), DX_ERR_INVALID_ARG, "null x/y");
+    DX_CHECK(T == 0 || (router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG,
+             "exactly one of router_w (router mode) and logits (trace mode) must be given");
+    DX_CHECK(p->cfg.ep_size == 1, DX_ERR_INVALID_ARG,
+             "ep_size > 1: use dx_ep_dispatch / dx_moe_forward_routed / dx_ep_combine");
+    if (T == 0) return fuse_fold ? fold(p, layer) : DX_OK;
+    cudaEvent_t ev[4];
+    const bool sampled = prof_begin(p, ev);
+    RouteWs ws = p->ws;
+    if (p->profiling && !sampled) ws.stats = nullptr;   // byte counters follow the sampled forwards
+    if (topk_idx) ws.idx = topk_idx;
+    if (topk_gate) ws.gate = topk_gate;
+    p->last_logits_router = router_w != nullptr;
+    p->last_T = T;
+    route_tokens(p, layer, x, T, router_w, router_bias, logits, ws);
     p->pend_tokens[layer] += (u64)T;
+    return expert_ffn(p, layer, ws, x, T, p->k, y, ev, fuse_fold);
+}
+
+extern "C" dx_status dx_moe_forward(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
+                                    const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
+                                    float* topk_gate) {
+    return forward_impl(p, layer, x, T, router_w, router_bias, logits, y, topk_idx, topk_gate, false);
+}
+
+extern "C" dx_status dx_moe_step(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
+                                 const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
+                                 float* topk_gate) {
+    dx_status st = forward_impl(p, layer, x, T, router_w, router_bias, logits, y, topk_idx, topk_gate, true);
+    if (st != DX_OK) return st;
+    return dx_plan_precision(p, layer, nullptr);
+}
+
+extern "C" dx_status dx_get_logits(dx_pool p, float* host_out, int64_t cap) {
+    DX_CHECK(p && host_out, DX_ERR_INVALID_ARG, "null pool/out");
+    DX_CHECK(p->last_logits_router, DX_ERR_NOT_READY, "the last forward was not in router mode");
+    const int64_t n = (int64_t)p->last_T * p->E;
+    DX_CHECK(cap >= n, DX_ERR_INVALID_ARG, "output too small (%lld < %lld)", (long long)cap, (long long)n);
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    DX_CUDA(cudaMemcpy(host_out, p->ws.logits, n * 4, cudaMemcpyDeviceToHost));
     return DX_OK;
 }
 
 // a6-a8 on rows already routed and placed in `ws`: grouped expert GEMMs over the slot pool, then the
 // weighted combine of k rows per token into y (k = 1: the rows themselves, EP owner side).
 static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void* x, int T, int k, void* y,
-                            cudaEvent_t* ev) {
+                            cudaEvent_t* ev, bool fuse_fold) {
     const size_t base = (size_t)layer * p->E_loc;
     const int E = p->E_loc;
     ExpertArgs a;
@@ -687,7 +735,15 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         launch_gemm(1, dec, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
     }
     if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));
-    launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs);
+    if (fuse_fold) {
+        // a8 + a10 + a14 in one launch: the fold block runs after the down GEMM (griddepcontrol.wait)
+        FoldReq req;
+        dx_status st = fold_prepare(p, layer, &req);
+        if (st != DX_OK) return st;
+        launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs, nullptr, &p->ctrl, &req);
+    } else {
+        launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs);
+    }
     p->launches += 3;
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "launch failed: %s", cudaGetErrorString(ce));
@@ -757,9 +813,10 @@ extern "C" dx_status dx_moe_forward_routed(dx_pool p, int32_t layer, const void*
     RouteWs ws = p->ws;
     if (p->profiling && !sampled) ws.stats = nullptr;   // byte counters follow the sampled forwards
     const size_t base = (size_t)layer * p->E_loc;
-    DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
+    // an out-of-range expert id in `meta` is routed to expert 0 with gate 0 (its output row is 0) and raises
+    // the sticky device error that the next dx_sync reports as DX_ERR_RANGE
     launch_route_given((const int2*)meta, R, p->E_loc, ws, p->ctrl.cnt + base, p->ctrl.mass + base,
-                       p->ctrl.tier + base, p->wbytes, p->err_flag, p->cs);
+                       p->ctrl.tier + base, p->wbytes, p->dev_err, p->cs);
     launch_place(R, p->E_loc, 1, ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
     p->launches += 2;
     return expert_ffn(p, layer, ws, rows, R, 1, y_rows, ev);
@@ -778,12 +835,13 @@ extern "C" dx_status dx_ep_combine(dx_pool p, int32_t layer, const void* back_ro
     return DX_OK;
 }
 
-static dx_status fold(dx_pool p, int layer) {
+// Host side of a10/a14: the step count, B_tot and -- when transitions publish at the new step -- the
+// compute stream's wait for the side stream (the exposed switch time, if any, is spent in that wait).
+static dx_status fold_prepare(dx_pool p, int layer, FoldReq* req) {
     const u64 B = p->pend_tokens[layer];
     p->pend_tokens[layer] = 0;
     const i64 t_new = p->t[layer] + 1;
     if (p->publish_at[layer] == t_new) {
-        // exposed switch time, if any, is spent here: registration waits for the side stream
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (p->profiling) {
             e0 = prof_event(p);
@@ -796,9 +854,18 @@ static dx_status fold(dx_pool p, int layer) {
         if (e1) DX_CUDA(cudaEventRecord(e1, p->cs));
         p->publish_at[layer] = -1;
     }
-    launch_fold(p->ctrl, layer, B, p->cs);
-    p->launches += 1;
     p->t[layer] = t_new;
+    req->layer = layer;
+    req->B_tot = B;
+    return DX_OK;
+}
+
+static dx_status fold(dx_pool p, int layer) {
+    FoldReq req;
+    dx_status st = fold_prepare(p, layer, &req);
+    if (st != DX_OK) return st;
+    launch_fold(p->ctrl, layer, req.B_tot, p->cs);
+    p->launches += 1;
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "fold launch failed: %s", cudaGetErrorString(ce));
     return DX_OK;
@@ -816,7 +883,8 @@ extern "C" dx_status dx_hotness_update_from(dx_pool p, int32_t layer, const int3
     const size_t base = (size_t)layer * p->E_loc;
     if (T > 0) {
         DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
-        launch_counts_from(idx, gate, T, p->E, p->k, p->e_lo, p->ctrl.cnt + base, p->ctrl.mass + base, p->err_flag, p->cs);
+        launch_counts_from(idx, gate, T, p->E, p->E_loc, p->k, p->e_lo, p->ctrl.cnt + base, p->ctrl.mass + base,
+                           p->err_flag, p->cs);
         p->launches += 1;
         int32_t err = 0;
         DX_CUDA(cudaMemcpyAsync(&err, p->err_flag, 4, cudaMemcpyDeviceToHost, p->cs));
@@ -916,6 +984,9 @@ static dx_status manual(dx_pool p, int layer, const int32_t* experts, int n, int
              "layer %d has transitions publishing at a different step", layer);
     std::vector<int2> cmds(n);
     for (int i = 0; i < n; ++i) cmds[i] = make_int2(experts[i], dir);
+    // k_manual rewrites the layer's command list (plan_cmd / plan_n): transitions issued earlier for this
+    // layer must have finished reading it on the side stream first
+    if (p->publish_at[layer] >= 0) DX_CUDA(cudaStreamWaitEvent(p->cs, p->ev_side[layer], 0));
     DX_CUDA(cudaMemcpyAsync(p->manual_cmds, cmds.data(), n * sizeof(int2), cudaMemcpyHostToDevice, p->cs));
     launch_manual(p->ctrl, layer, p->manual_cmds, n, p->manual_status, p->cs);
     DX_CUDA(cudaEventRecord(p->ev_plan, p->cs));
@@ -952,6 +1023,13 @@ extern "C" dx_status dx_sync(dx_pool p) {
     DX_CUDA(cudaStreamSynchronize(p->ss));
     DX_CUDA(cudaStreamSynchronize(p->cs));
     DX_CUDA(cudaGetLastError());
+    int32_t err = 0;
+    DX_CUDA(cudaMemcpy(&err, p->dev_err, 4, cudaMemcpyDeviceToHost));
+    if (err) {
+        DX_CUDA(cudaMemset(p->dev_err, 0, 4));
+        dx_set_error("dx_moe_forward_routed received an expert id outside [0, E_loc) (row output set to 0)");
+        return DX_ERR_RANGE;
+    }
     return DX_OK;
 }
 

@@ -83,6 +83,37 @@ struct Ctrl {
 
 #define DX_NEVER (-(i64)(1ULL << 61))
 
+#ifdef __CUDACC__
+// a10 + a14 for one layer, run by ONE thread block (any size): Eq. 2 with Alg. 1's passive
+// decay, S <- alpha*S + (1-alpha)*gbar in fp64 without contraction (R-H2), counters cleared, then the
+// registration of transitions due at the new step (R-T1): table flip, version++, the old block reclaimed
+// (PAPER.md:238).  Used by k_fold and by the combine kernel's fold block (fused step).
+__device__ __forceinline__ void fold_layer(const Ctrl& c, int layer, u64 B_tot, double oma) {
+    const int E = c.E;
+    const i64 t_new = c.t[layer] + 1;
+    __syncthreads();
+    const double denom = __dmul_rn((double)B_tot, 16777216.0);
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int i = layer * E + e;
+        const double gbar = B_tot ? __ddiv_rn((double)c.mass[i], denom) : 0.0;
+        c.S[i] = __dadd_rn(__dmul_rn(c.alpha, c.S[i]), __dmul_rn(oma, gbar));
+        c.cnt[i] = 0;
+        c.mass[i] = 0;
+        if (c.pend_dir[i] != 0 && c.pend_at[i] == t_new) {      // registration + reclaim
+            const int old = c.slot[i];
+            const int ob = layer * (E + c.s);
+            if (c.pend_dir[i] > 0) { c.lo_owner[ob + old] = -1; c.tier[i] = 1; }
+            else                   { c.hi_owner[ob + old] = -1; c.tier[i] = 0; }
+            c.slot[i] = c.pend_dst[i];
+            c.version[i] += 1;
+            c.pend_dir[i] = 0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) c.t[layer] = t_new;
+}
+#endif
+
 // ---------------------------------------------------------------- programmatic dependent launch
 // Every hot-path kernel waits for its predecessor's memory with griddepcontrol.wait (a no-op when it
 // was launched without the PDL attribute) and immediately allows its successor to be scheduled, so
@@ -109,6 +140,17 @@ static inline cudaError_t dx_launch(void (*kern)(KArgs...), dim3 grid, dim3 bloc
 }
 #endif
 extern bool g_dx_pdl;   // library-wide switch (default on; DX_PDL=0 disables)
+
+// Function attributes (large dynamic smem) are per device context: true the first time it is called for
+// the current device with this mask (one static mask per kernel).
+static inline bool dx_first_on_device(unsigned long long& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+}
 
 // ---------------------------------------------------------------- numerics
 __device__ __forceinline__ float dx_bf2f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
@@ -169,6 +211,9 @@ struct RouteWs {
     int32_t* inv;         // [T*k] permuted row of entry
     u64* stats;           // [4] device counters: weight bytes gate/up, down, active experts, -
     unsigned* done;       // [1] route-block completion counter (last block runs the scan)
+    int16_t* ent;         // [T*k] decode routing: expert of every entry (cross-CTA exchange)
+    uint32_t* gm;         // [T*k] decode routing: rint(gate * 2^24) of every entry
+    unsigned* gbar;       // [2] decode routing: grid barrier {arrivals, generation}
 };
 struct RouteStats {       // profiling: algorithmic weight bytes per touched expert [tier][phase]
     const int32_t* tier;
@@ -182,23 +227,30 @@ void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float*
 // tier: layer table (or NULL); bytes[tier][phase]: algorithmic weight bytes of one expert
 void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
                   uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st);
-// decode batches (route1_ok): a2-a4 in one single-block launch (top-k, gates, counters, offsets, active
-// list, perm / inv), then the x gather
-bool route1_ok(int T, int E, int k);
-void launch_route1(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
-                   uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st);
-void launch_gather(int T, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp, cudaStream_t st);
+// decode batches (route_dec_ok): a1-a4 in ONE multi-CTA launch -- router logits (router mode, wr != NULL) or
+// the given logits (trace mode), top-k + gates, hotness counters, offsets, active list, stable perm / inv and
+// the gather of x rows into Xp -- with two grid-wide barriers between the phases
+bool route_dec_ok(int T, int E, int k);
+void launch_route_dec(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, const float* logits_in,
+                      int T, int E, int k, int H, int e_lo, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
+                      const int32_t* tier, const u64 (&bytes)[2][2], __nv_bfloat16* Xp, cudaStream_t st);
 // stable placement of every (t, j) entry; Xp != NULL also gathers x rows in permuted order
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
                   cudaStream_t st);
+// a8 combine; with fold != NULL one extra block also runs the layer's EMA fold + publication (a10, a14)
+struct FoldReq {
+    int layer;
+    u64 B_tot;
+};
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st,
-                    const int32_t* inv = nullptr);
+                    const int32_t* inv = nullptr, const Ctrl* ctrl = nullptr, const FoldReq* fold = nullptr);
 // expert parallelism: owner-side routing from received (local expert, gate) rows (k = 1), and the
 // source-side dispatch metadata / per-owner counts
 void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
                         const int32_t* tier, const u64 (&bytes)[2][2], int32_t* err, cudaStream_t st);
 void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, cudaStream_t st);
-void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int k, int e_lo,
+// E: global expert count (range check), e_cnt: local experts counted ([e_lo, e_lo + e_cnt))
+void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int e_cnt, int k, int e_lo,
                         uint32_t* cnt_acc, u64* mass_acc, int32_t* err, cudaStream_t st);
 
 // k_expert.cu

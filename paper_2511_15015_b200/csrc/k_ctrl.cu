@@ -42,28 +42,7 @@ __device__ __forceinline__ int32_t bscan_excl(int32_t v, int32_t* tmp, int32_t* 
 __global__ void __launch_bounds__(CTRL_THREADS) k_fold(Ctrl c, int layer, u64 B_tot, double oma) {
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
-    const int E = c.E;
-    const i64 t_new = c.t[layer] + 1;
-    __syncthreads();
-    const double denom = __dmul_rn((double)B_tot, 16777216.0);
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        const int i = layer * E + e;
-        const double gbar = B_tot ? __ddiv_rn((double)c.mass[i], denom) : 0.0;
-        c.S[i] = __dadd_rn(__dmul_rn(c.alpha, c.S[i]), __dmul_rn(oma, gbar));
-        c.cnt[i] = 0;
-        c.mass[i] = 0;
-        if (c.pend_dir[i] != 0 && c.pend_at[i] == t_new) {      // registration + reclaim
-            const int old = c.slot[i];
-            const int ob = layer * (E + c.s);
-            if (c.pend_dir[i] > 0) { c.lo_owner[ob + old] = -1; c.tier[i] = 1; }
-            else                   { c.hi_owner[ob + old] = -1; c.tier[i] = 0; }
-            c.slot[i] = c.pend_dst[i];
-            c.version[i] += 1;
-            c.pend_dir[i] = 0;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) c.t[layer] = t_new;
+    fold_layer(c, layer, B_tot, oma);
 }
 
 // ------------------------------------------------------------------ a11

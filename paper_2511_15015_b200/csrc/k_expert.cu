@@ -235,10 +235,9 @@ void launch_phase(const ExpertArgs& a, const __nv_bfloat16* x, const float* gate
                   int max_items, __nv_bfloat16* act, __nv_bfloat16* Y, cudaStream_t st) {
     const int K = PHASE == 0 ? a.H : a.I;
     const size_t sm = (size_t)NT * 8 * (K / 2 + 4) * 4 + (size_t)FFN_WARPS * 2 * NT * 32 * 4 * 4;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr_mask = 0;
+    if (dx_first_on_device(attr_mask)) {
         cudaFuncSetAttribute(k_ffn<PHASE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
     }
     if (max_items <= 0) return;
     dx_launch(k_ffn<PHASE, NT>, dim3(max_items), dim3(256), sm, st, g_dx_pdl, a, x, gate, (const int32_t*)ws.perm,

@@ -686,10 +686,9 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
 template <int PHASE, bool DEC>
 void launch_one(const GemmMaps& maps, const GemmArgs& a, int items, cudaStream_t st) {
     using C = Cfg<DEC>;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr_mask = 0;
+    if (dx_first_on_device(attr_mask)) {
         cudaFuncSetAttribute(k_gemm<PHASE, DEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        attr = true;
     }
     const int grid = items < DX_NUM_SMS ? items : DX_NUM_SMS;    // persistent: one CTA per SM
     dx_launch(k_gemm<PHASE, DEC>, dim3(grid), dim3(Roles<DEC>::THREADS), C::SMEM, st, g_dx_pdl, maps, a);

@@ -200,64 +200,129 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
     if (threadIdx.x == 0) *done = 0;
 }
 
-// ------------------------------------------------------------------ a2-a4 in ONE block (decode batches)
-// T*k <= ROUTE1_MAX_ENT: top-k + gates + counters (as k_route), then the offsets scan, the active list and
-// the stable placement (entry i's row = off[e] + #{i' < i : e_i' = e}) all in shared memory -- no
-// cross-block completion counter, no second launch for the ranks.
-#define ROUTE1_MAX_ENT 512
-#define ROUTE1_CHUNKS 16
+// ------------------------------------------------------------------ a1-a4 in ONE launch (decode batches)
+// T*k <= RDEC_MAX_ENT entries.  Grid of up to 128 CTAs x 512 threads, three phases separated by grid-wide
+// barriers (every CTA is resident: the grid is smaller than the SM count and the next kernel is released
+// with griddepcontrol.launch_dependents only after the last barrier):
+//   A (router mode) logits = x W_r^T + b, tiles of 16 tokens x 8 experts spread over the CTAs (mma.sync,
+//     exact bf16 products, fp32 sums in a fixed order: deterministic);
+//   B top-k + gates, one warp per token (R-G1, R-G2), written to idx/gate and to the per-entry exchange;
+//   C every CTA recomputes the per-chunk expert histograms of all entries (match_any, integer sums), the
+//     offsets scan and the chunk bases in shared memory (identical in every CTA), CTA 0 publishes off /
+//     active list / hotness counters, and each CTA places and gathers its share of the entries
+//     (perm / inv, Xp[pos] = x[t]) -- the stable order (t asc, j asc) of a4.
+#define RDEC_MAX_ENT 512
+#define RDEC_CHUNKS (RDEC_MAX_ENT / 32)
 template <typename Tv>
 __device__ Tv block_excl_scan(Tv v, Tv* tmp, Tv* total);
-#ifdef DX_ROUTE_PROF
-__device__ unsigned g_route1_calls = 0;
-#define R1P(i) do { if (threadIdx.x == 0) tp[i] = clock64(); } while (0)
-#else
-#define R1P(i) do {} while (0)
-#endif
-template <int NVT>
-__global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits, int T, int E, int k, int e_lo,
-                                                int e_cnt, int32_t* __restrict__ idx_out, float* __restrict__ gate_out,
-                                                uint32_t* __restrict__ cnt_acc, u64* __restrict__ mass_acc,
-                                                int32_t* __restrict__ off, int32_t* __restrict__ act_e,
-                                                int32_t* __restrict__ n_act, int32_t* __restrict__ perm,
-                                                int32_t* __restrict__ inv, RouteStats rs) {
-#ifdef DX_ROUTE_PROF
-    long long tp[8] = {0};
-#endif
-    R1P(0);
-    __shared__ int16_t ent_s[ROUTE1_MAX_ENT];                // expert of every entry (t*k + j)
-    __shared__ uint32_t gm_s[ROUTE1_MAX_ENT];                // rint(gate * 2^24) of every entry (R-H1)
-    __shared__ int32_t tmp[32];
-    __shared__ int32_t total_s, na_s;
-    extern __shared__ __align__(16) uint8_t dyn_s[];
-    float* lg_s = reinterpret_cast<float*>(dyn_s);                              // [T][E] logits of the batch
-    uint32_t* cmass = reinterpret_cast<uint32_t*>(lg_s + (size_t)T * E);        // [chunk][expert] mass
-    int16_t* chist = reinterpret_cast<int16_t*>(cmass + ROUTE1_CHUNKS * E);     // [chunk][expert] counts, bases
-    for (int i = threadIdx.x; i < ROUTE1_CHUNKS * E; i += blockDim.x) { chist[i] = 0; cmass[i] = 0; }
-    DX_GRID_WAIT();
-    DX_GRID_LAUNCH();
-    R1P(1);
-    {
-        const int n4 = T * E / 4;                            // E % 4 == 0 (route1_ok)
-        const float4* src = reinterpret_cast<const float4*>(logits);
-        float4* dst = reinterpret_cast<float4*>(lg_s);
-#pragma unroll 4
-        for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = src[i];
+
+// Grid-wide barrier over a {arrivals, generation} pair that resets itself (reusable across phases and
+// launches).  Release: __threadfence before arriving; acquire: fence after observing the new generation.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
     }
     __syncthreads();
-    R1P(2);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    // a2 + a3: one warp per token, k rounds of (value desc, id asc) warp arg-max, gates (R-G1, R-G2):
-    // lane j < k evaluates e_j = dx_expf(l_j - l_0) for its rank, lane 0 forms the sequential rank-order
-    // sum from shuffles (the same operations in the same order as one thread doing it all)
-    for (int t = warp; t < T; t += nwarps) {
+}
+
+struct RouteDecArgs {
+    const __nv_bfloat16* x;
+    const __nv_bfloat16* wr;      // router mode (else logits_in)
+    const float* bias;
+    const float* logits_in;
+    int T, E, k, H, e_lo, e_cnt;
+    RouteWs ws;
+    uint32_t* cnt_acc;
+    u64* mass_acc;
+    RouteStats rs;
+    __nv_bfloat16* Xp;
+};
+
+template <int NVT>
+__global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
+    extern __shared__ __align__(16) uint8_t dyn_s[];
+    __shared__ float red[16][16][9];                         // phase A: [warp][token][expert] partials
+    __shared__ int16_t ent_s[RDEC_MAX_ENT];
+    __shared__ int16_t rk_s[RDEC_MAX_ENT];
+    __shared__ uint32_t gm_s[RDEC_MAX_ENT];
+    __shared__ int32_t tmp[32];
+    __shared__ int32_t total_s, na_s, nhi_s;
+    uint32_t* cmass = reinterpret_cast<uint32_t*>(dyn_s);                       // [chunk][E]
+    int16_t* chist = reinterpret_cast<int16_t*>(cmass + RDEC_CHUNKS * a.E);      // [chunk][E] counts -> bases
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int T = a.T, E = a.E, k = a.k, H = a.H;
+    for (int i = threadIdx.x; i < RDEC_CHUNKS * E; i += blockDim.x) { chist[i] = 0; cmass[i] = 0; }
+    DX_GRID_WAIT();
+    const float* lgs = a.logits_in;
+    if (a.wr) {
+        // ---------------- A: router logits (the router stays full precision)
+        const int g = lane >> 2, q = lane & 3;
+        const int nunit = ((T + 15) / 16) * (E / 8);
+        const int nsteps = H / 16;
+        for (int u = blockIdx.x; u < nunit; u += gridDim.x) {
+            const int e0 = (u % (E / 8)) * 8, t0 = (u / (E / 8)) * 16;
+            const int ta = t0 + g, tb = t0 + g + 8, e = e0 + g;
+            const uint32_t* xa = reinterpret_cast<const uint32_t*>(a.x + (size_t)min(ta, T - 1) * H) + q;
+            const uint32_t* xb = reinterpret_cast<const uint32_t*>(a.x + (size_t)min(tb, T - 1) * H) + q;
+            const uint32_t* we = reinterpret_cast<const uint32_t*>(a.wr + (size_t)e * H) + q;
+            float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            constexpr int U = 8;
+            for (int s0 = warp; s0 < nsteps; s0 += 16 * U) {
+                uint32_t f[U][6];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    const int s = s0 + 16 * uu;
+                    if (s < nsteps) {
+                        const int kk = s * 8;
+                        f[uu][0] = __ldg(xa + kk); f[uu][1] = __ldg(xb + kk);
+                        f[uu][2] = __ldg(xa + kk + 4); f[uu][3] = __ldg(xb + kk + 4);
+                        f[uu][4] = __ldg(we + kk); f[uu][5] = __ldg(we + kk + 4);
+                    }
+                }
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu)
+                    if (s0 + 16 * uu < nsteps) mma16816(c, f[uu][0], f[uu][1], f[uu][2], f[uu][3], f[uu][4], f[uu][5]);
+            }
+            red[warp][g][2 * q] = c[0];
+            red[warp][g][2 * q + 1] = c[1];
+            red[warp][g + 8][2 * q] = c[2];
+            red[warp][g + 8][2 * q + 1] = c[3];
+            __syncthreads();
+            if (threadIdx.x < 128) {
+                const int tl = threadIdx.x >> 3, el = threadIdx.x & 7;
+                const int t = t0 + tl, ee = e0 + el;
+                if (t < T) {
+                    float v = red[0][tl][el];
+#pragma unroll
+                    for (int w = 1; w < 16; ++w) v += red[w][tl][el];
+                    a.ws.logits[(size_t)t * E + ee] = a.bias ? v + a.bias[ee] : v;
+                }
+            }
+            __syncthreads();
+        }
+        grid_sync(a.ws.gbar);
+        lgs = a.ws.logits;
+    }
+    // ---------------- B: top-k + gates, one warp per token (R-G1, R-G2)
+    for (int t = warp * gridDim.x + blockIdx.x; t < T; t += gridDim.x * 16) {    // spread over the SMs first
         float v[NVT];
         uint32_t taken = 0;
-        const float* lrow = lg_s + (size_t)t * E;
+        const float* lrow = lgs + (size_t)t * E;
 #pragma unroll
         for (int i = 0; i < NVT; ++i) {
             const int e = lane + 32 * i;
-            v[i] = e < E ? lrow[e] : -INFINITY;
+            v[i] = e < E ? __ldcg(lrow + e) : -INFINITY;
             if (e >= E) taken |= 1u << i;
         }
         float sel_v[ROUTE_MAX_K];
@@ -278,104 +343,96 @@ __global__ void __launch_bounds__(512) k_route1(const float* __restrict__ logits
             if (j < k) sum = __fadd_rn(sum, part[j]);
         if (lane < k) {
             const float gte = __fdiv_rn(my_ev, sum);
-            idx_out[(size_t)t * k + lane] = my_e;
-            gate_out[(size_t)t * k + lane] = gte;
-            ent_s[t * k + lane] = (int16_t)my_e;
-            gm_s[t * k + lane] = (uint32_t)rintf(__fmul_rn(gte, 16777216.0f));
+            a.ws.idx[(size_t)t * k + lane] = my_e;
+            a.ws.gate[(size_t)t * k + lane] = gte;
+            a.ws.ent[t * k + lane] = (int16_t)my_e;
+            a.ws.gm[t * k + lane] = (uint32_t)rintf(__fmul_rn(gte, 16777216.0f));
+        }
+    }
+    grid_sync(a.ws.gbar);
+    DX_GRID_LAUNCH();                       // every CTA is resident and past its last barrier
+    // ---------------- C: histograms, offsets, active list, counters (every CTA, identical results)
+    const int n = T * k;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        ent_s[i] = __ldcg(a.ws.ent + i);
+        gm_s[i] = __ldcg(a.ws.gm + i);
+    }
+    __syncthreads();
+    {
+        const int ci = warp, i = warp * 32 + lane;            // n <= 512 = 16 warps x 32 entries
+        const bool have = i < n;
+        const int ei = have ? ent_s[i] : -1 - lane;
+        const unsigned same = __match_any_sync(0xffffffffu, ei);
+        const int rk = __popc(same & ((1u << lane) - 1u));
+        const uint32_t gsum = __reduce_add_sync(same, have ? gm_s[i] : 0u);
+        if (have) rk_s[i] = (int16_t)rk;
+        if (have && rk == 0) {
+            chist[ci * E + ei] = (int16_t)__popc(same);
+            cmass[ci * E + ei] = gsum;
         }
     }
     __syncthreads();
-    R1P(3);
-    // per 32-entry chunk (one warp each): same-expert groups by match_any -> in-chunk rank, count, mass
-    const int n = T * k;
-    const int ci = warp, i = warp * 32 + lane;               // n <= 512 = 16 warps x 32 entries
-    const bool have = i < n;
-    const int ei = have ? ent_s[i] : -1 - lane;
-    const unsigned same = __match_any_sync(0xffffffffu, ei);
-    const int rk = __popc(same & ((1u << lane) - 1u));
-    const uint32_t gsum = __reduce_add_sync(same, have ? gm_s[i] : 0u);
-    if (have && rk == 0) {
-        chist[ci * E + ei] = (int16_t)__popc(same);
-        cmass[ci * E + ei] = gsum;
-    }
-    __syncthreads();
-    // per expert (thread e): totals in chunk order (integer sums: order-free), offsets scan, active list,
-    // hotness accumulators, chunk bases
-    const int e = threadIdx.x;
+    const int e = threadIdx.x;                                // E <= 512 = blockDim
     uint32_t c = 0;
     u64 m = 0;
     if (e < E) {
 #pragma unroll
-        for (int c2 = 0; c2 < ROUTE1_CHUNKS; ++c2) {
+        for (int c2 = 0; c2 < RDEC_CHUNKS; ++c2) {
             c += (uint32_t)chist[c2 * E + e];
             m += cmass[c2 * E + e];
         }
-        if (c) {
-            const int le = e - e_lo;
-            if (le >= 0 && le < e_cnt && cnt_acc) {
-                atomicAdd(&cnt_acc[le], c);
-                atomicAdd(&mass_acc[le], m);
+        if (c && blockIdx.x == 0) {
+            const int le = e - a.e_lo;
+            if (le >= 0 && le < a.e_cnt && a.cnt_acc) {
+                atomicAdd(&a.cnt_acc[le], c);
+                atomicAdd(&a.mass_acc[le], m);
             }
         }
     }
-    R1P(4);
     const int32_t o = block_excl_scan<int32_t>((int32_t)c, tmp, &total_s);
-    const int32_t a = block_excl_scan<int32_t>(c > 0 ? 1 : 0, tmp, &na_s);
+    const int32_t ac = block_excl_scan<int32_t>(c > 0 ? 1 : 0, tmp, &na_s);
     // active list HIGH tier first (the grouped GEMMs hand out work items in this order, heaviest first)
-    __shared__ int32_t nhi_s;
-    const int32_t hi = (e < E && c && rs.tier && rs.tier[e]) ? 1 : 0;
+    const int32_t hi = (e < E && c && a.rs.tier && a.rs.tier[e]) ? 1 : 0;
     const int32_t ah = block_excl_scan<int32_t>(hi, tmp, &nhi_s);
     if (e < E) {
-        off[e] = o;
-        if (c) act_e[hi ? ah : nhi_s + (a - ah)] = e;
+        if (blockIdx.x == 0) {
+            a.ws.off[e] = o;
+            if (c) a.ws.act_e[hi ? ah : nhi_s + (ac - ah)] = e;
+        }
         int run = o;
 #pragma unroll
-        for (int c2 = 0; c2 < ROUTE1_CHUNKS; ++c2) {
+        for (int c2 = 0; c2 < RDEC_CHUNKS; ++c2) {
             const int b = chist[c2 * E + e];
             chist[c2 * E + e] = (int16_t)run;
             run += b;
         }
     }
-    if (rs.stats && rs.tier) {                               // algorithmic weight bytes of this forward
-        if (threadIdx.x == 0) {                               // (profiling): 3 atomics per forward
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ws.off[E] = total_s;
+        *a.ws.n_act = na_s;
+        if (a.rs.stats && a.rs.tier) {                      // algorithmic weight bytes (profiling)
             const u64 nh = (u64)nhi_s, nl = (u64)na_s - nh;
-            atomicAdd(&rs.stats[0], nh * rs.b10 + nl * rs.b00);
-            atomicAdd(&rs.stats[1], nh * rs.b11 + nl * rs.b01);
-            atomicAdd(&rs.stats[2], (u64)na_s);
+            atomicAdd(&a.rs.stats[0], nh * a.rs.b10 + nl * a.rs.b00);
+            atomicAdd(&a.rs.stats[1], nh * a.rs.b11 + nl * a.rs.b01);
+            atomicAdd(&a.rs.stats[2], (u64)na_s);
         }
     }
-    if (threadIdx.x == 0) { off[E] = total_s; *n_act = na_s; }
     __syncthreads();
-    R1P(5);
-    // a4: stable placement (entry order t asc, j asc): pos = off[e] + earlier chunks + in-chunk rank
-    if (have) {
-        const int pos = chist[ci * E + ei] + rk;
-        perm[pos] = i;
-        inv[i] = pos;
+    // a4: stable placement (pos = off[e] + earlier chunks + in-chunk rank) and the x-row gather, one warp
+    // per entry, entries spread over all CTAs
+    for (int i = warp * gridDim.x + blockIdx.x; i < n; i += gridDim.x * 16) {
+        const int ei = ent_s[i];
+        const int pos = chist[(i >> 5) * E + ei] + rk_s[i];
+        if (lane == 0) {
+            a.ws.perm[pos] = i;
+            a.ws.inv[i] = pos;
+        }
+        if (a.Xp) {
+            const uint4* src = reinterpret_cast<const uint4*>(a.x + (size_t)(i / k) * H);
+            uint4* dst = reinterpret_cast<uint4*>(a.Xp + (size_t)pos * H);
+            for (int h = lane; h < H / 8; h += 32) dst[h] = __ldg(src + h);
+        }
     }
-#ifdef DX_ROUTE_PROF
-    R1P(6);
-    if (threadIdx.x == 0) {
-        const unsigned c = atomicAdd(&g_route1_calls, 1u);
-        if (c == 300)
-            printf("route1 T=%d clocks: wait %lld copy %lld topk %lld chunks %lld scans %lld place %lld total %lld\n", T,
-                   tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5], tp[6] - tp[0]);
-    }
-#endif
-}
-
-// x rows gathered into the permuted order (B operand of the gate/up GEMM): Xp[inv[i]] = x[i / k]; one
-// warp per entry, 16 B per lane per step
-__global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ inv, int n, int k, const __nv_bfloat16* __restrict__ x,
-                                                int H, __nv_bfloat16* __restrict__ Xp) {
-    DX_GRID_WAIT();
-    DX_GRID_LAUNCH();
-    const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (i >= n) return;
-    const int pos = inv[i];
-    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(i / k) * H);
-    uint4* dst = reinterpret_cast<uint4*>(Xp + (size_t)pos * H);
-    for (int h = lane; h < H / 8; h += 32) dst[h] = src[h];
 }
 
 // ------------------------------------------------------------------ a4: offsets + stable scatter
@@ -488,28 +545,45 @@ __global__ void __launch_bounds__(128) k_place(const int32_t* __restrict__ idx, 
 
 // ------------------------------------------------------------------ a8: y_t = bf16(sum_j Y[t,j])
 // inv == NULL: Y rows in entry order (t*k + j); else Y rows in permuted order, entry i at row inv[i]
-// (expert-parallel combine: the rows come back from their owners in dispatch order).
-__global__ void k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, __nv_bfloat16* __restrict__ y,
-                          const int32_t* __restrict__ inv) {
+// (expert-parallel combine: the rows come back from their owners in dispatch order).  Block = (token,
+// segment of 8*blockDim columns); every row load of a thread is issued before the rank-order fp32 sum.
+// fold_on: the LAST block instead runs the layer's EMA fold + publication (a10, a14), after the down GEMM
+// finished (griddepcontrol.wait), so the table flip never races the GEMMs that read the tables.
+__global__ void __launch_bounds__(128) k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, int nseg, int cthr,
+                                                 __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ inv,
+                                                 const Ctrl c, int fold_on, int fold_layer_id, u64 B_tot, double oma) {
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
-    const int t = blockIdx.x;
-    for (int h = threadIdx.x * 8; h < H; h += blockDim.x * 8) {
-        float acc[8];
+    if (fold_on && blockIdx.x == gridDim.x - 1) {
+        fold_layer(c, fold_layer_id, B_tot, oma);
+        return;
+    }
+    if ((int)threadIdx.x >= cthr) return;
+    const int t = blockIdx.x / nseg, seg = blockIdx.x % nseg;
+    const int h = (seg * cthr + threadIdx.x) * 8;
+    uint4 v[ROUTE_MAX_K];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-        for (int j = 0; j < k; ++j) {
+    for (int j = 0; j < ROUTE_MAX_K; ++j) {
+        if (j < k) {
             const size_t row = inv ? (size_t)inv[(size_t)t * k + j] : (size_t)t * k + j;
-            uint4 v = *reinterpret_cast<const uint4*>(Y + row * H + h);
-            const uint16_t* b = reinterpret_cast<const uint16_t*>(&v);
+            v[j] = __ldcg(reinterpret_cast<const uint4*>(Y + row * H + h));
+        }
+    }
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < ROUTE_MAX_K; ++j) {
+        if (j < k) {
+            const uint16_t* b = reinterpret_cast<const uint16_t*>(&v[j]);
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], dx_bf2f(b[i]));
         }
-        __align__(16) __nv_bfloat16 o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16_rn(acc[i]);
-        *reinterpret_cast<uint4*>(y + (size_t)t * H + h) = *reinterpret_cast<const uint4*>(o);
     }
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16_rn(acc[i]);
+    *reinterpret_cast<uint4*>(y + (size_t)t * H + h) = *reinterpret_cast<const uint4*>(o);
 }
 
 // ------------------------------------------------------------------ expert parallelism (a15)
@@ -535,6 +609,9 @@ __global__ void __launch_bounds__(256) k_route_given(const int2* __restrict__ me
         const float g = __int_as_float(m.y);
         if (m.x < 0 || m.x >= E) {
             atomicExch(err, 2);
+            idx_out[r] = 0;                                  // a valid placement with a zero gate
+            gate_out[r] = 0.0f;
+            atomicAdd(&cnt_s[0], 1u);
         } else {
             idx_out[r] = m.x;
             gate_out[r] = g;
@@ -620,34 +697,40 @@ void launch_route(const float* logits, int T, int E, int k, int e_lo, const Rout
 #undef DX_ROUTE_ARGS
 }
 
-bool route1_ok(int T, int E, int k) { return T * k <= ROUTE1_MAX_ENT && E <= 512 && E % 4 == 0 && T * E <= 32768; }
-
-void launch_route1(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
-                   uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st) {
-    if (T <= 0) return;
-    const int ec = cnt_acc ? E : 0;
-    RouteStats rs{tier, bytes[0][0], bytes[0][1], bytes[1][0], bytes[1][1], ws.stats};
-#define DX_R1_ARGS logits, T, E, k, e_lo, ec, ws.idx, ws.gate, cnt_acc, mass_acc, ws.off, ws.act_e, ws.n_act, \
-                   ws.perm, ws.inv, rs
-    static bool attr = false;
-    if (!attr) {
-        const int mx = 32768 * 4 + ROUTE1_CHUNKS * ROUTE_MAX_E * 6;
-        cudaFuncSetAttribute(k_route1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_route1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_route1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        attr = true;
-    }
-    const size_t sm = (size_t)T * E * 4 + (size_t)ROUTE1_CHUNKS * E * 6;
-    if (E <= 128)      dx_launch(k_route1<4>, dim3(1), dim3(512), sm, st, g_dx_pdl, DX_R1_ARGS);
-    else if (E <= 256) dx_launch(k_route1<8>, dim3(1), dim3(512), sm, st, g_dx_pdl, DX_R1_ARGS);
-    else               dx_launch(k_route1<16>, dim3(1), dim3(512), sm, st, g_dx_pdl, DX_R1_ARGS);
-#undef DX_R1_ARGS
+bool route_dec_ok(int T, int E, int k) {
+    return T >= 1 && T * k <= RDEC_MAX_ENT && E <= 512 && E % 32 == 0 && k <= ROUTE_MAX_K;
 }
 
-void launch_gather(int T, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp, cudaStream_t st) {
-    const int n = T * k;
-    if (n <= 0 || !Xp) return;
-    dx_launch(k_gather, dim3((n + 7) / 8), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.inv, n, k, x, H, Xp);
+template <int NVT>
+static void launch_rdec(const RouteDecArgs& a, int grid, size_t smem, cudaStream_t st) {
+    static unsigned long long attr_mask = 0;
+    if (dx_first_on_device(attr_mask))
+        cudaFuncSetAttribute(k_route_dec<NVT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             RDEC_CHUNKS * ROUTE_MAX_E * 6);
+    dx_launch(k_route_dec<NVT>, dim3(grid), dim3(512), smem, st, g_dx_pdl, a);
+}
+
+void launch_route_dec(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, const float* logits_in,
+                      int T, int E, int k, int H, int e_lo, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
+                      const int32_t* tier, const u64 (&bytes)[2][2], __nv_bfloat16* Xp, cudaStream_t st) {
+    if (T <= 0) return;
+    RouteDecArgs a;
+    a.x = x; a.wr = wr; a.bias = bias; a.logits_in = logits_in;
+    a.T = T; a.E = E; a.k = k; a.H = H; a.e_lo = e_lo; a.e_cnt = cnt_acc ? E : 0;
+    a.ws = ws; a.cnt_acc = cnt_acc; a.mass_acc = mass_acc;
+    a.rs = RouteStats{tier, bytes[0][0], bytes[0][1], bytes[1][0], bytes[1][1], ws.stats};
+    a.Xp = Xp;
+    // enough CTAs for the router tiles (16 tokens x 8 experts each) and for one warp per token / entry
+    const int units = wr ? ((T + 15) / 16) * (E / 8) : 0;
+    int grid = units;
+    const int need_warps = (T * k + 15) / 16;
+    if (grid < need_warps) grid = need_warps;
+    if (grid < 1) grid = 1;
+    if (grid > 128) grid = 128;
+    const size_t smem = (size_t)RDEC_CHUNKS * E * 6;
+    if (E <= 128)      launch_rdec<4>(a, grid, smem, st);
+    else if (E <= 256) launch_rdec<8>(a, grid, smem, st);
+    else               launch_rdec<16>(a, grid, smem, st);
 }
 
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
@@ -658,10 +741,18 @@ void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x
 }
 
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st,
-                    const int32_t* inv) {
-    if (T <= 0) return;
-    int threads = H / 8 < 256 ? H / 8 : 256;
-    dx_launch(k_combine, dim3(T), dim3(threads), 0, st, g_dx_pdl, Y, k, H, y, inv);
+                    const int32_t* inv, const Ctrl* ctrl, const FoldReq* fold) {
+    if (T <= 0 && !fold) return;
+    int nseg = 1;                               // segments of <= 128 threads x 8 columns that tile H exactly
+    while ((H / 8) / nseg > 128 || (H / 8) % nseg) ++nseg;
+    const int cthr = (H / 8) / nseg;
+    const int blocks = T * nseg + (fold ? 1 : 0);
+    Ctrl c{};
+    if (ctrl) c = *ctrl;
+    const int threads = fold ? (cthr > 128 ? cthr : 128) : cthr;
+    dx_launch(k_combine, dim3(blocks), dim3(threads), 0, st, g_dx_pdl, Y, k, H, nseg, cthr, y,
+              inv, c, fold ? 1 : 0, fold ? fold->layer : 0, fold ? fold->B_tot : (u64)0,
+              ctrl ? 1.0 - ctrl->alpha : 0.0);
 }
 
 void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
@@ -678,8 +769,8 @@ void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int3
               (const int32_t*)ws.idx, (const float*)ws.gate, (const int32_t*)ws.off, n, E_loc, G, meta, counts);
 }
 
-void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int k, int e_lo,
+void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int e_cnt, int k, int e_lo,
                         uint32_t* cnt_acc, u64* mass_acc, int32_t* err, cudaStream_t st) {
     if (T <= 0) return;
-    k_counts_from<<<(T + 127) / 128, 128, 0, st>>>(idx, gate, T, E, k, e_lo, E, cnt_acc, mass_acc, err);
+    k_counts_from<<<(T + 127) / 128, 128, 0, st>>>(idx, gate, T, E, k, e_lo, e_cnt, cnt_acc, mass_acc, err);
 }

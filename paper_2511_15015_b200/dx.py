@@ -82,6 +82,8 @@ _SIG = {
     "dx_pool_destroy": [_vp],
     "dx_pool_info": [_vp, _P(dx_info)],
     "dx_moe_forward": [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "dx_moe_step": [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "dx_get_logits": [_vp, _vp, _i64],
     "dx_hotness_update": [_vp, _i32],
     "dx_hotness_update_from": [_vp, _i32, _vp, _vp, _i32],
     "dx_plan_precision": [_vp, _i32, _P(dx_plan)],
@@ -200,6 +202,17 @@ class Pool:
                        topk_gate=None):
         _check(_lib.dx_moe_forward(self.h, layer, _ptr(x), T, _ptr(router_w), _ptr(router_bias), _ptr(logits),
                                    _ptr(y), _ptr(topk_idx), _ptr(topk_gate)), "dx_moe_forward")
+
+    def dx_moe_step(self, layer, x, T, y, router_w=None, router_bias=None, logits=None, topk_idx=None,
+                    topk_gate=None):
+        _check(_lib.dx_moe_step(self.h, layer, _ptr(x), T, _ptr(router_w), _ptr(router_bias), _ptr(logits),
+                                _ptr(y), _ptr(topk_idx), _ptr(topk_gate)), "dx_moe_step")
+
+    def dx_get_logits(self, T):
+        import numpy as np
+        out = np.zeros((T, self.cfg.num_experts), np.float32)
+        _check(_lib.dx_get_logits(self.h, _ptr(out), out.size), "dx_get_logits")
+        return out
 
     def dx_ep_dispatch(self, layer, x, T, send_rows, send_meta, send_counts, router_w=None, router_bias=None,
                        logits=None, topk_idx=None, topk_gate=None):

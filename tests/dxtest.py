@@ -72,3 +72,22 @@ def bf16_dev(a_u16: np.ndarray, dev="cuda"):
 
 def to_u16(t: torch.Tensor) -> np.ndarray:
     return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def elem_err(y, ref):
+    """SURVEY §8(c) O-5 per-element metric: max |y - ref| / (|ref| + 1e-2 * ||ref||_inf)."""
+    y = oracle.bits_to_f32(y).astype(np.float64)
+    ref = oracle.bits_to_f32(ref).astype(np.float64)
+    den = np.abs(ref) + 1e-2 * np.abs(ref).max()
+    return float((np.abs(y - ref) / np.where(den > 0, den, 1.0)).max())
+
+
+def dot_bound(x_u16, wr_u16, bias=None):
+    """Per-element scale sum_h |x_h w_eh| + |b_e| of a router logit: the fp32-summation error of an n-term
+    dot product of exact bf16 products is <= gamma_n times this (gamma_n ~ n * 2^-24)."""
+    x = np.abs(oracle.bits_to_f32(x_u16).astype(np.float64))
+    w = np.abs(oracle.bits_to_f32(wr_u16).astype(np.float64))
+    s = x @ w.T
+    if bias is not None:
+        s = s + np.abs(np.asarray(bias, np.float64))
+    return s

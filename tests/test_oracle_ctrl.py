@@ -224,3 +224,37 @@ def test_convergence_to_true_top_set():
         true = set(np.flatnonzero(rank_of < n_hot).tolist())
         js.append(len(hot & true) / len(hot | true))
     assert np.mean(js) >= 0.7, js
+
+
+def test_manual_command_semantics():
+    """or_ctrl_command (Alg. 1 EnqueueUpgrade/EnqueueDowngrade for a chosen expert) against
+    SPEC.md's op rules: range check, warm-up not finished, already at the tier, busy while in
+    flight, lowest-free destination, exhausted -> deferred with the pool unchanged
+    (SPEC.md:251), and publication L folds later with one alloc/free per transition."""
+    E, n_hot, s, L = 6, 2, 1, 2
+    c = oracle.Controller(E, n_hot, s, 0.9, 8, 4, 0, L)
+    assert c.command(0, 1) == 1                              # warm-up not finished
+    c.debug_set([0.9, 0.8, 0.1, 0.1, 0.1, 0.1], [1, 1, 0, 0, 0, 0], 0.5, 10)
+    st0 = c.state()
+    assert st0["cap_hi"] == n_hot + s and st0["cap_lo"] == E - n_hot + s
+    assert c.command(6, 1) == 2 and c.command(-1, -1) == 2 and c.command(2, 0) == 2
+    assert c.command(0, 1) == 1                              # already HIGH
+    assert c.command(2, -1) == 1                             # already LOW
+    assert c.command(2, 1) == 0                              # the one spare HIGH block
+    st = c.state()
+    assert st["in_flight"][2] == 1 and st["tier"][2] == 0   # not visible before publication
+    free_hi = [b for b in range(st0["cap_hi"]) if c.owner(True, b) in (-1, 2)]
+    assert c.owner(True, min(free_hi)) == 2                  # lowest free block
+    assert c.command(2, 1) == 5                              # busy
+    assert c.command(3, 1) == 4                              # exhausted: deferred, ledger unchanged
+    assert c.state()["used_hi"] == st["used_hi"] and c.state()["in_flight"][3] == 0
+    assert c.command(0, -1) == 0                             # demotion into the spare LOW block
+    for _ in range(L - 1):
+        c.fold(np.zeros(E, np.uint64), 1)
+        assert c.state()["tier"][2] == 0
+    c.fold(np.zeros(E, np.uint64), 1)                        # t + L: registration + reclaim
+    st = c.state()
+    assert st["tier"][2] == 1 and st["tier"][0] == 0 and st["in_flight"][2] == 0 and st["in_flight"][0] == 0
+    assert st["version"][2] == st0["version"][2] + 1 and st["version"][0] == st0["version"][0] + 1
+    assert st["used_hi"] == n_hot and st["used_lo"] == E - n_hot   # one alloc + one free per transition
+    assert c.command(3, 1) == 0                              # the block expert 0 released is free again

@@ -63,10 +63,57 @@ def test_k1_gate_is_exactly_one():
 
 
 def test_nonfinite_logits_rejected():
-    lg = np.zeros((2, 4), np.float32)
-    lg[1, 2] = np.nan
-    with pytest.raises(ValueError):
-        oracle.route(lg, 2)
+    for bad in (np.nan, np.inf):
+        lg = np.zeros((2, 4), np.float32)
+        lg[1, 2] = bad
+        with pytest.raises(ValueError):
+            oracle.route(lg, 2)
+    with pytest.raises(ValueError):                       # no finite logit in a token (R-G3)
+        oracle.route(np.full((1, 4), -np.inf, np.float32), 2)
+
+
+def test_masked_experts_neg_inf():
+    """R-G3: -inf = masked expert: ranked after every finite logit (ties among masked experts to the
+    lower id), gate exactly 0; the finite part of the selection is the plain top-k of the finite logits."""
+    lg = synth.trace_logits(4, 0, 0, 20, 16, 1.2)
+    lg[:, ::2] = -np.inf
+    idx, gate = oracle.route(lg, 4)
+    assert np.array_equal(idx, _brute_topk(np.where(np.isinf(lg), -1e30, lg), 4))
+    assert np.all(idx % 2 == 1)                           # 8 finite experts >= k: masked never chosen
+    one = np.full((3, 8), -np.inf, np.float32)
+    one[:, 5] = 0.25
+    idx, gate = oracle.route(one, 3)
+    assert idx.tolist() == [[5, 0, 1]] * 3                # then masked ones by ascending id
+    assert gate[:, 0].tolist() == [1.0] * 3 and np.all(gate[:, 1:] == 0.0)
+
+
+def test_signed_zero_logits_tie():
+    """-0 and +0 compare equal, so they tie and the lower id wins (R-G1)."""
+    lg = np.array([[-0.0, 0.0, -1.0, -0.0]], np.float32)
+    idx, gate = oracle.route(lg, 3)
+    assert idx.tolist() == [[0, 1, 3]]
+    assert np.all(gate == np.float32(1) / np.float32(3)) or np.allclose(gate, 1 / 3, rtol=1e-7)
+
+
+def test_router_logits_pins():
+    """or_router_logits (O-1 step 1, Eq. 1 router, full precision PAPER.md:281): (a) equals numpy's fp64
+    x @ W_r^T + b (a transposed or mis-strided W_r, a dropped bias or a wrong K range fails it on these
+    non-square shapes); (b) closed form: one-hot token rows pick out a column of W_r exactly."""
+    for (T, E, H) in [(7, 8, 64), (5, 128, 2048), (3, 512, 256)]:
+        x = synth.normal_bf16(2, T, E, H, (T, H))
+        wr = synth.router_bf16(2, 1, E, H)
+        b = synth.zipf_logp(synth.rank_perm(2, 1, 0, E, 4, 0.0), 1.2)
+        got = oracle.router_logits(x, wr, b)
+        ref = oracle.bits_to_f32(x).astype(np.float64) @ oracle.bits_to_f32(wr).astype(np.float64).T + b
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-12)
+        nob = oracle.router_logits(x, wr)
+        assert np.allclose(got - nob, np.broadcast_to(b.astype(np.float64), got.shape), atol=1e-12)
+    E, H = 16, 96
+    wr = synth.router_bf16(5, 0, E, H)
+    onehot = np.zeros((H, H), np.uint16)
+    onehot[np.arange(H), np.arange(H)] = 0x3F80            # bf16 1.0
+    got = oracle.router_logits(onehot, wr)
+    assert np.array_equal(got, oracle.bits_to_f32(wr).astype(np.float64).T)
 
 
 def test_route_matches_hf_qwen3_router():
