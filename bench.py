@@ -275,16 +275,14 @@ def run_ours(a, rank, world, local_rank):
     y_p = [y[i].data_ptr() for i in range(2)]
     wr_p = [wr[l].data_ptr() for l in range(L)]
     bias_p = [[bias[l, ep].data_ptr() for ep in range(n_epochs)] for l in range(L)]
-    fwd, hot, plan = pool.dx_moe_forward, pool.dx_hotness_update, pool.dx_plan_precision
+    mstep = pool.dx_moe_step           # forward + hotness update + plan, fold fused into the combine
 
     def step(x):
         s_ = step_counter[0]
         ep = s_ // c["drift"]
         xp = x if isinstance(x, int) else x.data_ptr()
         for l in range(L):
-            fwd(l, xp, B, y_p[l & 1], router_w=wr_p[l], router_bias=bias_p[l][ep])
-            hot(l)
-            plan(l)
+            mstep(l, xp, B, y_p[l & 1], router_w=wr_p[l], router_bias=bias_p[l][ep])
         step_counter[0] += 1
 
     # controller warm-up (t < W) and finalize at t = W, then the bench warm-up
@@ -454,9 +452,7 @@ def q80b_leg(a, peak, L=8):
         def qstep(x):
             ep = min(cnt[0] // 32, n_ep - 1)
             for l in range(L):
-                pool.dx_moe_forward(l, x, T, y, router_w=wr[l], router_bias=bias[l, ep])
-                pool.dx_hotness_update(l)
-                pool.dx_plan_precision(l)
+                pool.dx_moe_step(l, x, T, y, router_w=wr[l], router_bias=bias[l, ep])
             cnt[0] += 1
 
         if name == "decode":
@@ -511,9 +507,7 @@ def batch_sweep(a, pool, wr, bias, step_counter, L, H, dev, stream, peak):
         def bstep(x):
             ep = min(step_counter[0] // c["drift"], bias.shape[1] - 1)
             for l in range(L):
-                pool.dx_moe_forward(l, x, B, y, router_w=wr[l], router_bias=bias[l, ep])
-                pool.dx_hotness_update(l)
-                pool.dx_plan_precision(l)
+                pool.dx_moe_step(l, x, B, y, router_w=wr[l], router_bias=bias[l, ep])
             step_counter[0] += 1
 
         for i in range(2):
@@ -556,9 +550,7 @@ def prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream):
     def pstep(x):
         ep = step_counter[0] // c["drift"]
         for l in range(L):
-            pool.dx_moe_forward(l, x, T, y, router_w=wr[l], router_bias=bias[l, min(ep, bias.shape[1] - 1)])
-            pool.dx_hotness_update(l)
-            pool.dx_plan_precision(l)
+            pool.dx_moe_step(l, x, T, y, router_w=wr[l], router_bias=bias[l, min(ep, bias.shape[1] - 1)])
         step_counter[0] += 1
 
     for i in range(2):

@@ -229,7 +229,11 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (*gen == g) __nanosleep(20);
+            long long t0 = clock64();
+            while (*gen == g) {
+                __nanosleep(20);
+                if (clock64() - t0 > 4000000000ll) __trap();   // ~2 s: a protocol bug, fail the launch
+            }
         }
         __threadfence();
     }
