@@ -299,6 +299,38 @@ struct GemmArgs {
                                     // 5 skip the dequant transform, 6 both
 };
 bool gemm_decode_cfg(int T);
+
+// k_dec.cu (decode configuration, T <= 64): tensor maps live in device memory (one DecMaps per layer, one
+// DecBMaps per pool), 64-byte aligned.
+struct DecMaps {
+    CUtensorMap a16[2];             // [phase] bf16 HIGH weights: gate/up {K, rows, mat, slot} box {64, 64, 2, 1};
+                                    // down {K, rows, slot} box {64, 128, 1}; 128 B swizzle
+    CUtensorMap cq[2][2][3];        // [tier 0 LOW / 1 HIGH][phase][box width 128 / 64 / 32 B] raw codes,
+                                    // matching 128 / 64 / 32 B swizzle
+};
+struct DecBMaps {
+    CUtensorMap b[2][3][4];         // [phase: Xp / act][N rows 16 / 32 / 64][K chunks per box 1 / 2 / 4 / 8]
+};
+struct DecArgs {
+    const uint8_t* layer;
+    i64 hi_base;
+    SlotLayout hi, lo;
+    const int32_t* tier;
+    const int32_t* slot;
+    const int32_t* off;
+    const int32_t* act_e;
+    const int32_t* n_act;
+    const int32_t* perm;
+    const float* gate;
+    int H, I, g, k;
+    __nv_bfloat16* act;
+    __nv_bfloat16* Y;
+    int* sched;
+    int dbg;
+};
+void dec_trap_init();
+int dec_trap_report(char* buf, size_t n);
+void launch_dec(int phase, const DecMaps* lm, const DecBMaps* bm, const DecArgs& a, int max_items, cudaStream_t st);
 void gemm_trap_init();                            // host-mapped watchdog record (once per process)
 int gemm_trap_report(char* buf, size_t n);        // appends the record, if a k_gemm wait timed out
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
