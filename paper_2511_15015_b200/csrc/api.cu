@@ -88,9 +88,10 @@ struct dx_pool_s {
     std::vector<GemmMaps> gmaps;            // per layer (weights); xb filled per launch
     CUtensorMap xb0[4], xb1[4];             // B operand maps (Xp / act) for tiles of 16, 32, 64, 128 rows
     CUtensorMap xk0[3], xk1[3];             // 3-D B maps (Xp / act): several K chunks per box (decode int)
-    DecMaps* dec_maps = nullptr;            // device: per-layer maps of the decode kernels (k_dec.cu)
-    DecBMaps* dec_bmaps = nullptr;
-    bool dec_old = false;                   // DX_DEC_OLD=1: the round-1 decode configuration of k_gemm (A/B runs)
+    std::vector<DecMaps> dec_maps;          // host: per-layer maps of the decode kernels (k_dec.cu)
+    DecBMaps dec_bmaps;
+    bool use_kdec = false;                  // DX_DEC=1: the k_dec.cu decode kernels instead of k_gemm's decode
+                                            // configuration (A/B runs; measured slower on the int tiers)
 };
 
 // ---------------------------------------------------------------- TMA tensor maps (driver entry point)
@@ -177,7 +178,8 @@ static dx_status build_maps(dx_pool p) {
     }
     // decode kernels (k_dec.cu): per-layer A maps and the pool's B maps, copied to device memory
     {
-        std::vector<DecMaps> dm(p->L);
+        std::vector<DecMaps>& dm = p->dec_maps;
+        dm.assign(p->L, DecMaps{});
         memset(dm.data(), 0, dm.size() * sizeof(DecMaps));
         for (int l = 0; l < p->L; ++l) {
             DecMaps& d = dm[l];
@@ -205,7 +207,7 @@ static dx_status build_maps(dx_pool p) {
             }
             if (!ok) { dx_set_error("decode tensor map encoding failed (layer %d)", l); return DX_ERR_CUDA; }
         }
-        DecBMaps bmh;
+        DecBMaps& bmh = p->dec_bmaps;
         memset(&bmh, 0, sizeof(bmh));
         for (int ph = 0; ph < 2; ++ph) {
             const uint64_t K = ph == 0 ? (uint64_t)H : (uint64_t)I;
@@ -219,11 +221,6 @@ static dx_status build_maps(dx_pool p) {
                         return DX_ERR_CUDA;
                     }
                 }
-        }
-        if (cudaMemcpy(p->dec_maps, dm.data(), dm.size() * sizeof(DecMaps), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(p->dec_bmaps, &bmh, sizeof(bmh), cudaMemcpyHostToDevice) != cudaSuccess) {
-            dx_set_error("copying the decode tensor maps failed");
-            return DX_ERR_CUDA;
         }
     }
     for (int i = 0; i < 3; ++i) {                           // {rows, chunks}: {16, 4}, {32, 4}, {16, 8}
@@ -356,8 +353,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     if (G > 1)   // dispatch-side routing workspace (global experts, local tokens)
         ws_bytes += lg_rows * p->E * 4 + (size_t)T * k * 22 + 3 * 256 + (size_t)route_blocks(T) * p->E * 8 +
                     (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
-    const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048 +
-                               (size_t)L * sizeof(DecMaps) + sizeof(DecBMaps) + 512;
+    const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
     const size_t total = (size_t)L * p->layer_bytes + ctrl_bytes + ws_bytes + stage_bytes + ptr_bytes + 4096;
     cudaError_t ce = cudaMalloc(&p->arena, total);
@@ -437,8 +433,6 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     uint8_t* stage_master = carve<uint8_t>(q, (size_t)3 * p->I * p->H * 2);
     uint8_t* stage_high = carve<uint8_t>(q, (size_t)p->hi.bytes);
     p->hi_img_dev = carve<const uint8_t*>(q, (size_t)L * E);
-    p->dec_maps = carve<DecMaps>(q, (size_t)L);
-    p->dec_bmaps = carve<DecBMaps>(q, 1);
     if ((size_t)(q - p->arena) > total) {
         dx_set_error("internal: arena carve overflow");
         cudaFree(p->arena);
@@ -577,8 +571,8 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     gemm_trap_init();
     dec_trap_init();
     {
-        const char* e = getenv("DX_DEC_OLD");
-        p->dec_old = e && e[0] == '1';
+        const char* e = getenv("DX_DEC");
+        p->use_kdec = e && e[0] == '1';
     }
     st = build_maps(p);
     if (st != DX_OK) return fail(st);
@@ -782,7 +776,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         // tcgen05 grouped GEMMs (k_gemm.cu) over the rows placed in Xp: gate/up + SwiGLU, then down.
         // m_e <= T for top-k routing; the owner side (k = 1) sees m_e <= T rows as well.
         const bool dec = gemm_decode_cfg(T);
-        if (dec && !p->dec_old) {
+        if (dec && p->use_kdec) {
             // decode configuration: k_dec.cu (every weight tile read and dequantised once)
             DecArgs da;
             da.layer = a.arena_layer; da.hi_base = p->hi_base; da.hi = p->hi; da.lo = p->lo;
@@ -791,9 +785,9 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
             da.act = p->act; da.Y = p->Y; da.sched = p->gemm_sched;
             static const int dbg = [] { const char* s = getenv("DX_GEMM_DBG"); return s ? atoi(s) : 0; }();
             da.dbg = dbg;
-            launch_dec(0, p->dec_maps + layer, p->dec_bmaps, da, max_act * (p->I / 64), p->cs);
+            launch_dec(0, p->dec_maps[layer], p->dec_bmaps, da, max_act * (p->I / 64), p->cs);
             if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
-            launch_dec(1, p->dec_maps + layer, p->dec_bmaps, da, max_act * ((p->H + 127) / 128), p->cs);
+            launch_dec(1, p->dec_maps[layer], p->dec_bmaps, da, max_act * ((p->H + 127) / 128), p->cs);
         } else {
         GemmArgs ga;
         ga.layer = a.arena_layer; ga.hi_base = p->hi_base; ga.hi = p->hi; ga.lo = p->lo;

@@ -300,8 +300,10 @@ struct GemmArgs {
 };
 bool gemm_decode_cfg(int T);
 
-// k_dec.cu (decode configuration, T <= 64): tensor maps live in device memory (one DecMaps per layer, one
-// DecBMaps per pool), 64-byte aligned.
+// k_dec.cu (decode configuration, T <= 64): the host keeps one DecMaps per layer and one DecBMaps per pool
+// and passes one phase's maps by value (DecPhaseMaps, a __grid_constant__ kernel parameter).  Maps in
+// global memory would need a tensormap-proxy acquire on every use: the TMA unit caches descriptors by
+// address, and a later pool reusing the address would otherwise read another pool's stale maps.
 struct DecMaps {
     CUtensorMap a16[2];             // [phase] bf16 HIGH weights: gate/up {K, rows, mat, slot} box {64, 64, 2, 1};
                                     // down {K, rows, slot} box {64, 128, 1}; 128 B swizzle
@@ -330,7 +332,12 @@ struct DecArgs {
 };
 void dec_trap_init();
 int dec_trap_report(char* buf, size_t n);
-void launch_dec(int phase, const DecMaps* lm, const DecBMaps* bm, const DecArgs& a, int max_items, cudaStream_t st);
+struct DecPhaseMaps {
+    CUtensorMap a16;                // DecMaps::a16[phase]
+    CUtensorMap cq[2][3];           // DecMaps::cq[tier][phase][width]
+    CUtensorMap b[3][4];            // DecBMaps::b[phase]
+};
+void launch_dec(int phase, const DecMaps& lm, const DecBMaps& bm, const DecArgs& a, int max_items, cudaStream_t st);
 void gemm_trap_init();                            // host-mapped watchdog record (once per process)
 int gemm_trap_report(char* buf, size_t n);        // appends the record, if a k_gemm wait timed out
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);

@@ -12,10 +12,14 @@
 //    row with the matching TMA swizzle.  Four transform groups of four warps (thread = weight row = TMEM
 //    lane) dequantise the chunks round-robin, exactly as R-Q1 (bf16_rn((q - z) s)), into a ring of 12
 //    32-column TMEM A buffers; the MMAs take A from tensor memory (TS form).
-// Barriers: stage full (TMA), stage empty (one MMA commit: for int stages it follows the MMAs of every chunk,
-// which follow the transform's aready, so the codes are no longer read), aready / aempty per TMEM A buffer
-// (4 warp arrivals / 1 commit), accumulator full / empty.  The transform warps never touch bf16 items.  Every
-// wait is mbarrier.try_wait with a suspend-time hint (no polling loops taking issue slots from the dequant),
+// Barriers: stage full (bf16 TMA), stage empty (one MMA commit: for int stages it follows the MMAs of every
+// chunk, which follow the transform's aready, so the codes are no longer read), aready / aempty per TMEM A
+// buffer (4 warp arrivals / 1 commit), accumulator full / empty.  The transform warps never touch bf16 items,
+// so int stages land on their own barriers, numbered by int-stage sequence (qfull), and each is re-armed only
+// after all 16 transform warps have released its previous use (qdone): a warp that skipped a run of bf16
+// stages can never mistake an old phase for the one it waits for.  A warp issues a chunk's tcgen05.st and
+// signals it (aready) only after the next chunk's arithmetic, so the store latency overlaps work.  Every
+// wait re-polls mbarrier.try_wait (each probe blocks in hardware for a short, system-defined time),
 // bounded by a watchdog that traps with a readable diagnosis instead of hanging.
 // Warp roles (736 threads): 0 TMA producer, 1 TMEM owner + MMA issuer, 2-17 dequant, 18-21 epilogue,
 // 22 scheduler (dynamic work items through a global ticket counter; the routing kernel lists HIGH-tier
@@ -39,11 +43,16 @@ constexpr int NA = (512 - 2 * ACC_COLS) / 32;  // 12 TMEM A chunk buffers
 constexpr int W_EPI = 2 + NTW, W_SCHED = W_EPI + 4;
 constexpr int THREADS = 32 * (W_SCHED + 1);
 constexpr int N_CONSUMERS = W_SCHED;           // warps that read the item ring
-constexpr int RING = 2;
+#ifndef DX_DEC_RING
+#define DX_DEC_RING 2
+#endif
+constexpr int RING = DX_DEC_RING;              // work items published ahead of the slowest role (a CTA holding
+                                               // more unstarted items than that unbalances the launch's tail)
+constexpr int EMAX = 512;                      // active experts held in the shared item table
 constexpr int GTAB = 16;
 constexpr int TAB_BYTES = 128 * GTAB * 3;
 constexpr int XCH_BYTES = 64 * 32 * 4;
-constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2 * TAB_BYTES + 2048;
+constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + XCH_BYTES + 2 * TAB_BYTES + EMAX * 16 + 2048;
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
     uint16_t v;
@@ -83,20 +92,35 @@ __device__ __noinline__ void dec_trap(uint32_t tag, uint32_t parity) {
     }
     __trap();
 }
-__device__ __noinline__ void dwait_slow(uint32_t a, uint32_t parity, uint32_t tag) {
+// DX_DEC_BACKOFF=ns: roles other than the dequant warps sleep between polls (their polling loops otherwise
+// take issue slots and fma-pipe cycles -- IMAD moves -- from the dequant warps of their sub-partition)
+__device__ int g_dec_backoff_ns = 0;
+__device__ __noinline__ void dwait_slow(uint32_t a, uint32_t parity, uint32_t tag, int hint) {
     const uint64_t t0 = globaltimer_ns();
     const uint64_t lim = g_dec_watchdog_ns;
+    const int back = (tag == 6 || tag == 7 || tag == 8) ? 0 : g_dec_backoff_ns;
     for (;;) {
 #pragma unroll 1
-        for (int i = 0; i < 64; ++i)
-            if (mbar_try_wait_sleep(a, parity)) return;
+        for (int i = 0; i < 64; ++i) {
+            if (hint ? mbar_try_wait_sleep(a, parity) : mbar_try_wait(a, parity)) return;
+            if (back) __nanosleep(back);
+        }
         if (globaltimer_ns() - t0 > lim) dec_trap(tag, parity);
     }
 }
+// g_dec_wait_hint (DX_DEC_WAIT=1): waits suspend with a time hint instead of re-polling try_wait
+__device__ int g_dec_wait_hint = 0;
 __device__ __forceinline__ void dwait(uint64_t* bar, uint32_t parity, uint32_t tag) {
     const uint32_t a = smem_u32(bar);
-    if (mbar_try_wait_sleep(a, parity)) return;
-    dwait_slow(a, parity, tag);
+    if (mbar_try_wait(a, parity)) return;
+    dwait_slow(a, parity, tag, g_dec_wait_hint);
+}
+
+// ------------------------------------------------------------------ timeline trace (DX_GEMM_DBG=9, timing study)
+constexpr int TR_ITEMS = 32;
+__device__ unsigned long long g_dec_trace[2][148][TR_ITEMS][8];
+__device__ __forceinline__ void trace(int ph, int ii, int f, unsigned long long v) {
+    if (ii < TR_ITEMS && blockIdx.x < 148) g_dec_trace[ph][blockIdx.x][ii][f] = v;
 }
 
 // ------------------------------------------------------------------ work items
@@ -159,14 +183,14 @@ __device__ __forceinline__ uint32_t code_unit(uint32_t stage, int r, int c, int 
 }
 
 template <int PHASE>
-__global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ lm, const DecBMaps* __restrict__ bm,
-                                                    DecArgs a) {
+__global__ void __launch_bounds__(THREADS, 1) k_dec(const __grid_constant__ DecPhaseMaps mp, const DecArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sS = smem;                                                   // [STAGES][A | B]
     float* xch = reinterpret_cast<float*>(sS + STAGES * STAGE_BYTES);     // epilogue SwiGLU exchange
     uint8_t* tabs = reinterpret_cast<uint8_t*>(xch) + XCH_BYTES;          // [2][TAB_BYTES]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tabs + 2 * TAB_BYTES);
+    int4* etab = reinterpret_cast<int4*>(tabs + 2 * TAB_BYTES);          // [EMAX] {r0, m, slot, tier} per active expert
+    uint64_t* bars = reinterpret_cast<uint64_t*>(etab + EMAX);
     uint64_t* full = bars;                        // [STAGES]
     uint64_t* empty = full + STAGES;              // [STAGES]
     uint64_t* aready = empty + STAGES;            // [NA]
@@ -177,7 +201,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
     uint64_t* tabempty = tabfull + 2;             // [2]
     uint64_t* tkfull = tabempty + 2;              // [RING]
     uint64_t* tkempty = tkfull + RING;            // [RING]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tkempty + RING);
+    uint64_t* qfull = tkempty + RING;             // [STAGES] int stages land here (by int-stage sequence number)
+    uint64_t* qdone = qfull + STAGES;             // [STAGES] every transform warp has read that int stage
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qdone + STAGES);
     int32_t* ent_s = reinterpret_cast<int32_t*>(tmem_slot + 4);           // [64] epilogue: entry ids
     float* gate_s = reinterpret_cast<float*>(ent_s + 64);                 // [64] epilogue: gates
     Tick* ring = reinterpret_cast<Tick*>(gate_s + 64);                    // [RING]
@@ -197,17 +223,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
             mbar_init(&tabfull[b], 1); mbar_init(&tabempty[b], NTW);
         }
         for (int b = 0; b < RING; ++b) { mbar_init(&tkfull[b], 1); mbar_init(&tkempty[b], N_CONSUMERS); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&qfull[s], 1); mbar_init(&qdone[s], NTW); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 3; ++i) tma_prefetch(&bm->b[PHASE][i][0]);
-        tma_prefetch(&lm->a16[PHASE]);
+        for (int i = 0; i < 3; ++i) tma_prefetch(&mp.b[i][0]);
+        tma_prefetch(&mp.a16);
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
     const int n_act = a.n_act[0];
     const int n_items = n_act * nmb;
+    // the active experts' rows, slots and tiers, read once into shared memory so the scheduler decodes a ticket
+    // without a dependent chain of global loads per item
+    for (int i = threadIdx.x; i < n_act && i < EMAX; i += THREADS) {
+        const int e = a.act_e[i];
+        const int r0 = a.off[e];
+        etab[i] = make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -216,12 +250,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
-        int st = 0, tc = 0;
+        int st = 0, tc = 0, qs = 0;                  // ring position, int items, int stages issued
         uint32_t ph = 0;
         Item w;
         for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, nk, w); ++ii) {
-            const bool qt = w.bits != 16;
-            if (qt && tab_ok) {
+            const bool qt = w.bits != 16 && a.dbg != 12;    // dbg 12 (timing only): int stages flow like bf16 ones
+            if ((a.dbg == 9 || a.dbg == 12) && lane == 0) {
+                trace(PHASE, ii, 1, globaltimer_ns());
+                trace(PHASE, ii, 7, (unsigned long long)w.bits | ((unsigned long long)w.m << 8) | ((unsigned long long)w.nst << 16));
+            }
+            if (w.bits != 16 && tab_ok) {
                 const int tb = tc & 1;
                 dwait(&tabempty[tb], ((tc >> 1) & 1) ^ 1, 1);
                 ++tc;
@@ -250,25 +288,32 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
                 }
                 __syncwarp();
             }
-            const CUtensorMap* amap = qt ? &lm->cq[w.ti][PHASE][w.wi] : &lm->a16[PHASE];
-            const CUtensorMap* bmap = &bm->b[PHASE][w.rbi][w.ksi];
+            const CUtensorMap* amap = w.bits != 16 ? &mp.cq[w.ti][w.wi] : &mp.a16;
+            const CUtensorMap* bmap = &mp.b[w.rbi][w.ksi];
             const int arow = PHASE == 0 ? w.mb * 64 : w.mb * 128;
-            const int kunit = qt ? KCH * w.bits / 8 : KCH;       // A inner coordinate per chunk (bytes / elements)
-            const uint32_t abytes = qt ? 128u * (uint32_t)(w.ks * KCH * w.bits / 8) : (uint32_t)A_BYTES;
+            const int kunit = w.bits != 16 ? KCH * w.bits / 8 : KCH;       // A inner coordinate per chunk (bytes / elements)
+            const uint32_t abytes = w.bits != 16 ? 128u * (uint32_t)(w.ks * KCH * w.bits / 8) : (uint32_t)A_BYTES;
             const uint32_t bytes = abytes + (uint32_t)(w.ks * w.rb * 128);
             for (int s = 0; s < w.nst; ++s) {
                 const int kb0 = s * w.ks;
+                // an int stage lands on qfull[qs % STAGES]; that barrier is re-armed only after every transform
+                // warp has released its previous use (qdone), so no warp can see a stale phase
+                if (qt && qs >= STAGES) dwait(&qdone[qs % STAGES], (uint32_t)((qs / STAGES) - 1) & 1, 12);
                 dwait(&empty[st], ph ^ 1, 2);
                 if (elect_one()) {
                     uint8_t* sA = sS + st * STAGE_BYTES;
-                    mbar_arrive_expect_tx(&full[st], bytes);
-                    if (PHASE == 0) tma_load_4d(sA, amap, &full[st], kb0 * kunit, arow, 0, w.slot);
-                    else tma_load_3d(sA, amap, &full[st], kb0 * kunit, arow, w.slot);
-                    tma_load_3d(sA + A_BYTES, bmap, &full[st], 0, w.r0, kb0);
+                    uint64_t* fb = qt ? &qfull[qs % STAGES] : &full[st];
+                    mbar_arrive_expect_tx(fb, bytes);
+                    if (PHASE == 0) tma_load_4d(sA, amap, fb, kb0 * kunit, arow, 0, w.slot);
+                    else tma_load_3d(sA, amap, fb, kb0 * kunit, arow, w.slot);
+                    tma_load_3d(sA + A_BYTES, bmap, fb, 0, w.r0, kb0);
+                    if (qt) mbar_arrive(&full[st]);       // keeps full[]'s phase sequence for the MMA warp
                 }
                 __syncwarp();
+                if (qt) ++qs;
                 if (++st == STAGES) { st = 0; ph ^= 1; }
             }
+            if ((a.dbg == 9 || a.dbg == 12) && lane == 0) trace(PHASE, ii, 2, globaltimer_ns());
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (lane 0 issues; warp-uniform walk)
@@ -286,6 +331,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
                 const int kb0 = s * w.ks;
                 const int kc = min(w.ks, nk - kb0);
                 dwait(&full[st], ph, 4);
+                if ((a.dbg == 9 || a.dbg == 12) && s == 0 && lane == 0) trace(PHASE, ii, 3, globaltimer_ns());
                 tc_fence_after();
                 const uint32_t sA = smem_u32(sS + st * STAGE_BYTES), sB = sA + A_BYTES;
                 const uint64_t db = umma_desc_sw128(sB);
@@ -297,27 +343,32 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
                         mma_commit(&empty[st]);
                     }
                     __syncwarp();
+                } else if (a.dbg == 12) {
+                    if (elect_one()) mma_commit(&empty[st]);
+                    __syncwarp();
                 } else {
-                    for (int j = 0; j < kc; ++j, ++ch) {
-                        const int b = ch % NA;
-                        dwait(&aready[b], (uint32_t)(ch / NA) & 1, 5);
-                        tc_fence_after();
-                        const uint32_t at = tmem_a + 32 * b;
-                        const uint64_t bj = db + j * bstep;
-                        if (elect_one()) {
+                    // every chunk of the stage dequantised, then one issue region for all of its MMAs
+                    for (int j = 0; j < kc; ++j) dwait(&aready[(ch + j) % NA], (uint32_t)((ch + j) / NA) & 1, 5);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        for (int j = 0; j < kc; ++j) {
+                            const int b = (ch + j) % NA;
+                            const uint32_t at = tmem_a + 32 * b;
+                            const uint64_t bj = db + j * bstep;
                             if (a.dbg != 4 && a.dbg != 6) {
 #pragma unroll
                                 for (int q = 0; q < 4; ++q) mma_bf16_ts(d, at + 8 * q, bj + 2 * q, idesc, (kb0 | j | q) != 0);
                             }
                             mma_commit(&aempty[b]);
                         }
-                        __syncwarp();
+                        mma_commit(&empty[st]);
                     }
-                    if (elect_one()) mma_commit(&empty[st]);
                     __syncwarp();
+                    ch += kc;
                 }
                 if (++st == STAGES) { st = 0; ph ^= 1; }
             }
+            if ((a.dbg == 9 || a.dbg == 12) && lane == 0) trace(PHASE, ii, 4, globaltimer_ns());
             if (elect_one()) mma_commit(&tfull[buf]);
             __syncwarp();
         }
@@ -332,10 +383,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
         const int gsh = 31 - __clz(a.g);
         uint32_t magic = 0x43004300u;
         asm volatile("" : "+r"(magic));
-        int nsd = 0, ch = 0, tc = 0;                   // stages done, int chunks done (shared numbering with MMA)
+        int nsd = 0, qs = 0, ch = 0, tc = 0;          // ring position, int stages, int chunks (MMA numbering)
+        int pend = -1;                                 // TMEM buffer whose tcgen05.st is in flight, aready not yet signalled
+        auto flush = [&]() {
+            if (pend >= 0) {
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aready[pend]);
+                pend = -1;
+            }
+        };
         Item w;
         for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, nk, w); ++ii) {
             if (w.bits == 16) { nsd += w.nst; continue; }    // bf16 items need no transform
+            if (a.dbg == 12) {
+                if (tab_ok) {
+                    dwait(&tabfull[tc & 1], (tc >> 1) & 1, 6);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tabempty[tc & 1]);
+                    ++tc;
+                }
+                continue;
+            }
             const int mrow = PHASE == 0 ? w.mb * 64 + (r & 63) : w.mb * 128 + r;
             const bool valid = mrow < mat_rows;
             const SlotLayout& L = w.ti ? a.hi : a.lo;
@@ -355,59 +425,64 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
                               : (uint32_t)gscales[gi] | ((0x4300u + gzeros[gi]) << 16);
             };
             const bool four = w.bits == 4;
-            for (int s = 0; s < w.nst; ++s, ++nsd) {
+            for (int s = 0; s < w.nst; ++s, ++nsd, ++qs) {
                 const int kb0 = s * w.ks;
                 const int kc = min(w.ks, nk - kb0);
+                const int sq = qs % STAGES;
+                dwait(&qfull[sq], (uint32_t)(qs / STAGES) & 1, 7);   // every warp observes every int stage
+                const uint32_t stage = stages_u32 + (nsd % STAGES) * STAGE_BYTES;
                 // my chunks in this stage: ch + j with (ch + j) % NG == grp
-                const int j0 = (grp - ch % NG + NG) % NG;
-                if (j0 < kc) {
-                    const int st = nsd % STAGES;
-                    dwait(&full[st], (uint32_t)(nsd / STAGES) & 1, 7);
-                    const uint32_t stage = stages_u32 + st * STAGE_BYTES;
-                    for (int j = j0; j < kc; j += NG) {
-                        const int cj = ch + j, b = cj % NA;
-                        dwait(&aempty[b], ((uint32_t)(cj / NA) & 1) ^ 1, 8);
-                        if (a.dbg != 5 && a.dbg != 6) {
-                            const int k0 = (kb0 + j) * KCH;
-                            const uint32_t v0 = group_sz(k0 >> gsh);
-                            const uint32_t v1 = a.g >= 64 ? v0 : group_sz((k0 + 32) >> gsh);
-                            const uint32_t zz0 = (v0 >> 16) * 0x10001u, ss0 = (v0 & 0xFFFFu) * 0x10001u;
-                            const uint32_t zz1 = (v1 >> 16) * 0x10001u, ss1 = (v1 & 0xFFFFu) * 0x10001u;
-                            uint32_t wv[32];
-                            if (four) {
-                                uint32_t c[8];
-                                lds128(code_unit(stage, r, 2 * j, w.wi), c[0], c[1], c[2], c[3]);
-                                lds128(code_unit(stage, r, 2 * j + 1, w.wi), c[4], c[5], c[6], c[7]);
+                for (int j = (grp - ch % NG + NG) % NG; j < kc; j += NG) {
+                    const int cj = ch + j, b = cj % NA;
+                    uint32_t wv[32];
+                    if (a.dbg != 5 && a.dbg != 6) {
+                        const int k0 = (kb0 + j) * KCH;
+                        const uint32_t v0 = group_sz(k0 >> gsh);
+                        const uint32_t v1 = a.g >= 64 ? v0 : group_sz((k0 + 32) >> gsh);
+                        const uint32_t zz0 = (v0 >> 16) * 0x10001u, ss0 = (v0 & 0xFFFFu) * 0x10001u;
+                        const uint32_t zz1 = (v1 >> 16) * 0x10001u, ss1 = (v1 & 0xFFFFu) * 0x10001u;
+                        if (four) {
+                            uint32_t c[8];
+                            lds128(code_unit(stage, r, 2 * j, w.wi), c[0], c[1], c[2], c[3]);
+                            lds128(code_unit(stage, r, 2 * j + 1, w.wi), c[4], c[5], c[6], c[7]);
 #pragma unroll
-                                for (int u = 0; u < 8; ++u) {
-                                    const uint32_t zz = u < 4 ? zz0 : zz1, ss = u < 4 ? ss0 : ss1;
-                                    wv[4 * u + 0] = deq2(and_or(c[u], 0x000F000Fu, magic), zz, ss);
-                                    wv[4 * u + 1] = deq2(and_or(c[u] >> 4, 0x000F000Fu, magic), zz, ss);
-                                    wv[4 * u + 2] = deq2(and_or(c[u] >> 8, 0x000F000Fu, magic), zz, ss);
-                                    wv[4 * u + 3] = deq2(and_or(c[u] >> 12, 0x000F000Fu, magic), zz, ss);
-                                }
-                            } else {
-                                uint32_t c[4];
-                                lds128(code_unit(stage, r, j, w.wi), c[0], c[1], c[2], c[3]);
-#pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    const uint32_t zz = u < 2 ? zz0 : zz1, ss = u < 2 ? ss0 : ss1;
-#pragma unroll
-                                    for (int p = 0; p < 8; ++p)
-                                        wv[8 * u + p] = deq2(and_or(c[u] >> (2 * p), 0x00030003u, magic), zz, ss);
-                                }
+                            for (int u = 0; u < 8; ++u) {
+                                const uint32_t zz = u < 4 ? zz0 : zz1, ss = u < 4 ? ss0 : ss1;
+                                wv[4 * u + 0] = deq2(and_or(c[u], 0x000F000Fu, magic), zz, ss);
+                                wv[4 * u + 1] = deq2(and_or(c[u] >> 4, 0x000F000Fu, magic), zz, ss);
+                                wv[4 * u + 2] = deq2(and_or(c[u] >> 8, 0x000F000Fu, magic), zz, ss);
+                                wv[4 * u + 3] = deq2(and_or(c[u] >> 12, 0x000F000Fu, magic), zz, ss);
                             }
-                            tc_fence_after();
-                            tmem_st32(lane_base + 32 * b, wv);
-                            tmem_st_wait();
+                        } else {
+                            uint32_t c[4];
+                            lds128(code_unit(stage, r, j, w.wi), c[0], c[1], c[2], c[3]);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t zz = u < 2 ? zz0 : zz1, ss = u < 2 ? ss0 : ss1;
+#pragma unroll
+                                for (int p = 0; p < 8; ++p)
+                                    wv[8 * u + p] = deq2(and_or(c[u] >> (2 * p), 0x00030003u, magic), zz, ss);
+                            }
                         }
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&aready[b]);
                     }
+                    dwait(&aempty[b], ((uint32_t)(cj / NA) & 1) ^ 1, 8);   // TMEM buffer b drained by its MMAs
+                    flush();                                                // the previous chunk's store -> aready
+                    if (a.dbg != 5 && a.dbg != 6 && a.dbg != 11) {
+                        tc_fence_after();
+                        tmem_st32(lane_base + 32 * b, wv);
+                    } else if (a.dbg == 11) {                   // timing only: the math without the TMEM store
+                        uint32_t acc = 0;
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) acc ^= wv[u];
+                        if (acc == 0x9E3779B9u) a.act[0] = __float2bfloat16_rn(0.f);
+                    }
+                    pend = b;
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&qdone[sq]);     // this warp's reads of the stage's codes are done
                 ch += kc;
             }
+            flush();                                         // nothing outstanding across an item boundary
             if (tab_ok) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tabempty[tb]);
@@ -423,11 +498,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
             int item = 0;
             if (lane == 0) {
                 item = atomicAdd(ctr, 1);
+                if (a.dbg == 9 || a.dbg == 12) trace(PHASE, ii, 0, globaltimer_ns());
                 int4 v = make_int4(0, 0, 0, 0);
                 if (item < n_items) {
-                    const int e = a.act_e[item / nmb];
-                    const int r0 = a.off[e];
-                    v = make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+                    const int i = item / nmb;
+                    if (i < EMAX) {
+                        v = etab[i];
+                    } else {
+                        const int e = a.act_e[i];
+                        const int r0 = a.off[e];
+                        v = make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+                    }
                 }
                 ring[sl].v = v;
                 ring[sl].item = item;
@@ -453,6 +534,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
                 }
             }
             dwait(&tfull[buf], (cc >> 1) & 1, 9);
+            if ((a.dbg == 9 || a.dbg == 12) && et == 0) trace(PHASE, ii, 5, globaltimer_ns());
             tc_fence_after();
             named_bar(1, 128);
             for (int col = 0; col < (a.dbg == 8 ? 0 : nvalid); col += 32) {
@@ -500,6 +582,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
+            if ((a.dbg == 9 || a.dbg == 12) && et == 0) trace(PHASE, ii, 6, globaltimer_ns());
             named_bar(1, 128);                      // ent_s / gate_s / xch reused by the next item
         }
     }
@@ -519,15 +602,31 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const DecMaps* __restrict__ 
 }
 
 template <int PHASE>
-void launch_dec_one(const DecMaps* lm, const DecBMaps* bm, const DecArgs& a, int items, cudaStream_t st) {
+void launch_dec_one(const DecMaps& lm, const DecBMaps& bm, const DecArgs& a, int items, cudaStream_t st) {
     static unsigned long long attr_mask = 0;
     if (dx_first_on_device(attr_mask))
         cudaFuncSetAttribute(k_dec<PHASE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     const int grid = items < DX_NUM_SMS ? items : DX_NUM_SMS;
-    dx_launch(k_dec<PHASE>, dim3(grid), dim3(THREADS), SMEM, st, g_dx_pdl, lm, bm, a);
+    DecPhaseMaps mp;
+    mp.a16 = lm.a16[PHASE];
+    for (int t = 0; t < 2; ++t)
+        for (int w = 0; w < 3; ++w) mp.cq[t][w] = lm.cq[t][PHASE][w];
+    memcpy(mp.b, bm.b[PHASE], sizeof(mp.b));
+    dx_launch(k_dec<PHASE>, dim3(grid), dim3(THREADS), SMEM, st, g_dx_pdl, mp, a);
 }
 
 }  // namespace
+
+extern "C" int64_t dx_debug_dec_trace(void* host, int64_t bytes) {   // DX_GEMM_DBG=9 timeline (timing study)
+    const int64_t n = (int64_t)sizeof(g_dec_trace);
+    if (!host && bytes < 0) {                          // clear
+        static unsigned long long zero[sizeof(g_dec_trace) / 8];
+        return cudaMemcpyToSymbol(g_dec_trace, zero, n) == cudaSuccess ? 0 : -1;
+    }
+    if (!host) return n;
+    if (bytes < n || cudaMemcpyFromSymbol(host, g_dec_trace, n) != cudaSuccess) return -1;
+    return n;
+}
 
 static uint32_t* g_dec_trap_host = nullptr;
 void dec_trap_init() {
@@ -544,18 +643,27 @@ void dec_trap_init() {
         const uint64_t ns = (uint64_t)(atof(w) * 1e9);
         if (ns > 0) cudaMemcpyToSymbol(g_dec_watchdog_ns, &ns, sizeof(ns));
     }
+    if (const char* w = getenv("DX_DEC_BACKOFF")) {
+        const int h = atoi(w);
+        cudaMemcpyToSymbol(g_dec_backoff_ns, &h, sizeof(h));
+    }
+    if (const char* w = getenv("DX_DEC_WAIT")) {
+        const int h = atoi(w);
+        cudaMemcpyToSymbol(g_dec_wait_hint, &h, sizeof(h));
+    }
 }
 static const char* const k_dec_trap_names[] = {"?", "tabempty (producer)", "empty (producer)", "tempty (MMA)", "full (MMA)",
-                                               "aready (MMA)", "tabfull (dequant)", "full (dequant)", "aempty (dequant)",
-                                               "tfull (epilogue)", "tkfull (item ring)", "tkempty (scheduler)"};
+                                               "aready (MMA)", "tabfull (dequant)", "qfull (dequant)", "aempty (dequant)",
+                                               "tfull (epilogue)", "tkfull (item ring)", "tkempty (scheduler)",
+                                               "qdone (producer)"};
 int dec_trap_report(char* buf, size_t n) {
     if (!g_dec_trap_host || (g_dec_trap_host[0] >> 16) != 0xDEADu) return 0;
     const uint32_t tag = g_dec_trap_host[0] & 0xFFFFu;
     return snprintf(buf, n, " [k_dec watchdog: wait on %s, parity %u, block %u, thread %u]",
-                    tag < 12 ? k_dec_trap_names[tag] : "?", g_dec_trap_host[1], g_dec_trap_host[2], g_dec_trap_host[3]);
+                    tag < 13 ? k_dec_trap_names[tag] : "?", g_dec_trap_host[1], g_dec_trap_host[2], g_dec_trap_host[3]);
 }
 
-void launch_dec(int phase, const DecMaps* lm, const DecBMaps* bm, const DecArgs& a, int max_items, cudaStream_t st) {
+void launch_dec(int phase, const DecMaps& lm, const DecBMaps& bm, const DecArgs& a, int max_items, cudaStream_t st) {
     if (max_items <= 0) return;
     if (phase == 0) launch_dec_one<0>(lm, bm, a, max_items, st);
     else launch_dec_one<1>(lm, bm, a, max_items, st);

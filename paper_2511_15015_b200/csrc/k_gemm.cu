@@ -54,6 +54,8 @@ constexpr int B_REGION = 16384;               // B region per stage
 constexpr int STAGE_BYTES = A_BYTES + B_REGION;
 constexpr int XCH_BYTES = 64 * 32 * 4;        // epilogue SwiGLU exchange: 64 rows x 32 columns fp32
 constexpr int TPRE_BYTES = (512 + 1) * 4 + 12;   // prefill: per-active-expert N-tile prefix
+constexpr int EMAX = 512;
+constexpr int ETAB_BYTES = EMAX * 16;            // decode: {r0, m, slot, tier} per active expert
 #ifndef DX_GEMM_RING
 #define DX_GEMM_RING 2
 #endif
@@ -69,7 +71,7 @@ struct Cfg {
     static constexpr int ACH = DEC ? 4 : 1;                    // K chunks per TMEM A buffer (32 columns each)
     static constexpr int NA = (512 - 2 * NBMAX) / (32 * ACH);  // TMEM A buffers: 3 (decode) / 8 (prefill)
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + Roles<DEC>::EPI_TEAMS * XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES +
-                                TPRE_BYTES;
+                                (DEC ? ETAB_BYTES : TPRE_BYTES);
     __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : 128; }
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
@@ -194,7 +196,8 @@ __device__ __forceinline__ int4 decode_tiled(const GemmArgs& a, const int32_t* t
     const int m = min(NT, a.off[e + 1] - r0);
     return make_int4(r0, m, a.slot[e], a.tier[e]);
 }
-__device__ __forceinline__ int4 decode_raw(const GemmArgs& a, int item, int nmb) {   // {r0, m, slot, ti}
+__device__ __forceinline__ int4 decode_raw(const GemmArgs& a, const int4* etab, int item, int nmb) {   // {r0, m, slot, ti}
+    if (item / nmb < EMAX) return etab[item / nmb];
     const int e = a.act_e[item / nmb];
     const int r0 = a.off[e];
     return make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
@@ -261,6 +264,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
     Tick* ring = reinterpret_cast<Tick*>(reinterpret_cast<uint8_t*>(bars) + 2048);   // [RING] items
     uint8_t* tabs = reinterpret_cast<uint8_t*>(ring + RING);         // [2][TAB_BYTES]
     int32_t* tpre = reinterpret_cast<int32_t*>(tabs + 2 * TAB_BYTES); // [n_act + 1] prefill N-tile prefix
+    int4* etab = reinterpret_cast<int4*>(tabs + 2 * TAB_BYTES);       // decode: [EMAX] the active experts' items
 
     const int K = PHASE == 0 ? a.H : a.I;
     const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
@@ -310,6 +314,14 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         if (t <= n_act) tpre[t] = base + x - v;
         __syncthreads();
         n_items = tpre[n_act] * nmb;
+    } else {
+        // the active experts' rows, slots and tiers, read once into shared memory: the scheduler then
+        // decodes a ticket without a dependent chain of global loads per work item
+        for (int i = threadIdx.x; i < n_act && i < EMAX; i += Roles<DEC>::THREADS) {
+            const int e = a.act_e[i];
+            const int r0 = a.off[e];
+            etab[i] = make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -580,7 +592,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
             if (lane == 0) {
                 item = atomicAdd(ctr, 1);
                 ring[sl].v = item >= n_items ? make_int4(0, 0, 0, 0)
-                           : DEC ? decode_raw(a, item, nmb) : decode_tiled(a, tpre, n_act, item, nmb, C::NBMAX);
+                           : DEC ? decode_raw(a, etab, item, nmb) : decode_tiled(a, tpre, n_act, item, nmb, C::NBMAX);
                 ring[sl].item = item;
                 mbar_arrive(&tkfull[sl]);
             }

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdx.so")
+LIB_PATH = os.path.join(HERE, os.environ.get("DX_LIB", "libdx.so"))   # DX_LIB: an in-tree build variant (A/B runs)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
