@@ -6,8 +6,10 @@ promotions/demotions with their publication (DESIGN.md §1 rows a1-a14).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  N > 1 (torchrun): each rank serves its own batch on a full
-replica of the stack (weak scaling, no data-path collective); value = all ranks' tokens / max time.
+Prints ONE JSON line (rank 0).  N > 1 (torchrun): expert parallelism (north_star) -- rank r
+owns experts [r*E/N, (r+1)*E/N) of every layer with a per-GPU budget of 24e9/N B, serves its own batch of
+B tokens (weak scaling: global batch N*B) and the library exchanges rows over NCCL inside dx_moe_step
+(dx_pool_create_ep); value = all ranks' tokens / max time.  --replicas runs N independent full replicas.
 """
 from __future__ import annotations
 
@@ -52,6 +54,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-batch-sweep", action="store_true")
     ap.add_argument("--no-q80b", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent full replicas instead of EP")
+    ap.add_argument("--ep-loopback", action="store_true",
+                    help="N = 1: run the expert-parallel path on a one-rank NCCL communicator (tests the EP leg)")
     ap.add_argument("--switch-stress", action="store_true",
                     help="C5 (SURVEY 8(d)): one Q30B layer, n_hot swept 10%%..100%%, drift 0.5 every period; "
                          "prints the C5 JSON line instead of the main one")
@@ -167,12 +172,23 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------- ours
-def host_masters(seed, L, E, H, I, rank, world):
+def host_masters(seed, L, E, H, I, rank, world, experts=None):
     """bf16 masters of the whole stack in page-locked host memory (the paper's DRAM cache,
-    PAPER.md:236).  Multi-rank runs share one /dev/shm copy."""
+    PAPER.md:236).  Multi-rank replica runs share one /dev/shm copy; `experts` = (lo, n): only the global
+    experts [lo, lo + n) of every layer (an expert-parallel rank's slice), pointers [L][n]."""
     import torch
     import synth
     n = 3 * I * H
+    if experts is not None:
+        lo, ne = experts
+        arr = np.empty(L * ne * n, dtype=np.uint16)
+        for l in range(L):
+            for e in range(ne):
+                synth.expert_master_into(seed, l, lo + e, H, I, arr[(l * ne + e) * n:(l * ne + e + 1) * n])
+        rc = torch.cuda.cudart().cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+        if int(rc) != 0:
+            raise RuntimeError(f"cudaHostRegister failed: {rc}")
+        return arr, [arr.ctypes.data + i * n * 2 for i in range(L * ne)]
     total = L * E * n
     shm_ok = False
     if world > 1:
@@ -235,20 +251,34 @@ def run_ours(a, rank, world, local_rank):
     c = dict(C2)
     L, E, k, H, I, g, B = a.layers, c["E"], c["k"], c["H"], c["I"], c["g"], a.batch
     seed = a.seed
+    ep_mode = (world > 1 and not a.replicas) or a.ep_loopback
+    G = world if ep_mode else 1
+    E_loc = E // G
+    if ep_mode:       # the batch-sweep / prefill legs are single-GPU studies
+        a.no_batch_sweep, a.prefill_tokens = True, 0
     t0 = time.time()
-    arr, ptrs = host_masters(seed, L, E, H, I, rank, world)
+    arr, ptrs = host_masters(seed, L, E, H, I, rank, world, experts=(rank * E_loc, E_loc) if ep_mode else None)
     t_gen = time.time() - t0
     cfg = dx.dx_config()
     cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = L, E, k, H, I, g
     cfg.high_bits, cfg.low_bits = c["high"], c["low"]
     budget = int(a.budget_gb * 1e9) if a.budget_gb > 0 else c["budget"]
-    cfg.expert_budget_bytes = budget * L // C2["L"]
+    cfg.expert_budget_bytes = budget * L // C2["L"] // G         # per GPU: the north_star's artificial budget
     cfg.n_spare, cfg.ema_alpha = c["s"], c["alpha"]
     cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = c["Tp"], c["W"], c["dwell"], c["lag"]
-    cfg.max_tokens, cfg.ep_rank, cfg.ep_size = max(B, 64, a.prefill_tokens), 0, 1
+    cfg.max_tokens, cfg.ep_rank, cfg.ep_size = max(B, 64, a.prefill_tokens), rank if ep_mode else 0, G
     stream = torch.cuda.current_stream()
+    nccl_id = None
+    if ep_mode:       # the library's own NCCL communicator; its id travels over torch.distributed
+        import torch.distributed as dist
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(dx.dx_get_unique_id()), dtype=torch.uint8))
+        if world > 1:
+            dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().tolist())
     t0 = time.time()
-    pool = dx.Pool(cfg, ptrs, stream)
+    pool = dx.Pool(cfg, ptrs, stream, nccl_id=nccl_id)
     t_pool = time.time() - t0
     n_hot = pool.info.n_hot
     if a.ffn_path:
@@ -367,10 +397,12 @@ def run_ours(a, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded splitmix64 weights, "
         "Zipf(1.2) router bias with drift; see DESIGN.md input recipe)",
         "config": {"workload": f"C2: Qwen3-30B-A3B-shaped {L}-layer MoE decode stack (E=128, top-8, H=2048, "
-                               f"I=768), batch {B} per GPU, 24e9 B expert budget (n_hot={n_hot}/128 bf16, rest "
-                               f"int4 g=128), router mode (W_r x{a.router_scale:g} + Zipf(1.2) bias, ~90 experts "
-                               "touched per layer), controller Tp=16 L=4 with drift",
-                   "global_batch": B * world, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                               f"I=768), batch {B} per GPU, {budget / 1e9 / G:g}e9 B expert budget per GPU "
+                               f"(n_hot={n_hot}/{E_loc} bf16, rest int4 g=128), router mode (W_r x{a.router_scale:g} "
+                               "+ Zipf(1.2) bias, ~90 experts touched per layer), controller Tp=16 L=4 with drift"
+                               + (f"; expert parallel over {G} GPUs (NCCL all-to-all inside libdx)" if ep_mode else ""),
+                   "global_batch": B * world,
+                   "parallelism": f"ep{G}" if ep_mode else (f"replicas x{world}" if world > 1 else "single"),
                    "l2": "no flush: each step streams >=48 distinct layers of weights (> 126 MB L2)"},
         "roofline": {"bound": "hbm", "kernel": "k_gemm<0> decode gate/up + SwiGLU (tcgen05)", "achieved": ach0, "peak": peak,
                      "unit": "GB/s", "frac": ach0 / peak, "traffic": traffic, "peak_source": peak_src,
@@ -725,6 +757,8 @@ def run_reference(a, rank, world):
 
 def main():
     a = parse()
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):
+        os.environ["NCCL_DEBUG"] = "WARN"        # NCCL's version banner would precede the one JSON line on stdout
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

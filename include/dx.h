@@ -107,6 +107,25 @@ dx_status dx_pool_create(const dx_config* cfg, const void* const* master_bf16_ho
 dx_status dx_pool_destroy(dx_pool pool);
 dx_status dx_pool_info(dx_pool pool, dx_info* out);
 
+/* Expert parallelism over NCCL (north_star "partitioned across 1, 2, 4 and 8 B200s ... using NCCL
+ * all-to-all"; SURVEY §8(e) collective v1).  dx_get_unique_id writes a 128-byte NCCL unique id (call on one
+ * rank, broadcast it, e.g. with torch.distributed); dx_pool_create_ep is dx_pool_create plus a library-owned
+ * NCCL communicator over the cfg->ep_size ranks (cfg->ep_rank = this rank; the current CUDA device is this
+ * rank's GPU).  COLLECTIVE: every rank calls it with the same id and blocks until all have joined.  With a
+ * communicator, dx_moe_forward / dx_moe_step run the whole expert-parallel layer inside the library:
+ * dispatch over the global experts, an ncclAlltoAll of {rows per owner, token count} pairs, one device->host
+ * copy of those counts (the v1 synchronisation point), grouped ncclSend/ncclRecv of the bf16 rows and
+ * {local expert, gate} metadata, the owner-side FFN on the received rows (hotness counted there with B_tot =
+ * the global token count, so counters and plans equal a single-GPU run on the same global batch), the return
+ * exchange and the rank-order combine -- and are then collective too: every rank calls them for the same
+ * layers in the same order (T may differ per rank, max_tokens may not).  ep_size = 1 with a communicator is a
+ * valid loopback (self send/recv) that runs the same path on one GPU.  libnccl.so.2 is loaded at run time
+ * (DX_NCCL_LIB overrides).  Errors: NCCL (library missing, init or collective failure), plus
+ * dx_pool_create's. */
+dx_status dx_get_unique_id(void* id128);
+dx_status dx_pool_create_ep(const dx_config* cfg, const void* const* master_bf16_host, void* compute_stream,
+                            void* side_stream, const void* nccl_id, dx_pool* out);
+
 /* ---------------------------------------------------------------- the MoE layer (Eq. 1) */
 
 /* y = sum_{j in topk} g_j(x) E_j(x) for T tokens of one layer, each expert
@@ -136,13 +155,13 @@ dx_status dx_moe_step(dx_pool pool, int32_t layer, const void* x_bf16, int32_t T
  * in trace mode. */
 dx_status dx_get_logits(dx_pool pool, float* host_out, int64_t cap);
 
-/* ---------------------------------------------------------------- expert parallelism
+/* ---------------------------------------------------------------- expert parallelism, phase by phase
  * ep_size G > 1: GPU r owns experts [r*E/G, (r+1)*E/G) (its pool holds only those, master pointers
  * [L][E/G]); tokens are data-parallel.  One layer is dispatch -> all-to-all -> owner FFN ->
- * all-to-all -> combine.  The two all-to-alls are NCCL collectives issued by the caller (plumbing,
- * torch.distributed.all_to_all_single on the compute stream); every step of the path is in these
- * calls.  Hotness is counted on the owner from the received (expert, gate) rows, so counters and
- * plans are identical to a single-GPU run on the same global batch. */
+ * all-to-all -> combine.  With a communicator (dx_pool_create_ep) dx_moe_forward does all of it; these
+ * phase calls leave the two exchanges to the caller (used to run G pools in one process on one GPU, the
+ * exchange done by device copies).  Hotness is counted on the owner from the received (expert, gate)
+ * rows, so counters and plans are identical to a single-GPU run on the same global batch. */
 
 /* Route the T local tokens over the GLOBAL experts (router mode or trace mode as dx_moe_forward) and
  * build the send buffers, rows grouped by owner rank in (t asc, j asc) order:

@@ -90,6 +90,12 @@ struct dx_pool_s {
     CUtensorMap xk0[3], xk1[3];             // 3-D B maps (Xp / act): several K chunks per box (decode int)
     std::vector<DecMaps> dec_maps;          // host: per-layer maps of the decode kernels (k_dec.cu)
     DecBMaps dec_bmaps;
+    // expert parallelism over NCCL (ep_nccl.cu): library-owned communicator and exchange buffers
+    void* comm = nullptr;
+    __nv_bfloat16 *ep_send_rows = nullptr, *ep_recv_rows = nullptr, *ep_y_rows = nullptr, *ep_back_rows = nullptr;
+    int2 *ep_send_meta = nullptr, *ep_recv_meta = nullptr;
+    int32_t* ep_pairs = nullptr;            // device [2][G] int2: my {count, T} per peer | received per peer
+    int32_t* ep_pairs_host = nullptr;       // pinned mirror (the v1 host synchronisation point)
     bool use_kdec = false;                  // DX_DEC=1: the k_dec.cu decode kernels instead of k_gemm's decode
                                             // configuration (A/B runs; measured slower on the int tiers)
 };
@@ -302,8 +308,8 @@ static dx_status validate(const dx_config* c) {
     return DX_OK;
 }
 
-extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* master, void* compute_stream,
-                                    void* side_stream, dx_pool* out) {
+static dx_status pool_create(const dx_config* cfg, const void* const* master, void* compute_stream,
+                             void* side_stream, const void* nccl_id, dx_pool* out) {
     dx_status st = validate(cfg);
     if (st != DX_OK) return st;
     DX_CHECK(master && out, DX_ERR_INVALID_ARG, "null master/out");
@@ -337,10 +343,11 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     // ---- the one device allocation: weights | controller | workspace | staging
     const int T = cfg->max_tokens, k = p->k, L = p->L;
     const int G = cfg->ep_size;
+    const bool ep = G > 1 || nccl_id != nullptr;     // dispatch-side workspace (and NCCL buffers with an id)
     // entries (rows) one forward can see: T*k locally; an EP owner receives up to G*T*min(k, E_loc) rows
     const size_t n_ent = G > 1 ? std::max((size_t)T * k, (size_t)G * T * std::min(k, E)) : (size_t)T * k;
     p->n_ent = n_ent;
-    const int nblk = route_blocks((int)(G > 1 ? n_ent : (size_t)T));
+    const int nblk = route_blocks((int)(ep ? n_ent : (size_t)T));   // the owner side routes up to n_ent rows
     const size_t Ek = (size_t)E;
     size_t ctrl_bytes = 0;
     {
@@ -350,9 +357,11 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     const size_t lg_rows = (size_t)T;
     size_t ws_bytes = lg_rows * p->E * 4 + n_ent * (4 + 4 + 4 + 4 + 2 + 4) + 3 * 256 + (size_t)nblk * p->E * 8 +
                       (size_t)(p->E + 1) * 8 + n_ent * (p->I + 2 * p->H) * 2 + 64 * 256 + 4096 * 8 + 256;
-    if (G > 1)   // dispatch-side routing workspace (global experts, local tokens)
+    if (ep)      // dispatch-side routing workspace (global experts, local tokens)
         ws_bytes += lg_rows * p->E * 4 + (size_t)T * k * 22 + 3 * 256 + (size_t)route_blocks(T) * p->E * 8 +
                     (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
+    if (nccl_id) // NCCL exchange buffers: send / back rows (T*k), receive / result rows (n_ent), metadata, counts
+        ws_bytes += (size_t)T * k * (2 * p->H * 2 + 8) + n_ent * (2 * p->H * 2 + 8) + (size_t)G * 16 + 6 * 256;
     const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
     const size_t total = (size_t)L * p->layer_bytes + ctrl_bytes + ws_bytes + stage_bytes + ptr_bytes + 4096;
@@ -404,7 +413,7 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
     w.ent = carve<int16_t>(q, n_ent);
     w.gm = carve<uint32_t>(q, n_ent);
     w.gbar = carve<unsigned>(q, 2);
-    if (G > 1) {
+    if (ep) {
         RouteWs& v = p->ws_src;
         v.logits = carve<float>(q, lg_rows * p->E);
         v.idx = carve<int32_t>(q, (size_t)T * k);
@@ -421,6 +430,15 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         v.ent = carve<int16_t>(q, (size_t)T * k);
         v.gm = carve<uint32_t>(q, (size_t)T * k);
         v.gbar = carve<unsigned>(q, 2);
+    }
+    if (nccl_id) {
+        p->ep_send_rows = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
+        p->ep_back_rows = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
+        p->ep_send_meta = carve<int2>(q, (size_t)T * k);
+        p->ep_recv_rows = carve<__nv_bfloat16>(q, n_ent * p->H);
+        p->ep_y_rows = carve<__nv_bfloat16>(q, n_ent * p->H);
+        p->ep_recv_meta = carve<int2>(q, n_ent);
+        p->ep_pairs = carve<int32_t>(q, (size_t)4 * G);
     }
     p->act = carve<__nv_bfloat16>(q, n_ent * p->I);
     p->Y = carve<__nv_bfloat16>(q, n_ent * p->H);
@@ -462,6 +480,15 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
         dx_pool_destroy(p);
         return code;
     };
+    if (nccl_id) {
+        // collective: every rank of the EP group creates its pool with the same id (blocks until all joined)
+        if (cudaHostAlloc((void**)&p->ep_pairs_host, (size_t)4 * G * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
+            dx_set_error("cudaHostAlloc(EP counts) failed");
+            return fail(DX_ERR_OOM);
+        }
+        st = ep_nccl_init(nccl_id, G, cfg->ep_rank, &p->comm);
+        if (st != DX_OK) return fail(st);
+    }
 
     // ---- HIGH image sources (the DRAM cache)
     p->hi_img_host.resize((size_t)L * E);
@@ -587,10 +614,28 @@ extern "C" dx_status dx_set_ffn_path(dx_pool p, int32_t path) {
     return DX_OK;
 }
 
+extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* master, void* compute_stream,
+                                    void* side_stream, dx_pool* out) {
+    return pool_create(cfg, master, compute_stream, side_stream, nullptr, out);
+}
+
+extern "C" dx_status dx_pool_create_ep(const dx_config* cfg, const void* const* master, void* compute_stream,
+                                       void* side_stream, const void* nccl_id, dx_pool* out) {
+    DX_CHECK(nccl_id, DX_ERR_INVALID_ARG, "null nccl_id (use dx_pool_create without expert parallelism)");
+    return pool_create(cfg, master, compute_stream, side_stream, nccl_id, out);
+}
+
+extern "C" dx_status dx_get_unique_id(void* id128) {
+    DX_CHECK(id128, DX_ERR_INVALID_ARG, "null id");
+    return ep_nccl_unique_id(id128);
+}
+
 extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (!p) return DX_OK;
     if (p->cs) cudaStreamSynchronize(p->cs);
     if (p->ss) cudaStreamSynchronize(p->ss);
+    if (p->comm) ep_nccl_destroy(p->comm);
+    if (p->ep_pairs_host) cudaFreeHost(p->ep_pairs_host);
     for (auto ev : p->ev_side) cudaEventDestroy(ev);
     if (p->ev_plan) cudaEventDestroy(p->ev_plan);
     if (p->own_ss && p->ss) cudaStreamDestroy(p->ss);
@@ -670,7 +715,7 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
 }
 
 static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void* x, int T, int k, void* y,
-                            cudaEvent_t* ev, bool fuse_fold = false);
+                            cudaEvent_t* ev, bool fuse_fold = false, int m_max = -1);
 static bool prof_begin(dx_pool p, cudaEvent_t* ev);
 static dx_status fold(dx_pool p, int layer);
 static dx_status fold_prepare(dx_pool p, int layer, FoldReq* req);
@@ -706,6 +751,9 @@ static void route_tokens(dx_pool p, int layer, const void* x, int T, const void*
     p->launches += 2;
 }
 
+static dx_status ep_forward(dx_pool p, int layer, const void* x, int T, const void* router_w, const float* router_bias,
+                            const float* logits, void* y, int32_t* topk_idx, float* topk_gate, bool fuse_fold);
+
 static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
                               const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
                               float* topk_gate, bool fuse_fold) {
@@ -714,8 +762,10 @@ static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T
     DX_CHECK(T == 0 || (x && y), DX_ERR_INVALID_ARG, "null x/y");
     DX_CHECK(T == 0 || (router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG,
              "exactly one of router_w (router mode) and logits (trace mode) must be given");
+    if (p->comm) return ep_forward(p, layer, x, T, router_w, router_bias, logits, y, topk_idx, topk_gate, fuse_fold);
     DX_CHECK(p->cfg.ep_size == 1, DX_ERR_INVALID_ARG,
-             "ep_size > 1: use dx_ep_dispatch / dx_moe_forward_routed / dx_ep_combine");
+             "ep_size > 1 without a communicator (dx_pool_create_ep): use dx_ep_dispatch / dx_moe_forward_routed / "
+             "dx_ep_combine");
     if (T == 0) return fuse_fold ? fold(p, layer) : DX_OK;
     cudaEvent_t ev[4];
     const bool sampled = prof_begin(p, ev);
@@ -756,8 +806,9 @@ extern "C" dx_status dx_get_logits(dx_pool p, float* host_out, int64_t cap) {
 
 // a6-a8 on rows already routed and placed in `ws`: grouped expert GEMMs over the slot pool, then the
 // weighted combine of k rows per token into y (k = 1: the rows themselves, EP owner side).
+// m_max: an upper bound on any expert's row count (-1: T, as for top-k routing of T tokens)
 static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void* x, int T, int k, void* y,
-                            cudaEvent_t* ev, bool fuse_fold) {
+                            cudaEvent_t* ev, bool fuse_fold, int m_max) {
     const size_t base = (size_t)layer * p->E_loc;
     const int E = p->E_loc;
     ExpertArgs a;
@@ -775,7 +826,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
     } else {
         // tcgen05 grouped GEMMs (k_gemm.cu) over the rows placed in Xp: gate/up + SwiGLU, then down.
         // m_e <= T for top-k routing; the owner side (k = 1) sees m_e <= T rows as well.
-        const bool dec = gemm_decode_cfg(T);
+        const bool dec = gemm_decode_cfg(m_max >= 0 ? m_max : T);
         if (dec && p->use_kdec) {
             // decode configuration: k_dec.cu (every weight tile read and dequantised once)
             DecArgs da;
@@ -836,17 +887,18 @@ static bool prof_begin(dx_pool p, cudaEvent_t* ev) {
 }
 
 // ---------------------------------------------------------------- expert parallelism (a15)
-extern "C" dx_status dx_ep_dispatch(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
-                                    const float* router_bias, const float* logits, void* send_rows, void* send_meta,
-                                    int32_t* send_counts, int32_t* topk_idx, float* topk_gate) {
+static dx_status ep_dispatch_impl(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
+                                  const float* router_bias, const float* logits, void* send_rows, void* send_meta,
+                                  int32_t* send_counts, int32_t* send_pairs, int32_t* topk_idx, float* topk_gate) {
     CHECK_LAYER(p, layer);
-    DX_CHECK(p->cfg.ep_size > 1, DX_ERR_INVALID_ARG, "dx_ep_dispatch needs ep_size > 1 (use dx_moe_forward)");
+    DX_CHECK(p->cfg.ep_size > 1 || p->comm, DX_ERR_INVALID_ARG, "dx_ep_dispatch needs ep_size > 1 (use dx_moe_forward)");
     DX_CHECK(T >= 0 && T <= p->cfg.max_tokens, DX_ERR_RANGE, "T=%d outside [0, max_tokens]", T);
-    DX_CHECK((router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG, "exactly one of router_w / logits");
-    DX_CHECK(send_rows && send_meta && send_counts && (T == 0 || x), DX_ERR_INVALID_ARG, "null buffer");
+    DX_CHECK(T == 0 || (router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG, "exactly one of router_w / logits");
+    DX_CHECK(send_rows && send_meta && (send_counts || send_pairs) && (T == 0 || x), DX_ERR_INVALID_ARG, "null buffer");
     p->ep_T = T;
     if (T == 0) {
-        DX_CUDA(cudaMemsetAsync(send_counts, 0, sizeof(int32_t) * p->cfg.ep_size, p->cs));
+        if (send_counts) DX_CUDA(cudaMemsetAsync(send_counts, 0, sizeof(int32_t) * p->cfg.ep_size, p->cs));
+        if (send_pairs) DX_CUDA(cudaMemsetAsync(send_pairs, 0, sizeof(int32_t) * 2 * p->cfg.ep_size, p->cs));
         return DX_OK;
     }
     RouteWs ws = p->ws_src;
@@ -865,15 +917,24 @@ extern "C" dx_status dx_ep_dispatch(dx_pool p, int32_t layer, const void* x, int
     launch_route(lg, T, p->E, p->k, 0, ws, nullptr, nullptr, nullptr, nob, p->cs);
     // rows sorted by global expert = grouped by owner rank: the placement IS the send buffer
     launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, (__nv_bfloat16*)send_rows, p->cs);
-    launch_ep_meta(ws, T * p->k, p->E_loc, p->cfg.ep_size, (int2*)send_meta, send_counts, p->cs);
+    launch_ep_meta(ws, T * p->k, p->E_loc, p->cfg.ep_size, (int2*)send_meta, send_counts, (int2*)send_pairs, T, p->cs);
     p->launches += 3;
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "dispatch launch failed: %s", cudaGetErrorString(ce));
     return DX_OK;
 }
 
-extern "C" dx_status dx_moe_forward_routed(dx_pool p, int32_t layer, const void* rows, int32_t R, const void* meta,
-                                           void* y_rows, int64_t tokens_global) {
+extern "C" dx_status dx_ep_dispatch(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
+                                    const float* router_bias, const float* logits, void* send_rows, void* send_meta,
+                                    int32_t* send_counts, int32_t* topk_idx, float* topk_gate) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    DX_CHECK(send_counts, DX_ERR_INVALID_ARG, "null send_counts");
+    return ep_dispatch_impl(p, layer, x, T, router_w, router_bias, logits, send_rows, send_meta, send_counts, nullptr,
+                            topk_idx, topk_gate);
+}
+
+static dx_status routed_impl(dx_pool p, int32_t layer, const void* rows, int32_t R, const void* meta, void* y_rows,
+                             int64_t tokens_global) {
     CHECK_LAYER(p, layer);
     DX_CHECK(R >= 0 && (size_t)R <= p->n_ent, DX_ERR_RANGE, "R=%d exceeds the workspace (%zu rows)", R, p->n_ent);
     DX_CHECK(tokens_global >= 0, DX_ERR_INVALID_ARG, "tokens_global < 0");
@@ -891,12 +952,71 @@ extern "C" dx_status dx_moe_forward_routed(dx_pool p, int32_t layer, const void*
                        p->ctrl.tier + base, p->wbytes, p->dev_err, p->cs);
     launch_place(R, p->E_loc, 1, ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
     p->launches += 2;
-    return expert_ffn(p, layer, ws, rows, R, 1, y_rows, ev);
+    // an expert receives at most one row per token of the step: m_e <= min(R, tokens_global)
+    return expert_ffn(p, layer, ws, rows, R, 1, y_rows, ev, false,
+                      (int)std::min<int64_t>(R, tokens_global > 0 ? tokens_global : R));
+}
+
+extern "C" dx_status dx_moe_forward_routed(dx_pool p, int32_t layer, const void* rows, int32_t R, const void* meta,
+                                           void* y_rows, int64_t tokens_global) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    return routed_impl(p, layer, rows, R, meta, y_rows, tokens_global);
+}
+
+// One EP layer inside the library (SURVEY §8(e) collective v1): dispatch over the global experts, NCCL count
+// exchange + one host synchronisation, grouped send/recv of rows and metadata, the owner-side FFN on the received
+// rows (hotness counted here, B_tot = the global token count), the return exchange, the rank-order combine.
+static dx_status ep_forward(dx_pool p, int layer, const void* x, int T, const void* router_w, const float* router_bias,
+                            const float* logits, void* y, int32_t* topk_idx, float* topk_gate, bool fuse_fold) {
+    const int G = p->cfg.ep_size, k = p->k;
+    dx_status st = ep_dispatch_impl(p, layer, x, T, router_w, router_bias, logits, p->ep_send_rows, p->ep_send_meta,
+                                    nullptr, p->ep_pairs, topk_idx, topk_gate);
+    if (st != DX_OK) return st;
+    int32_t* recv_pairs = p->ep_pairs + 2 * G;
+    st = ep_nccl_exchange_counts(p->comm, G, p->ep_pairs, recv_pairs, p->cs);
+    if (st != DX_OK) return st;
+    DX_CUDA(cudaMemcpyAsync(p->ep_pairs_host, p->ep_pairs, sizeof(int32_t) * 4 * G, cudaMemcpyDeviceToHost, p->cs));
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    std::vector<int> sc(G), rc(G), soff(G), roff(G);
+    int64_t tokens_global = 0;
+    int ns = 0, R = 0;
+    for (int r = 0; r < G; ++r) {
+        sc[r] = p->ep_pairs_host[2 * r];
+        rc[r] = p->ep_pairs_host[2 * G + 2 * r];
+        tokens_global += p->ep_pairs_host[2 * G + 2 * r + 1];
+        soff[r] = ns;
+        roff[r] = R;
+        ns += sc[r];
+        R += rc[r];
+    }
+    DX_CHECK(ns == T * k, DX_ERR_INVALID_ARG, "internal: dispatched %d rows != T*k = %d", ns, T * k);
+    DX_CHECK(R >= 0 && (size_t)R <= p->n_ent, DX_ERR_RANGE, "received %d rows > workspace %zu (max_tokens per rank "
+             "must be the same on every rank)", R, p->n_ent);
+    st = ep_nccl_exchange_rows(p->comm, G, p->H, p->ep_send_rows, p->ep_send_meta, sc.data(), soff.data(),
+                               p->ep_recv_rows, p->ep_recv_meta, rc.data(), roff.data(), p->cs);
+    if (st != DX_OK) return st;
+    st = routed_impl(p, layer, p->ep_recv_rows, R, p->ep_recv_meta, p->ep_y_rows, tokens_global);
+    if (st != DX_OK) return st;
+    st = ep_nccl_exchange_rows(p->comm, G, p->H, p->ep_y_rows, nullptr, rc.data(), roff.data(), p->ep_back_rows, nullptr,
+                               sc.data(), soff.data(), p->cs);
+    if (st != DX_OK) return st;
+    if (fuse_fold) {
+        FoldReq req;
+        st = fold_prepare(p, layer, &req);
+        if (st != DX_OK) return st;
+        launch_combine(p->ep_back_rows, T, k, p->H, (__nv_bfloat16*)y, p->cs, p->ws_src_live.inv, &p->ctrl, &req);
+    } else if (T > 0) {
+        launch_combine(p->ep_back_rows, T, k, p->H, (__nv_bfloat16*)y, p->cs, p->ws_src_live.inv);
+    }
+    p->launches += 1;
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "EP combine launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
 }
 
 extern "C" dx_status dx_ep_combine(dx_pool p, int32_t layer, const void* back_rows, int32_t T, void* y) {
     CHECK_LAYER(p, layer);
-    DX_CHECK(p->cfg.ep_size > 1, DX_ERR_INVALID_ARG, "dx_ep_combine needs ep_size > 1");
+    DX_CHECK(p->cfg.ep_size > 1 || p->comm, DX_ERR_INVALID_ARG, "dx_ep_combine needs ep_size > 1");
     DX_CHECK(T == p->ep_T, DX_ERR_INVALID_ARG, "T=%d does not match the last dispatch (%d)", T, p->ep_T);
     if (T == 0) return DX_OK;
     DX_CHECK(back_rows && y, DX_ERR_INVALID_ARG, "null buffer");

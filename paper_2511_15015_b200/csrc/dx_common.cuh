@@ -248,7 +248,20 @@ void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* 
 // source-side dispatch metadata / per-owner counts
 void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
                         const int32_t* tier, const u64 (&bytes)[2][2], int32_t* err, cudaStream_t st);
-void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, cudaStream_t st);
+// counts: [G] rows per owner (or NULL); pairs: [G] {rows per owner, T_src} for the NCCL count exchange (or NULL)
+void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, int2* pairs, int T_src,
+                    cudaStream_t st);
+
+// ep_nccl.cu: the NCCL transport of expert parallelism (dlopen'd libnccl, host API)
+dx_status ep_nccl_available();
+int ep_nccl_version();
+dx_status ep_nccl_unique_id(void* id128);
+dx_status ep_nccl_init(const void* id128, int G, int rank, void** comm);
+void ep_nccl_destroy(void* comm);
+dx_status ep_nccl_exchange_counts(void* comm, int G, const int32_t* pairs, int32_t* recv_pairs, cudaStream_t st);
+dx_status ep_nccl_exchange_rows(void* comm, int G, int H, const void* send_rows, const void* send_meta,
+                                const int* sc, const int* soff, void* recv_rows, void* recv_meta, const int* rc,
+                                const int* roff, cudaStream_t st);
 // E: global expert count (range check), e_cnt: local experts counted ([e_lo, e_lo + e_cnt))
 void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int e_cnt, int k, int e_lo,
                         uint32_t* cnt_acc, u64* mass_acc, int32_t* err, cudaStream_t st);

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) k_route_given(const int2* __restrict__ me
 // contiguously: [off[o*E_loc], off[(o+1)*E_loc]) ).
 __global__ void k_ep_meta(const int32_t* __restrict__ perm, const int32_t* __restrict__ idx,
                           const float* __restrict__ gate, const int32_t* __restrict__ off, int n, int E_loc, int G,
-                          int2* __restrict__ meta, int32_t* __restrict__ counts) {
+                          int2* __restrict__ meta, int32_t* __restrict__ counts, int2* __restrict__ pairs, int T_src) {
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
     const int pos = blockIdx.x * blockDim.x + threadIdx.x;
@@ -656,7 +656,11 @@ __global__ void k_ep_meta(const int32_t* __restrict__ perm, const int32_t* __res
         const int e = idx[ent];
         meta[pos] = make_int2(e % E_loc, __float_as_int(gate[ent]));
     }
-    if (pos < G) counts[pos] = off[(pos + 1) * E_loc] - off[pos * E_loc];
+    if (pos < G) {
+        const int c = off[(pos + 1) * E_loc] - off[pos * E_loc];
+        if (counts) counts[pos] = c;
+        if (pairs) pairs[pos] = make_int2(c, T_src);     // {rows for owner pos, my token count} (NCCL transport)
+    }
 }
 
 // ------------------------------------------------------------------ trace-mode counters
@@ -767,10 +771,11 @@ void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint3
               cnt_acc, mass_acc, ws.base, ws.off, ws.act_e, ws.n_act, rs, ws.done, err);
 }
 
-void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, cudaStream_t st) {
+void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, int2* pairs, int T_src,
+                    cudaStream_t st) {
     const int thr = 256, nb = ((n > G ? n : G) + thr - 1) / thr;
     dx_launch(k_ep_meta, dim3(nb > 0 ? nb : 1), dim3(thr), 0, st, g_dx_pdl, (const int32_t*)ws.perm,
-              (const int32_t*)ws.idx, (const float*)ws.gate, (const int32_t*)ws.off, n, E_loc, G, meta, counts);
+              (const int32_t*)ws.idx, (const float*)ws.gate, (const int32_t*)ws.off, n, E_loc, G, meta, counts, pairs, T_src);
 }
 
 void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int e_cnt, int k, int e_lo,

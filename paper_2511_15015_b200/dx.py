@@ -79,6 +79,8 @@ _vp, _i32, _i64, _u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.
 _P = ctypes.POINTER
 _SIG = {
     "dx_pool_create": [_P(dx_config), _vp, _vp, _vp, _P(_vp)],
+    "dx_pool_create_ep": [_P(dx_config), _vp, _vp, _vp, _vp, _P(_vp)],
+    "dx_get_unique_id": [_vp],
     "dx_pool_destroy": [_vp],
     "dx_pool_info": [_vp, _P(dx_info)],
     "dx_moe_forward": [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -163,6 +165,13 @@ def dx_last_error() -> str:
     return _lib.dx_last_error().decode(errors="replace")
 
 
+def dx_get_unique_id() -> bytes:
+    """128-byte NCCL unique id for dx_pool_create_ep (create on one rank, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.dx_get_unique_id(buf), "dx_get_unique_id")
+    return buf.raw
+
+
 def dx_quantize(w, N, K, g, bits, codes, scales, zeros, stream=None):
     _check(_lib.dx_quantize(_ptr(w), N, K, g, bits, _ptr(codes), _ptr(scales), _ptr(zeros), _stream(stream)),
            "dx_quantize")
@@ -176,13 +185,19 @@ def dx_dequantize(codes, scales, zeros, N, K, g, bits, w, stream=None):
 class Pool:
     """Owns one dx_pool; methods are the dx_* calls of include/dx.h with the pool bound."""
 
-    def __init__(self, cfg: dx_config, master_ptrs, compute_stream=None, side_stream=None):
+    def __init__(self, cfg: dx_config, master_ptrs, compute_stream=None, side_stream=None, nccl_id: bytes = None):
+        """nccl_id (bytes from dx_get_unique_id): dx_pool_create_ep -- a collective over cfg.ep_size ranks."""
         arr = (ctypes.c_void_p * len(master_ptrs))(*[int(p) for p in master_ptrs])
         self._keep = arr
         h = ctypes.c_void_p()
         self.cfg = cfg
-        _check(_lib.dx_pool_create(ctypes.byref(cfg), ctypes.cast(arr, ctypes.c_void_p), _stream(compute_stream),
-                                   _stream(side_stream), ctypes.byref(h)), "dx_pool_create")
+        if nccl_id is None:
+            _check(_lib.dx_pool_create(ctypes.byref(cfg), ctypes.cast(arr, ctypes.c_void_p), _stream(compute_stream),
+                                       _stream(side_stream), ctypes.byref(h)), "dx_pool_create")
+        else:
+            idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            _check(_lib.dx_pool_create_ep(ctypes.byref(cfg), ctypes.cast(arr, ctypes.c_void_p), _stream(compute_stream),
+                                          _stream(side_stream), idb, ctypes.byref(h)), "dx_pool_create_ep")
         self.h = h.value
         self.info = dx_info()
         _check(_lib.dx_pool_info(self.h, ctypes.byref(self.info)), "dx_pool_info")

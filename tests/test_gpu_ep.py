@@ -80,3 +80,51 @@ def test_ep_local_matches_oracle_and_single_gpu(dx, G):
     for p in pools:
         p.close()
     single.close()
+
+
+@pytest.mark.parametrize("router", [False, True], ids=["trace", "router"])
+def test_ep_nccl_loopback_matches_single_pool(dx, router):
+    """The in-library NCCL expert-parallel layer (dx_pool_create_ep, SURVEY §8(e) collective v1) on a one-rank
+    communicator: dispatch, NCCL count exchange + host sync, grouped send/recv of rows and metadata (to self),
+    owner-side FFN, return exchange, combine -- through dx_moe_step over warm-up, finalize, plan periods with
+    transitions and their publication.  Routing, counters, EMA scores, plans and tables must be bit-exact to a
+    plain pool fed the same steps; y within 2e-2 of the oracle (the owner side runs the grouped GEMMs on T*k
+    k=1 rows, i.e. another tile configuration than the plain pool's)."""
+    E, k, H, I, g, T, W, Tp = 16, 4, 256, 128, 64, 24, 3, 2
+    n_hot = 4
+    m = Masters(7, 1, E, H, I)
+    cfg = make_cfg(dx, 1, E, k, H, I, g, 16, 4, budget_for(E, H, I, g, 16, 4, n_hot, 1), 1, 0.9, Tp, W, 2, 1, T)
+    nid = dx.dx_get_unique_id()
+    ep_pool = dx.Pool(cfg, m.ptrs(), torch.cuda.current_stream(), nccl_id=nid)
+    plain = dx.Pool(cfg, m.ptrs(), torch.cuda.current_stream())
+    wr = synth.router_bf16(7, 0, E, H)
+    wr_d = bf16_dev(wr)
+    for step in range(14):
+        x = synth.normal_bf16(7, 1, step, 0, (T, H))
+        lg = synth.trace_logits(7, 0, step, T, E, 1.2)
+        kw = dict(router_w=wr_d) if router else dict(logits=torch.from_numpy(lg).cuda())
+        tab = plain.dx_get_table(0)
+        outs = []
+        for p in (ep_pool, plain):
+            y = torch.zeros(T, H, dtype=torch.bfloat16, device="cuda")
+            idx = torch.zeros(T, k, dtype=torch.int32, device="cuda")
+            gate = torch.zeros(T, k, dtype=torch.float32, device="cuda")
+            p.dx_moe_step(0, bf16_dev(x), T, y, topk_idx=idx, topk_gate=gate, **kw)
+            outs.append((to_u16(y), idx.cpu().numpy(), gate.cpu().numpy()))
+        (y_ep, i_ep, g_ep), (y_pl, i_pl, g_pl) = outs
+        assert np.array_equal(i_ep, i_pl) and np.array_equal(g_ep.view(np.uint32), g_pl.view(np.uint32)), step
+        Wt = {int(e): oracle.expert_tier(m.get(0, int(e)), H, I, g, 16, 4, bool(tab["tier"][e])) for e in np.unique(i_pl)}
+        _, y_o = oracle.moe_ffn(x, i_pl, g_pl, Wt, H, I, nthreads=8)
+        assert rel_err(y_ep, y_o) <= 2e-2 and rel_err(y_pl, y_o) <= 2e-2, step
+        h_ep, h_pl = ep_pool.dx_get_hotness(0), plain.dx_get_hotness(0)
+        assert np.array_equal(h_ep["S"].view(np.uint64), h_pl["S"].view(np.uint64)), step
+        assert h_ep["t"] == h_pl["t"] == step + 1
+        t_ep, t_pl = ep_pool.dx_get_table(0), plain.dx_get_table(0)
+        for key in ("tier", "slot", "version", "in_flight"):
+            assert np.array_equal(t_ep[key], t_pl[key]), (step, key)
+    transitions = int(np.sum(plain.dx_get_table(0)["version"]))
+    ep_pool.dx_sync()
+    plain.dx_sync()
+    assert transitions > 0
+    ep_pool.close()
+    plain.close()
