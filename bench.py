@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-batch-sweep", action="store_true")
     ap.add_argument("--no-q80b", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent full replicas instead of EP")
+    ap.add_argument("--no-teleport", action="store_true", help="skip the zero-cost-transition replay (switch cost)")
     ap.add_argument("--ep-loopback", action="store_true",
                     help="N = 1: run the expert-parallel path on a one-rank NCCL communicator (tests the EP leg)")
     ap.add_argument("--switch-stress", action="store_true",
@@ -305,24 +306,28 @@ def run_ours(a, rank, world, local_rank):
     y_p = [y[i].data_ptr() for i in range(2)]
     wr_p = [wr[l].data_ptr() for l in range(L)]
     bias_p = [[bias[l, ep].data_ptr() for ep in range(n_epochs)] for l in range(L)]
-    mstep = pool.dx_moe_step           # forward + hotness update + plan, fold fused into the combine
+    nonlocal_pool = [pool]             # the pool step() drives (the teleport replay swaps in its own)
 
     def step(x):
         s_ = step_counter[0]
         ep = s_ // c["drift"]
         xp = x if isinstance(x, int) else x.data_ptr()
+        mstep = nonlocal_pool[0].dx_moe_step   # forward + hotness update + plan, fold fused into the combine
         for l in range(L):
             mstep(l, xp, B, y_p[l & 1], router_w=wr_p[l], router_bias=bias_p[l][ep])
         step_counter[0] += 1
 
     # controller warm-up (t < W) and finalize at t = W, then the bench warm-up
-    for s_ in range(c["W"]):
-        step(xs[s_])
-    for l in range(L):
-        pool.dx_plan_precision(l)
-    for s_ in range(a.warmup):
-        step(xs[c["W"] + s_])
-    pool.dx_sync()
+    def warm(pool_):
+        for s_ in range(c["W"]):
+            step(xs[s_])
+        for l in range(L):
+            pool_.dx_plan_precision(l)
+        for s_ in range(a.warmup):
+            step(xs[c["W"] + s_])
+        pool_.dx_sync()
+
+    warm(pool)
     pool.dx_profile_read()
     dist_on = world > 1
     if dist_on:
@@ -356,6 +361,29 @@ def run_ours(a, rank, world, local_rank):
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_max = float(tt.item())
+
+    def teleport_replay():
+        """The same steps from a fresh pool whose transitions are free (dx_set_teleport): identical routing,
+        plans and per-step tier tables, no transfer work -- SURVEY §8(d)'s exposed switch time is
+        (t_on - t_teleport) / t_on over the timed steps."""
+        tp = dx.Pool(cfg, ptrs, stream, nccl_id=None)
+        tp.dx_set_teleport(True)
+        saved = step_counter[0]
+        step_counter[0] = 0
+        nonlocal_pool[0] = tp
+        warm(tp)
+        tp.dx_profile_enable(PROF_EVERY)           # the same event sampling as the timed run
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s_ in range(a.steps):
+            step(xs[base + s_])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        nonlocal_pool[0] = pool
+        step_counter[0] = saved
+        tp.close()
+        return e0.elapsed_time(e1)
     # ---------------- end-to-end: host x -> device, stack, y -> host, every step
     e2e = None
     if not a.no_e2e:
@@ -421,6 +449,8 @@ def run_ours(a, rank, world, local_rank):
                              "exposed_ms_total": prof["exposed_ms"],
                              "exposed_frac_of_step_time": prof["exposed_ms"] / ms if ms > 0 else None,
                              "xfer_ms_mean": prof["xfer_ms"] / max(prof["plans"], 1),
+                             "promotion_gbs": prof["copy_bytes"] / (prof["copy_ms"] / 1e3) / 1e9
+                             if prof["copy_ms"] > 0 else None,
                              "xfer_ms_max": prof["xfer_max_ms"]},
                   "setup_s": {"masters": t_gen, "pool_create": t_pool},
                   "host_issue_ms_per_step": host_ms / a.steps},
@@ -433,6 +463,14 @@ def run_ours(a, rank, world, local_rank):
     if a.prefill_tokens > 0:
         out["extra"]["prefill"] = prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream)
     pool.close()
+    if not ep_mode and not a.no_teleport:
+        ms_tel = teleport_replay()
+        sw = out["extra"]["switch"]
+        sw["teleport_ms_per_step"] = ms_tel / a.steps
+        sw["on_ms_per_step"] = ms / a.steps
+        sw["exposed_frac_teleport"] = (ms - ms_tel) / ms
+        sw["definition"] = ("(t_on - t_teleport) / t_on over the timed steps; teleport = a fresh pool replaying the "
+                            "same steps with dx_set_teleport (same plans and tier tables, no transfers)")
     torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
     del arr
     return out
@@ -630,7 +668,10 @@ def switch_stress(a):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     E, k, H, I, g, s_sp = 128, 8, 2048, 768, 128, 2
-    Tp, W, lag, alpha = 8, 16, 2, 0.9
+    W, alpha = 16, 0.9
+    # publish lag sized so the lag window (lag x step time) covers a plan's transfers (~0.5-1 ms: a 9.4 MB
+    # promotion over PCIe plus a demotion): decode steps of one layer take ~0.11 ms, prefill steps ~1 ms
+    lag_of = {"decode": (16, 10), "prefill": (8, 2)}          # mode -> (Tp, L)
     arr, ptrs = host_masters(a.seed, 1, E, H, I, 0, 1)
     S_h, S_l = dx.dx_slot_bytes(H, I, g, 16), dx.dx_slot_bytes(H, I, g, 4)
     wr = torch.from_numpy(router_weights(a.seed, 0, E, H, a.router_scale).view(np.int16)).to(dev).view(torch.bfloat16)
@@ -638,7 +679,8 @@ def switch_stress(a):
     rows = []
     for n_hot in (13, 26, 38, 51, 64, 77, 90, 102, 115, 128):
         budget = n_hot * S_h + (E - n_hot) * S_l + s_sp * (S_h + S_l)
-        for mode, T, steps in (("decode", 16, 48), ("prefill", 4096, 24)):
+        for mode, T, steps in (("decode", 16, 64), ("prefill", 4096, 24)):
+            Tp, lag = lag_of[mode]
             cfg = dx.dx_config()
             cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = 1, E, k, H, I, g
             cfg.high_bits, cfg.low_bits = 16, 4
@@ -646,8 +688,6 @@ def switch_stress(a):
             cfg.n_spare, cfg.ema_alpha = s_sp, alpha
             cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = Tp, W, Tp, lag
             cfg.max_tokens, cfg.ep_rank, cfg.ep_size = T, 0, 1
-            pool = dx.Pool(cfg, ptrs, stream)
-            assert pool.info.n_hot == n_hot, (pool.info.n_hot, n_hot)
             total = W + Tp + steps + 1
             bias = torch.stack([torch.from_numpy(synth.zipf_logp(
                 synth.rank_perm(a.seed, 0, ep, E, max(n_hot, 1), 0.5), 1.2)) for ep in range(total // Tp + 2)]).to(dev)
@@ -655,42 +695,56 @@ def switch_stress(a):
                   for i in range(2)]
             y = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
 
-            def one(t):
-                pool.dx_moe_forward(0, xs[t & 1], T, y, router_w=wr, router_bias=bias[t // Tp])
-                pool.dx_hotness_update(0)
-                pool.dx_plan_precision(0)
+            def run_cfg(teleport):
+                pool = dx.Pool(cfg, ptrs, stream)
+                assert pool.info.n_hot == n_hot, (pool.info.n_hot, n_hot)
+                pool.dx_set_teleport(teleport)
 
-            for t in range(W):
-                one(t)
-            pool.dx_plan_precision(0)
-            for t in range(W, W + Tp):
-                one(t)
-            pool.dx_sync()
-            pool.dx_profile_read()
-            pool.dx_profile_enable(True)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for t in range(W + Tp, W + Tp + steps):
-                one(t)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1)
-            pr = pool.dx_profile_read()
-            pool.dx_profile_enable(False)
-            pool.close()
+                def one(t):
+                    pool.dx_moe_forward(0, xs[t & 1], T, y, router_w=wr, router_bias=bias[t // Tp])
+                    pool.dx_hotness_update(0)
+                    pool.dx_plan_precision(0)
+
+                for t in range(W):
+                    one(t)
+                pool.dx_plan_precision(0)
+                for t in range(W, W + Tp):
+                    one(t)
+                pool.dx_sync()
+                pool.dx_profile_read()
+                pool.dx_profile_enable(True)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for t in range(W + Tp, W + Tp + steps):
+                    one(t)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms_ = e0.elapsed_time(e1)
+                pr_ = pool.dx_profile_read()
+                pool.dx_profile_enable(False)
+                pool.close()
+                return ms_, pr_
+
+            ms, pr = run_cfg(False)
+            ms_tel, _ = run_cfg(True)
             rows.append({"n_hot": n_hot, "hot_frac": n_hot / E, "mode": mode, "tokens": T, "steps": steps,
-                         "ms_per_step": ms / steps, "promotions": pr["promotions"], "demotions": pr["demotions"],
+                         "ms_per_step": ms / steps, "teleport_ms_per_step": ms_tel / steps,
+                         "exposed_frac_teleport": (ms - ms_tel) / ms if ms > 0 else None,
+                         "promotions": pr["promotions"], "demotions": pr["demotions"],
                          "plans": pr["plans"], "switch_ms_mean": pr["xfer_ms"] / max(pr["plans"], 1),
-                         "switch_ms_max": pr["xfer_max_ms"], "exposed_ms": pr["exposed_ms"],
-                         "exposed_frac": pr["exposed_ms"] / ms if ms > 0 else None})
+                         "switch_ms_max": pr["xfer_max_ms"], "Tp": Tp, "publish_lag": lag,
+                         "promotion_gbs": pr["copy_bytes"] / (pr["copy_ms"] / 1e3) / 1e9 if pr["copy_ms"] > 0 else None,
+                         "publish_stall_ms": pr["exposed_ms"],
+                         "publish_stall_frac": pr["exposed_ms"] / ms if ms > 0 else None})
     torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
-    return {"metric": "C5 precision-switch stress: exposed switch time / step time", "unit": "fraction",
+    return {"metric": "C5 precision-switch stress: exposed switch time (t_on - t_teleport) / t_on", "unit": "fraction",
             "higher_is_better": False, "n_gpus": 1, "data": "synthetic",
             "config": {"workload": "C5: one Q30B-shaped layer (E=128, k=8, H=2048, I=768, bf16/int4 g=128), "
-                                   "s=2 spares per tier, Tp=8, W=16, dwell=8, L=2, alpha=0.9, Zipf(1.2) router bias "
-                                   "with half of the top-n_hot set rotating every period"},
-            "value": max(r["exposed_frac"] for r in rows), "rows": rows}
+                                   "s=2 spares per tier, W=16, dwell=Tp, alpha=0.9, decode B=16 (Tp=16, L=10) and "
+                                   "prefill T=4096 (Tp=8, L=2), Zipf(1.2) router bias with half of the top-n_hot set "
+                                   "rotating every period"},
+            "value": max(r["exposed_frac_teleport"] for r in rows), "rows": rows}
 
 
 # ---------------------------------------------------------------------------------------- oracle arm

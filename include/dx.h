@@ -259,7 +259,14 @@ typedef struct {
     double   xfer_max_ms;       /* longest single plan's transitions */
     int64_t  plans;             /* plans whose transitions were issued */
     int64_t  promotions, demotions; /* transitions those plans issued */
+    double   copy_ms;           /* summed side-stream time of the plans' copy-engine promotions (H2D) */
+    uint64_t copy_bytes;        /* bytes those copies moved (copy_bytes / copy_ms = promotion bandwidth) */
 } dx_profile_t;
+/* TIMING BASELINE ONLY (SURVEY §8(d) C5 "teleport"): on != 0 makes runtime plans and their publication
+ * happen exactly as scheduled but skips the side-stream transfers, so the per-step tier tables are the
+ * same while switching costs nothing -- and the moved experts' weights are garbage.  The exposed switch
+ * time is (t_on - t_teleport) / t_on over the same steps.  Never for results. */
+dx_status dx_set_teleport(dx_pool pool, int32_t on);
 /* Per-forward CUDA-event timing: enable = 0 off; enable = n >= 1 times every n-th forward (n > 1 keeps the
    host cost of event records off most forwards).  While enabled, the device weight-byte counters count
    exactly the timed (sampled) forwards, so bytes / time stay consistent; while disabled they count every

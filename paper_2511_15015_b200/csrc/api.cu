@@ -80,6 +80,10 @@ struct dx_pool_s {
     std::vector<cudaEvent_t> prof_free;
     std::vector<cudaEvent_t> prof_wait_ev;  // pairs around the publish wait (exposed switch time)
     std::vector<cudaEvent_t> prof_xfer_ev;  // pairs around side-stream transitions (switch latency)
+    std::vector<cudaEvent_t> prof_copy_ev;  // pairs around the copy-engine promotions of a plan
+    std::vector<u64> prof_copy_bytes;       // their bytes
+    cudaStream_t ss2 = nullptr;             // second side stream: demotion kernels beside the H2D copies
+    cudaEvent_t ev_dem = nullptr;
     i64 prof_fwd = 0;
     int ffn_path = 0;                       // 0: tcgen05 grouped GEMM, 1: mma.sync decode kernel
     bool last_logits_router = false;        // the last forward computed router logits into ws.logits
@@ -96,6 +100,16 @@ struct dx_pool_s {
     int2 *ep_send_meta = nullptr, *ep_recv_meta = nullptr;
     int32_t* ep_pairs = nullptr;            // device [2][G] int2: my {count, T} per peer | received per peer
     int32_t* ep_pairs_host = nullptr;       // pinned mirror (the v1 host synchronisation point)
+    u64 copy_promotions = 0;                // promotions issued as copy-engine H2D copies
+    bool teleport = false;                  // timing baseline: plans and publications without the transfers
+    // runtime plans reach the host through pinned memory; the host then issues the promotions' H2D copies on the
+    // copy engine (cudaMemcpyAsync on the side stream) and the demotion kernel -- as soon as the plan is seen
+    // done (polled at every library call), at the latest at the publication step
+    int4* plan_host = nullptr;              // pinned [L][E_loc] copy of the device plan list
+    int32_t* plan_n_host = nullptr;         // pinned [L]
+    std::vector<cudaEvent_t> ev_planh;      // plan copied to the host
+    std::vector<int> xfer_pending;          // per layer: plan made, transfers not yet issued
+    int n_pending = 0;
     bool use_kdec = false;                  // DX_DEC=1: the k_dec.cu decode kernels instead of k_gemm's decode
                                             // configuration (A/B runs; measured slower on the int tiers)
 };
@@ -469,8 +483,17 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         p->own_ss = true;
     }
     cudaEventCreateWithFlags(&p->ev_plan, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p->ev_dem, cudaEventDisableTiming);
+    {
+        int lo_prio, hi_prio;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        cudaStreamCreateWithPriority(&p->ss2, cudaStreamNonBlocking, lo_prio);
+    }
     p->ev_side.resize(L);
     for (int l = 0; l < L; ++l) cudaEventCreateWithFlags(&p->ev_side[l], cudaEventDisableTiming);
+    p->ev_planh.resize(L);
+    for (int l = 0; l < L; ++l) cudaEventCreateWithFlags(&p->ev_planh[l], cudaEventDisableTiming);
+    p->xfer_pending.assign(L, 0);
     p->t.assign(L, 0);
     p->publish_at.assign(L, -1);
     p->pend_tokens.assign(L, 0);
@@ -480,6 +503,11 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         dx_pool_destroy(p);
         return code;
     };
+    if (cudaHostAlloc((void**)&p->plan_host, (size_t)L * E * sizeof(int4), cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc((void**)&p->plan_n_host, (size_t)L * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
+        dx_set_error("cudaHostAlloc(plan mirror) failed");
+        return fail(DX_ERR_OOM);
+    }
     if (nccl_id) {
         // collective: every rank of the EP group creates its pool with the same id (blocks until all joined)
         if (cudaHostAlloc((void**)&p->ep_pairs_host, (size_t)4 * G * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
@@ -636,6 +664,12 @@ extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (p->ss) cudaStreamSynchronize(p->ss);
     if (p->comm) ep_nccl_destroy(p->comm);
     if (p->ep_pairs_host) cudaFreeHost(p->ep_pairs_host);
+    for (auto ev : p->ev_planh) cudaEventDestroy(ev);
+    if (p->ss2) { cudaStreamSynchronize(p->ss2); cudaStreamDestroy(p->ss2); }
+    if (p->ev_dem) cudaEventDestroy(p->ev_dem);
+    for (auto ev : p->prof_copy_ev) cudaEventDestroy(ev);
+    if (p->plan_host) cudaFreeHost(p->plan_host);
+    if (p->plan_n_host) cudaFreeHost(p->plan_n_host);
     for (auto ev : p->ev_side) cudaEventDestroy(ev);
     if (p->ev_plan) cudaEventDestroy(p->ev_plan);
     if (p->own_ss && p->ss) cudaStreamDestroy(p->ss);
@@ -644,6 +678,12 @@ extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (p->hi_cache) cudaFreeHost(p->hi_cache);
     if (p->arena) cudaFree(p->arena);
     delete p;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_set_teleport(dx_pool p, int32_t on) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    p->teleport = on != 0;
     return DX_OK;
 }
 
@@ -692,6 +732,15 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
         out->xfer_max_ms = a > out->xfer_max_ms ? a : out->xfer_max_ms;
         out->plans += 1;
     }
+    for (size_t i = 0; i + 1 < p->prof_copy_ev.size(); i += 2) {
+        float a = 0;
+        DX_CUDA(cudaEventElapsedTime(&a, p->prof_copy_ev[i], p->prof_copy_ev[i + 1]));
+        out->copy_ms += a;
+        out->copy_bytes += p->prof_copy_bytes[i / 2];
+    }
+    for (size_t i = 0; i < p->prof_copy_ev.size(); i += 2) p->prof_free.push_back(p->prof_copy_ev[i + 1]);
+    p->prof_copy_ev.clear();
+    p->prof_copy_bytes.clear();
     for (auto e : p->prof_ev) p->prof_free.push_back(e);
     for (auto e : p->prof_wait_ev) p->prof_free.push_back(e);
     for (auto e : p->prof_xfer_ev) p->prof_free.push_back(e);
@@ -753,6 +802,7 @@ static void route_tokens(dx_pool p, int layer, const void* x, int T, const void*
 
 static dx_status ep_forward(dx_pool p, int layer, const void* x, int T, const void* router_w, const float* router_bias,
                             const float* logits, void* y, int32_t* topk_idx, float* topk_gate, bool fuse_fold);
+static dx_status poll_transfers(dx_pool p, int wait_layer = -1);
 
 static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
                               const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
@@ -762,6 +812,10 @@ static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T
     DX_CHECK(T == 0 || (x && y), DX_ERR_INVALID_ARG, "null x/y");
     DX_CHECK(T == 0 || (router_w != nullptr) != (logits != nullptr), DX_ERR_INVALID_ARG,
              "exactly one of router_w (router mode) and logits (trace mode) must be given");
+    {
+        dx_status st = poll_transfers(p);
+        if (st != DX_OK) return st;
+    }
     if (p->comm) return ep_forward(p, layer, x, T, router_w, router_bias, logits, y, topk_idx, topk_gate, fuse_fold);
     DX_CHECK(p->cfg.ep_size == 1, DX_ERR_INVALID_ARG,
              "ep_size > 1 without a communicator (dx_pool_create_ep): use dx_ep_dispatch / dx_moe_forward_routed / "
@@ -1034,6 +1088,8 @@ static dx_status fold_prepare(dx_pool p, int layer, FoldReq* req) {
     p->pend_tokens[layer] = 0;
     const i64 t_new = p->t[layer] + 1;
     if (p->publish_at[layer] == t_new) {
+        dx_status st = poll_transfers(p, layer);        // the plan's transfers must have been issued by now
+        if (st != DX_OK) return st;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (p->profiling) {
             e0 = prof_event(p);
@@ -1115,6 +1171,74 @@ static dx_status read_plan(dx_pool p, int layer, dx_plan* out) {
     return DX_OK;
 }
 
+// a12/a13 of one layer's runtime plan on the side stream: the demotion kernel (on-device quantisation) and one
+// copy-engine H2D per promotion from the pinned HIGH image into its destination block; ev_side marks them done.
+static dx_status issue_transfers(dx_pool p, int layer) {
+    const size_t E = (size_t)p->E_loc;
+    cudaEvent_t x0 = nullptr;
+    if (p->profiling) {
+        x0 = prof_event(p);
+        p->prof_xfer_ev.push_back(x0);
+        DX_CUDA(cudaEventRecord(x0, p->ss));
+    }
+    const int n = p->plan_n_host[layer];
+    int nd = 0;
+    for (int i = 0; i < n; ++i) nd += p->plan_host[layer * E + i].y == -1;
+    if (nd > 0) {                    // demotions: device quantisation on the second side stream, beside the copies
+        DX_CUDA(cudaStreamWaitEvent(p->ss2, p->ev_planh[layer], 0));
+        launch_transitions(p->ctrl, layer, xfer_args(p, layer), n, 3, p->ss2);
+        DX_CUDA(cudaEventRecord(p->ev_dem, p->ss2));
+        p->launches += 1;
+    }
+    const size_t bytes = p->hi.bits == 16 ? (size_t)3 * p->I * p->H * 2 : (size_t)p->hi.bytes;
+    uint8_t* hi_region = p->weights + (size_t)layer * p->layer_bytes + p->hi_base;
+    u64 np = 0;
+    for (int i = 0; i < n; ++i) {
+        const int4 cmd = p->plan_host[layer * E + i];
+        if (cmd.y != 1) continue;
+        DX_CUDA(cudaMemcpyAsync(hi_region + (size_t)cmd.z * p->hi.bytes, p->hi_img_host[layer * E + cmd.x], bytes,
+                                cudaMemcpyHostToDevice, p->ss));
+        ++np;
+    }
+    if (x0 && np > 0) {
+        cudaEvent_t xc = prof_event(p);
+        DX_CUDA(cudaEventRecord(xc, p->ss));
+        p->prof_copy_ev.push_back(x0);
+        p->prof_copy_ev.push_back(xc);
+        p->prof_copy_bytes.push_back(np * bytes);
+    }
+    if (nd > 0) DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_dem, 0));
+    if (x0) {
+        cudaEvent_t x1 = prof_event(p);
+        p->prof_xfer_ev.push_back(x1);
+        DX_CUDA(cudaEventRecord(x1, p->ss));
+    }
+    DX_CUDA(cudaEventRecord(p->ev_side[layer], p->ss));
+    p->xfer_pending[layer] = 0;
+    p->n_pending -= 1;
+    return DX_OK;
+}
+
+// issue every pending layer's transfers whose plan has reached the host (non-blocking), or -- wait_layer >= 0 --
+// that layer's unconditionally (it publishes now)
+static dx_status poll_transfers(dx_pool p, int wait_layer) {
+    if (p->n_pending == 0) return DX_OK;
+    if (wait_layer >= 0 && p->xfer_pending[wait_layer]) {
+        DX_CUDA(cudaEventSynchronize(p->ev_planh[wait_layer]));
+        dx_status st = issue_transfers(p, wait_layer);
+        if (st != DX_OK) return st;
+    }
+    for (int l = 0; l < p->L && p->n_pending > 0; ++l) {
+        if (!p->xfer_pending[l]) continue;
+        const cudaError_t q = cudaEventQuery(p->ev_planh[l]);
+        if (q == cudaErrorNotReady) continue;
+        DX_CHECK(q == cudaSuccess, DX_ERR_CUDA, "plan event: %s", cudaGetErrorString(q));
+        dx_status st = issue_transfers(p, l);
+        if (st != DX_OK) return st;
+    }
+    return DX_OK;
+}
+
 extern "C" dx_status dx_plan_precision(dx_pool p, int32_t layer, dx_plan* out) {
     CHECK_LAYER(p, layer);
     const i64 t = p->t[layer];
@@ -1138,22 +1262,20 @@ extern "C" dx_status dx_plan_precision(dx_pool p, int32_t layer, dx_plan* out) {
     }
     if (!p->finalized[layer] || t <= c.warmup_steps || t % c.period != 0 || p->publish_at[layer] >= 0) return DX_OK;
     launch_plan(p->ctrl, layer, 0, p->cs);
-    DX_CUDA(cudaEventRecord(p->ev_plan, p->cs));
-    DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_plan, 0));
-    cudaEvent_t x0 = nullptr;
-    if (p->profiling) {
-        x0 = prof_event(p);
-        p->prof_xfer_ev.push_back(x0);
-        DX_CUDA(cudaEventRecord(x0, p->ss));
+    p->launches += 1;
+    if (p->teleport) {
+        DX_CUDA(cudaEventRecord(p->ev_side[layer], p->cs));
+    } else {
+        // the plan to pinned host memory; the transfers are issued once the host sees it (issue_transfers)
+        const size_t E = (size_t)p->E_loc;
+        DX_CUDA(cudaMemcpyAsync(p->plan_n_host + layer, p->ctrl.plan_n + layer, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                p->cs));
+        DX_CUDA(cudaMemcpyAsync(p->plan_host + layer * E, p->ctrl.plan_cmd + layer * E, E * sizeof(int4),
+                                cudaMemcpyDeviceToHost, p->cs));
+        DX_CUDA(cudaEventRecord(p->ev_planh[layer], p->cs));
+        p->xfer_pending[layer] = 1;
+        p->n_pending += 1;
     }
-    launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 0, p->ss);
-    if (x0) {
-        cudaEvent_t x1 = prof_event(p);
-        p->prof_xfer_ev.push_back(x1);
-        DX_CUDA(cudaEventRecord(x1, p->ss));
-    }
-    DX_CUDA(cudaEventRecord(p->ev_side[layer], p->ss));
-    p->launches += 2;
     p->publish_at[layer] = t + c.publish_lag;
     if (out) {
         out->due = 1;
@@ -1174,6 +1296,10 @@ static dx_status manual(dx_pool p, int layer, const int32_t* experts, int n, int
     const i64 due = p->t[layer] + p->cfg.publish_lag;
     DX_CHECK(p->publish_at[layer] < 0 || p->publish_at[layer] == due, DX_ERR_BUSY,
              "layer %d has transitions publishing at a different step", layer);
+    {
+        dx_status st = poll_transfers(p, layer);     // a pending plan's demotions read plan_cmd: issue them first
+        if (st != DX_OK) return st;
+    }
     std::vector<int2> cmds(n);
     for (int i = 0; i < n; ++i) cmds[i] = make_int2(experts[i], dir);
     // k_manual rewrites the layer's command list (plan_cmd / plan_n): transitions issued earlier for this
@@ -1212,6 +1338,12 @@ extern "C" dx_status dx_demote(dx_pool p, int32_t layer, const int32_t* experts,
 
 extern "C" dx_status dx_sync(dx_pool p) {
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    for (int l = 0; l < p->L; ++l) {
+        if (!p->xfer_pending[l]) continue;
+        dx_status st = poll_transfers(p, l);
+        if (st != DX_OK) return st;
+    }
+    DX_CUDA(cudaStreamSynchronize(p->ss2));
     DX_CUDA(cudaStreamSynchronize(p->ss));
     DX_CUDA(cudaStreamSynchronize(p->cs));
     DX_CUDA(cudaGetLastError());

@@ -214,7 +214,8 @@ __global__ void k_manual(Ctrl c, int layer, const int2* __restrict__ cmds, int n
 // (finalize only): LOW block -> LOW block.
 #define XFER_CHUNKS 64
 // mode: 0 = regular plan (promotions + demotions), 1 = finalize moves only, 2 = finalize promotions
-// only (the second finalize pass runs after every move has left the future HIGH region).
+// only (the second finalize pass runs after every move has left the future HIGH region), 3 = demotions only
+// (runtime plans: the promotions' H2D copies run on the copy engine, issued by the host).
 // Side-stream transitions run as a few small, register-lean blocks (128 threads, <= 48 registers) so
 // that each fits on an SM next to a resident persistent k_gemm CTA (736 threads x 80 registers): the
 // transfer then overlaps the expert GEMMs instead of holding SMs they are waiting for.
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(128, 10) k_xfer(Ctrl c, int layer, XferArgs x,
         const int ci = w / XFER_CHUNKS, ch = w % XFER_CHUNKS;
         const int4 cmd = c.plan_cmd[layer * E + ci];
         const int e = cmd.x, dir = cmd.y, dst = cmd.z, src = cmd.w;
-        if ((mode == 1 && dir != 0) || (mode == 2 && dir != 1)) continue;
+        if ((mode == 1 && dir != 0) || (mode == 2 && dir != 1) || (mode == 3 && dir != -1)) continue;
         if (dir == 1) {
             const uint4* s = reinterpret_cast<const uint4*>(x.hi_img[e]);
             uint4* d = reinterpret_cast<uint4*>(x.layer_base + x.hi_base + (i64)dst * x.hi.bytes);
@@ -301,7 +302,11 @@ void launch_transitions(const Ctrl& c, int layer, const XferArgs& x, int max_cmd
 #ifndef DX_XFER_BLOCKS
 #define DX_XFER_BLOCKS DX_NUM_SMS
 #endif
-    const int cap = mode == 0 ? DX_XFER_BLOCKS : 4 * DX_NUM_SMS;
+    // demotions of runtime plans (mode 3; DX_DEMOTE_BLOCKS caps the grid): measured on C5 decode, 16 blocks took
+    // 2.6 ms per plan and 4 blocks 10 ms (the warp-per-group quantiser is latency-bound), both past the publish
+    // lag, while one lean block per SM (0.37 ms) exposed ~10 % -- so the default stays at one per SM
+    static const int dem_blocks = [] { const char* e = getenv("DX_DEMOTE_BLOCKS"); return e ? atoi(e) : DX_NUM_SMS; }();
+    const int cap = mode == 0 ? DX_XFER_BLOCKS : (mode == 3 ? dem_blocks : 4 * DX_NUM_SMS);
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     k_xfer<<<grid, 128, 0, st>>>(c, layer, x, mode);

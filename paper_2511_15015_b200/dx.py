@@ -67,7 +67,8 @@ class dx_profile_t(ctypes.Structure):
                 ("weight_bytes", ctypes.c_uint64 * 2), ("active_experts", ctypes.c_uint64),
                 ("route_ms", ctypes.c_double), ("exposed_ms", ctypes.c_double), ("publishes", ctypes.c_int64),
                 ("xfer_ms", ctypes.c_double), ("xfer_max_ms", ctypes.c_double), ("plans", ctypes.c_int64),
-                ("promotions", ctypes.c_int64), ("demotions", ctypes.c_int64)]
+                ("promotions", ctypes.c_int64), ("demotions", ctypes.c_int64), ("copy_ms", ctypes.c_double),
+                ("copy_bytes", ctypes.c_uint64)]
 
 
 class dx_plan(ctypes.Structure):
@@ -104,6 +105,7 @@ _SIG = {
     "dx_ep_combine": [_vp, _i32, _vp, _i32, _vp],
     "dx_profile_enable": [_vp, _i32],
     "dx_set_ffn_path": [_vp, _i32],
+    "dx_set_teleport": [_vp, _i32],
     "dx_profile_read": [_vp, _P(dx_profile_t)],
 }
 for _n, _a in _SIG.items():
@@ -316,6 +318,10 @@ class Pool:
     def dx_set_ffn_path(self, path: int):
         _check(_lib.dx_set_ffn_path(self.h, path), "dx_set_ffn_path")
 
+    def dx_set_teleport(self, on: bool):
+        """Timing baseline only: plans publish on schedule but no transfer runs (weights become garbage)."""
+        _check(_lib.dx_set_teleport(self.h, 1 if on else 0), "dx_set_teleport")
+
     def dx_profile_enable(self, enable=True):
         """enable: False/0 off, True/1 every forward, n > 1 every n-th forward."""
         _check(_lib.dx_profile_enable(self.h, int(enable)), "dx_profile_enable")
@@ -327,4 +333,5 @@ class Pool:
                     weight_bytes=[int(pr.weight_bytes[0]), int(pr.weight_bytes[1])],
                     active_experts=int(pr.active_experts), route_ms=pr.route_ms, exposed_ms=pr.exposed_ms,
                     publishes=pr.publishes, xfer_ms=pr.xfer_ms, xfer_max_ms=pr.xfer_max_ms, plans=pr.plans,
-                    promotions=pr.promotions, demotions=pr.demotions)
+                    promotions=pr.promotions, demotions=pr.demotions, copy_ms=pr.copy_ms,
+                    copy_bytes=int(pr.copy_bytes))
