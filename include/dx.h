@@ -150,6 +150,14 @@ dx_status dx_moe_step(dx_pool pool, int32_t layer, const void* x_bf16, int32_t T
                       const void* router_w_bf16, const float* router_bias, const float* logits,
                       void* y_bf16, int32_t* topk_idx, float* topk_gate);
 
+/* dx_moe_step over layers [layer0, layer0 + n_layers) in one call (a stack step without a host round trip per
+ * layer): host arrays of n_layers DEVICE pointers, entry i for layer layer0 + i -- x, y, and either router_w
+ * (+ router_bias, whose array may be NULL) or logits.  Entries may repeat (e.g. y ping-pong, or x[i] = y[i-1]
+ * to chain the layers).  Stops at the first failing layer and returns its status. */
+dx_status dx_moe_step_layers(dx_pool pool, int32_t layer0, int32_t n_layers, const void* const* x, int32_t T,
+                             const void* const* router_w, const float* const* router_bias, const float* const* logits,
+                             void* const* y);
+
 /* The fp32 router logits [T][E] of the last router-mode forward of this pool (exactly what its top-k
  * consumed), into host memory of cap >= T*E floats.  Synchronising.  NOT_READY if the last forward was
  * in trace mode. */

@@ -848,6 +848,22 @@ extern "C" dx_status dx_moe_step(dx_pool p, int32_t layer, const void* x, int32_
     return dx_plan_precision(p, layer, nullptr);
 }
 
+extern "C" dx_status dx_moe_step_layers(dx_pool p, int32_t layer0, int32_t n_layers, const void* const* x, int32_t T,
+                                        const void* const* router_w, const float* const* router_bias,
+                                        const float* const* logits, void* const* y) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    DX_CHECK(n_layers >= 0 && layer0 >= 0 && layer0 + n_layers <= p->L, DX_ERR_RANGE, "layers [%d, %d) outside [0, %d)",
+             (int)layer0, (int)(layer0 + n_layers), p->L);
+    DX_CHECK(x && y && (router_w || logits), DX_ERR_INVALID_ARG, "null pointer array");
+    for (int i = 0; i < n_layers; ++i) {
+        dx_status st = dx_moe_step(p, layer0 + i, x[i], T, router_w ? router_w[i] : nullptr,
+                                   router_bias ? router_bias[i] : nullptr, logits ? logits[i] : nullptr, y[i], nullptr,
+                                   nullptr);
+        if (st != DX_OK) return st;
+    }
+    return DX_OK;
+}
+
 extern "C" dx_status dx_get_logits(dx_pool p, float* host_out, int64_t cap) {
     DX_CHECK(p && host_out, DX_ERR_INVALID_ARG, "null pool/out");
     DX_CHECK(p->last_logits_router, DX_ERR_NOT_READY, "the last forward was not in router mode");

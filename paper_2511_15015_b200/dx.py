@@ -86,6 +86,7 @@ _SIG = {
     "dx_pool_info": [_vp, _P(dx_info)],
     "dx_moe_forward": [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "dx_moe_step": [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "dx_moe_step_layers": [_vp, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     "dx_get_logits": [_vp, _vp, _i64],
     "dx_hotness_update": [_vp, _i32],
     "dx_hotness_update_from": [_vp, _i32, _vp, _vp, _i32],
@@ -224,6 +225,17 @@ class Pool:
                     topk_gate=None):
         _check(_lib.dx_moe_step(self.h, layer, _ptr(x), T, _ptr(router_w), _ptr(router_bias), _ptr(logits),
                                 _ptr(y), _ptr(topk_idx), _ptr(topk_gate)), "dx_moe_step")
+
+    @staticmethod
+    def ptr_array(ptrs):
+        """A C array of device pointers (ints / tensors) for dx_moe_step_layers; keep it alive across calls."""
+        return (ctypes.c_void_p * len(ptrs))(*[_ptr(q) for q in ptrs])
+
+    def dx_moe_step_layers(self, layer0, n_layers, x_arr, T, y_arr, router_w_arr=None, router_bias_arr=None,
+                           logits_arr=None):
+        """Arrays from Pool.ptr_array (one entry per layer)."""
+        _check(_lib.dx_moe_step_layers(self.h, layer0, n_layers, x_arr, T, router_w_arr, router_bias_arr, logits_arr,
+                                       y_arr), "dx_moe_step_layers")
 
     def dx_get_logits(self, T):
         import numpy as np
