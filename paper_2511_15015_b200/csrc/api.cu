@@ -797,7 +797,7 @@ static void route_tokens(dx_pool p, int layer, const void* x, int T, const void*
     launch_route(lg, T, p->E, p->k, p->e_lo, ws, p->ctrl.cnt + base, p->ctrl.mass + base, p->ctrl.tier + base,
                  p->wbytes, p->cs);
     launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, Xp, p->cs);
-    p->launches += 2;
+    p->launches += 3;
 }
 
 static dx_status ep_forward(dx_pool p, int layer, const void* x, int T, const void* router_w, const float* router_bias,
@@ -988,7 +988,7 @@ static dx_status ep_dispatch_impl(dx_pool p, int32_t layer, const void* x, int32
     // rows sorted by global expert = grouped by owner rank: the placement IS the send buffer
     launch_place(T, p->E, p->k, ws, (const __nv_bfloat16*)x, p->H, (__nv_bfloat16*)send_rows, p->cs);
     launch_ep_meta(ws, T * p->k, p->E_loc, p->cfg.ep_size, (int2*)send_meta, send_counts, (int2*)send_pairs, T, p->cs);
-    p->launches += 3;
+    p->launches += 4;
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "dispatch launch failed: %s", cudaGetErrorString(ce));
     return DX_OK;
@@ -1021,7 +1021,7 @@ static dx_status routed_impl(dx_pool p, int32_t layer, const void* rows, int32_t
     launch_route_given((const int2*)meta, R, p->E_loc, ws, p->ctrl.cnt + base, p->ctrl.mass + base,
                        p->ctrl.tier + base, p->wbytes, p->dev_err, p->cs);
     launch_place(R, p->E_loc, 1, ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
-    p->launches += 2;
+    p->launches += 3;
     // an expert receives at most one row per token of the step: m_e <= min(R, tokens_global)
     return expert_ffn(p, layer, ws, rows, R, 1, y_rows, ev, false,
                       (int)std::min<int64_t>(R, tokens_global > 0 ? tokens_global : R));

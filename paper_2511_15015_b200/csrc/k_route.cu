@@ -75,6 +75,99 @@ __global__ void __launch_bounds__(512) k_router(const __nv_bfloat16* __restrict_
     }
 }
 
+// Router for larger T (prefill): a tiled tensor-core GEMM logits[T][E] = x[T][H] W_r[E][H]^T (+ b).  Block tile
+// 64 tokens x 128 experts, K in chunks of 64 staged through shared memory by cp.async (double-buffered; 16-byte
+// units XOR-swizzled by row so the ldmatrix row groups hit distinct banks), 8 warps
+// of 32 tokens x 32 experts (2 x 4 mma.sync m16n8k16 tiles, fragments by ldmatrix).  Each logit is one warp's
+// fp32 accumulation in K order: deterministic.  x is read once, W_r once per 64-token tile (from L2).
+constexpr int RT_M = 64, RT_N = 128, RT_K = 64, RT_LD = RT_K;   // rows of 8 16-byte units, unit c at c ^ (row & 7)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(pred ? 16 : 0));
+}
+__global__ void __launch_bounds__(256) k_router_tiled(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wr,
+                                                      const float* __restrict__ bias, int T, int E, int H,
+                                                      float* __restrict__ logits) {
+    __shared__ __align__(16) __nv_bfloat16 xs[2][RT_M][RT_LD];
+    __shared__ __align__(16) __nv_bfloat16 ws[2][RT_N][RT_LD];
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t0 = blockIdx.x * RT_M, e0 = blockIdx.y * RT_N;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;        // warp tile origin in the block tile
+    auto stage = [&](int buf, int k0) {
+        // x: 64 rows x 8 16-byte units; W_r: 128 rows x 8 units -> 1536 units over 256 threads
+        for (int u = tid; u < (RT_M + RT_N) * 8; u += 256) {
+            const int row = u >> 3, c = u & 7;
+            if (row < RT_M) {
+                const int t = t0 + row;
+                cp_async16((uint32_t)__cvta_generic_to_shared(&xs[buf][row][(c ^ (row & 7)) * 8]),
+                           x + (size_t)min(t, T - 1) * H + k0 + c * 8, t < T);
+            } else {
+                const int e = e0 + row - RT_M;
+                const int wrow = row - RT_M;
+                cp_async16((uint32_t)__cvta_generic_to_shared(&ws[buf][wrow][(c ^ (wrow & 7)) * 8]),
+                           wr + (size_t)min(e, E - 1) * H + k0 + c * 8, e < E);
+            }
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    float acc[2][4][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0f;
+    const int nk = H / RT_K;
+    stage(0, 0);
+    for (int kc = 0; kc < nk; ++kc) {
+        const int buf = kc & 1;
+        if (kc + 1 < nk) {
+            stage(buf ^ 1, (kc + 1) * RT_K);
+            asm volatile("cp.async.wait_group 1;");
+        } else {
+            asm volatile("cp.async.wait_group 0;");
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < RT_K; ks += 16) {
+            uint32_t a[2][4], b[4][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {                   // A 16x16: rows wm+16i.., ldmatrix.x4
+                const int r = wm + 16 * i + (lane & 15), cu = (ks >> 3) + (lane >> 4);
+                const uint32_t ad = (uint32_t)__cvta_generic_to_shared(&xs[buf][r][(cu ^ (r & 7)) * 8]);
+                asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(a[i][0]), "=r"(a[i][1]), "=r"(a[i][2]), "=r"(a[i][3]) : "r"(ad));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {                   // B 16x8 from W_r rows (K contiguous), ldmatrix.x2
+                const int r = wn + 8 * j + (lane & 7), cu = (ks >> 3) + ((lane >> 3) & 1);
+                const uint32_t ad = (uint32_t)__cvta_generic_to_shared(&ws[buf][r][(cu ^ (r & 7)) * 8]);
+                asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(b[j][0]), "=r"(b[j][1]) : "r"(ad));
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) mma16816(acc[i][j], a[i][0], a[i][1], a[i][2], a[i][3], b[j][0], b[j][1]);
+        }
+        __syncthreads();
+    }
+    const int g = lane >> 2, q = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = t0 + wm + 16 * i + g + 8 * h;
+                const int e = e0 + wn + 8 * j + 2 * q;
+                if (t < T) {
+                    if (e < E) logits[(size_t)t * E + e] = bias ? acc[i][j][2 * h] + bias[e] : acc[i][j][2 * h];
+                    if (e + 1 < E) logits[(size_t)t * E + e + 1] = bias ? acc[i][j][2 * h + 1] + bias[e + 1] : acc[i][j][2 * h + 1];
+                }
+            }
+}
+
 __device__ __forceinline__ bool better(float a, int ea, float b, int eb) {
     return a > b || (a == b && ea < eb);
 }
@@ -124,9 +217,7 @@ __device__ __forceinline__ void topk_warp(const float (&v)[NVT], uint32_t taken,
 // atomic per touched expert.
 template <typename Tv>
 __device__ Tv block_excl_scan(Tv v, Tv* tmp, Tv* total);
-__device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int32_t* __restrict__ base,
-                          int32_t* __restrict__ off, int32_t* __restrict__ act_e, int32_t* __restrict__ n_act,
-                          const RouteStats& rs);
+
 
 template <int NVT>
 __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits, int T, int E, int k,
@@ -181,23 +272,13 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
     }
     __syncthreads();
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        hist[(size_t)blockIdx.x * E + e] = (int32_t)cnt_s[e];
+        hist[(size_t)e * gridDim.x + blockIdx.x] = (int32_t)cnt_s[e];     // [expert][route block]
         const int le = e - e_lo;
         if (cnt_s[e] && le >= 0 && le < e_cnt && cnt_acc) {
             atomicAdd(&cnt_acc[le], cnt_s[e]);
             atomicAdd(&mass_acc[le], mass_s[e]);
         }
     }
-    // the last block to finish runs the offset scan (a4) for the whole forward
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    scan_tail(hist, gridDim.x, E, base, off, act_e, n_act, rs);
-    if (threadIdx.x == 0) *done = 0;
 }
 
 // ------------------------------------------------------------------ a1-a4 in ONE launch (decode batches)
@@ -467,84 +548,87 @@ __device__ Tv block_excl_scan(Tv v, Tv* tmp /*[32]*/, Tv* total) {
     return before;
 }
 
-// Offsets of every expert's row segment, per-route-block bases and the active-expert list.  Run by
-// the LAST route block to finish (threadfence + completion counter), so routing and its scan are one
-// launch.  256 threads, 2 experts per thread (E <= 512).
-__device__ void scan_tail(const int32_t* __restrict__ hist, int nblk, int E, int32_t* __restrict__ base,
-                          int32_t* __restrict__ off, int32_t* __restrict__ act_e, int32_t* __restrict__ n_act,
-                          const RouteStats& rs) {
+// a4 offsets, parallel over experts: block e scans expert e's per-route-block counts hist[e][0..nblk) into
+// base[e][b] (rows of expert e in earlier route blocks) and its total; the last block to finish (completion
+// counter) turns the totals into off[] (exclusive scan), the active-expert list (HIGH tier first: the grouped
+// GEMMs hand out work items in this order, heaviest first) and the profiling byte counters.
+__global__ void __launch_bounds__(256) k_scan_e(const int32_t* __restrict__ hist, int nblk, int E,
+                                                int32_t* __restrict__ base, int32_t* __restrict__ off,
+                                                int32_t* __restrict__ act_e, int32_t* __restrict__ n_act, RouteStats rs,
+                                                unsigned* __restrict__ done) {
     __shared__ int32_t tmp[32];
-    __shared__ int32_t total_s, na_s;
-    const int e0 = 2 * threadIdx.x, e1 = e0 + 1;
-    int32_t t0 = 0, t1 = 0;
-    for (int b = 0; b < nblk; ++b) {
-        if (e0 < E) t0 += __ldcg(hist + (size_t)b * E + e0);
-        if (e1 < E) t1 += __ldcg(hist + (size_t)b * E + e1);
+    __shared__ int32_t total_s, na_s, nhi_s;
+    __shared__ bool last;
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int e = blockIdx.x;
+    int32_t run = 0;
+    for (int b0 = 0; b0 < nblk; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        const int32_t v = b < nblk ? __ldcg(hist + (size_t)e * nblk + b) : 0;
+        const int32_t x = block_excl_scan<int32_t>(v, tmp, &total_s);
+        if (b < nblk) base[(size_t)e * nblk + b] = run + x;
+        run += total_s;
     }
+    if (threadIdx.x == 0) off[e] = run;                     // this expert's total, scanned below
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // E <= 512: two experts per thread
+    const int e0 = 2 * threadIdx.x, e1 = e0 + 1;
+    const int32_t t0 = e0 < E ? __ldcg(off + e0) : 0, t1 = e1 < E ? __ldcg(off + e1) : 0;
     const int32_t o = block_excl_scan<int32_t>(t0 + t1, tmp, &total_s);
     const int32_t a = block_excl_scan<int32_t>((t0 > 0) + (t1 > 0), tmp, &na_s);
-    // active list HIGH tier first (the grouped GEMMs hand out work items in this order, heaviest first)
-    __shared__ int32_t nhi_s;
     const bool h0 = e0 < E && t0 > 0 && rs.tier && rs.tier[e0], h1 = e1 < E && t1 > 0 && rs.tier && rs.tier[e1];
     const int32_t ah = block_excl_scan<int32_t>((int32_t)h0 + (int32_t)h1, tmp, &nhi_s);
     int32_t ahi = ah, alo = nhi_s + (a - ah);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int e = h ? e1 : e0;
-        const int32_t tot = h ? t1 : t0;
-        if (e >= E) continue;
-        const int32_t oe = h ? o + t0 : o;
-        off[e] = oe;
-        if (tot > 0) act_e[(h ? h1 : h0) ? ahi++ : alo++] = e;
-        int32_t run = oe;
-        for (int b = 0; b < nblk; ++b) {
-            base[(size_t)b * E + e] = run;
-            run += __ldcg(hist + (size_t)b * E + e);
-        }
+    if (e0 < E) {
+        off[e0] = o;
+        if (t0 > 0) act_e[h0 ? ahi++ : alo++] = e0;
     }
-    if (rs.stats && rs.tier) {                  // algorithmic weight bytes of this forward (profiling)
-        if (threadIdx.x == 0) {
-            const u64 nh = (u64)nhi_s, nl = (u64)na_s - nh;
-            atomicAdd(&rs.stats[0], nh * rs.b10 + nl * rs.b00);
-            atomicAdd(&rs.stats[1], nh * rs.b11 + nl * rs.b01);
-            atomicAdd(&rs.stats[2], (u64)na_s);
-        }
+    if (e1 < E) {
+        off[e1] = o + t0;
+        if (t1 > 0) act_e[h1 ? ahi++ : alo++] = e1;
     }
-    if (threadIdx.x == 0) { off[E] = total_s; *n_act = na_s; }
+    if (rs.stats && rs.tier && threadIdx.x == 0) {          // algorithmic weight bytes of this forward (profiling)
+        const u64 nh = (u64)nhi_s, nl = (u64)na_s - nh;
+        atomicAdd(&rs.stats[0], nh * rs.b10 + nl * rs.b00);
+        atomicAdd(&rs.stats[1], nh * rs.b11 + nl * rs.b01);
+        atomicAdd(&rs.stats[2], (u64)na_s);
+    }
+    if (threadIdx.x == 0) { off[E] = total_s; *n_act = na_s; *done = 0; }
 }
 
-// One block per entry (t*k + j): its row position = base[block][e] + number of earlier entries of the
-// same expert inside its route block (the stable counting-sort order: t asc, j asc); the block then
-// copies x[t] into Xp[pos] (the B operand of the gate/up GEMM) when Xp != NULL.
-__global__ void __launch_bounds__(128) k_place(const int32_t* __restrict__ idx, int T, int E, int k,
-                                               const int32_t* __restrict__ base, int32_t* __restrict__ perm,
-                                               int32_t* __restrict__ inv, const __nv_bfloat16* __restrict__ x,
-                                               int H, __nv_bfloat16* __restrict__ Xp) {
-    __shared__ int pos_s;
+// One warp per entry (t*k + j): its row position = off[e] + rows of expert e in earlier route blocks
+// (base[e][block]) + earlier entries of the same expert inside its route block -- the stable counting-sort
+// order (t asc, j asc); the warp then copies x[t] into Xp[pos] (the B operand of the gate/up GEMM) when Xp != NULL.
+__global__ void __launch_bounds__(256) k_place(const int32_t* __restrict__ idx, int n, int nblk, int k,
+                                               const int32_t* __restrict__ base, const int32_t* __restrict__ off,
+                                               int32_t* __restrict__ perm, int32_t* __restrict__ inv,
+                                               const __nv_bfloat16* __restrict__ x, int H, __nv_bfloat16* __restrict__ Xp) {
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
-    const int i = blockIdx.x;
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        const int b = (i / k) / ROUTE_TOK_PER_BLK;
-        const int e = idx[i];
-        int r = 0;
-        for (int q = b * ROUTE_TOK_PER_BLK * k + lane; q < i; q += 32) r += (idx[q] == e);
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n) return;
+    const int b = (i / k) / ROUTE_TOK_PER_BLK;
+    const int e = __ldcg(idx + i);
+    int r = 0;
+    for (int q = b * ROUTE_TOK_PER_BLK * k + lane; q < i; q += 32) r += (__ldcg(idx + q) == e);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        if (lane == 0) {
-            const int pos = base[(size_t)b * E + e] + r;
-            perm[pos] = i;
-            inv[i] = pos;
-            pos_s = pos;
-        }
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    const int pos = __ldcg(off + e) + __ldcg(base + (size_t)e * nblk + b) + r;
+    if (lane == 0) {
+        perm[pos] = i;
+        inv[i] = pos;
     }
     if (!Xp) return;
-    __syncthreads();
-    const int pos = pos_s;
-    const __nv_bfloat16* src = x + (size_t)(i / k) * H;
-    for (int h = threadIdx.x * 8; h < H; h += blockDim.x * 8)
-        *reinterpret_cast<uint4*>(Xp + (size_t)pos * H + h) = *reinterpret_cast<const uint4*>(src + h);
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(i / k) * H);
+    uint4* dst = reinterpret_cast<uint4*>(Xp + (size_t)pos * H);
+    for (int h = lane; h < H / 8; h += 32) dst[h] = __ldg(src + h);
 }
 
 // ------------------------------------------------------------------ a8: y_t = bf16(sum_j Y[t,j])
@@ -625,21 +709,12 @@ __global__ void __launch_bounds__(256) k_route_given(const int2* __restrict__ me
     }
     __syncthreads();
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        hist[(size_t)blockIdx.x * E + e] = (int32_t)cnt_s[e];
+        hist[(size_t)e * gridDim.x + blockIdx.x] = (int32_t)cnt_s[e];     // [expert][route block]
         if (cnt_s[e] && cnt_acc) {
             atomicAdd(&cnt_acc[e], cnt_s[e]);
             atomicAdd(&mass_acc[e], mass_s[e]);
         }
     }
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    scan_tail(hist, gridDim.x, E, base, off, act_e, n_act, rs);
-    if (threadIdx.x == 0) *done = 0;
 }
 
 // Source side after placement: metadata of every dispatched row (local expert id at its owner, gate
@@ -688,9 +763,16 @@ int route_blocks(int T) { return (T + ROUTE_TOK_PER_BLK - 1) / ROUTE_TOK_PER_BLK
 void launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, int T, int E, int H,
                    float* logits, cudaStream_t st) {
     if (T <= 0) return;
+    if (T >= 128 && H % RT_K == 0) {               // prefill-sized batches: the tiled GEMM
+        dim3 grid((T + RT_M - 1) / RT_M, (E + RT_N - 1) / RT_N);
+        dx_launch(k_router_tiled, grid, dim3(256), 0, st, g_dx_pdl, x, wr, bias, T, E, H, logits);
+        return;
+    }
     dim3 grid((E + 7) / 8, (T + 15) / 16);
     dx_launch(k_router, grid, dim3(512), 0, st, g_dx_pdl, x, wr, bias, T, E, H, logits);
 }
+
+static void launch_scan_e(int nblk, int E, const RouteWs& ws, const RouteStats& rs, cudaStream_t st);
 
 void launch_route(const float* logits, int T, int E, int k, int e_lo, const RouteWs& ws,
                   uint32_t* cnt_acc, u64* mass_acc, const int32_t* tier, const u64 (&bytes)[2][2], cudaStream_t st) {
@@ -703,6 +785,7 @@ void launch_route(const float* logits, int T, int E, int k, int e_lo, const Rout
     else if (E <= 256) dx_launch(k_route<8>, dim3(nb), dim3(256), 0, st, g_dx_pdl, DX_ROUTE_ARGS);
     else               dx_launch(k_route<16>, dim3(nb), dim3(256), 0, st, g_dx_pdl, DX_ROUTE_ARGS);
 #undef DX_ROUTE_ARGS
+    launch_scan_e(nb, E, ws, rs, st);
 }
 
 bool route_dec_ok(int T, int E, int k) {
@@ -744,8 +827,14 @@ void launch_route_dec(const __nv_bfloat16* x, const __nv_bfloat16* wr, const flo
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
                   cudaStream_t st) {
     if (T <= 0) return;
-    dx_launch(k_place, dim3(T * k), dim3(128), 0, st, g_dx_pdl, (const int32_t*)ws.idx, T, E, k,
-              (const int32_t*)ws.base, ws.perm, ws.inv, x, H, Xp);
+    const int n = T * k;
+    dx_launch(k_place, dim3((n + 7) / 8), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.idx, n, route_blocks(T), k,
+              (const int32_t*)ws.base, (const int32_t*)ws.off, ws.perm, ws.inv, x, H, Xp);
+}
+
+static void launch_scan_e(int nblk, int E, const RouteWs& ws, const RouteStats& rs, cudaStream_t st) {
+    dx_launch(k_scan_e, dim3(E), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.hist, nblk, E, ws.base, ws.off,
+              ws.act_e, ws.n_act, rs, ws.done);
 }
 
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st,
@@ -769,6 +858,7 @@ void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint3
     RouteStats rs{tier, bytes[0][0], bytes[0][1], bytes[1][0], bytes[1][1], ws.stats};
     dx_launch(k_route_given, dim3(route_blocks(R)), dim3(256), 0, st, g_dx_pdl, meta, R, E, ws.idx, ws.gate, ws.hist,
               cnt_acc, mass_acc, ws.base, ws.off, ws.act_e, ws.n_act, rs, ws.done, err);
+    launch_scan_e(route_blocks(R), E, ws, rs, st);
 }
 
 void launch_ep_meta(const RouteWs& ws, int n, int E_loc, int G, int2* meta, int32_t* counts, int2* pairs, int T_src,

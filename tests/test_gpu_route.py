@@ -1,7 +1,8 @@
 """GPU parity of the routing steps on the benched path (router mode, fused decode routing kernel) and their
 edge cases, through the C ABI, against the CPU oracle.
 
-- a1 router logits: the GPU's fp32 logits (dx_get_logits = exactly what its top-k consumed) against the fp64
+- a1 router logits (the fused decode kernel for T*k <= 512, the tiled prefill router otherwise): the GPU's fp32
+  logits (dx_get_logits = exactly what its top-k consumed) against the fp64
   oracle (or_router_logits) element by element, within the fp32 summation bound gamma_n * sum|x w| (n = H),
   and row-wise max |d| / max |ref| <= 1e-3, at C2 / Q80B sizes.
 - a2-a8 in router mode: the oracle routes the GPU's own logits; idx / gates / counters bit-exact, y <= 2e-2.
@@ -45,7 +46,8 @@ def _shape(name):
     return dict(E=512, k=10, H=2048, I=512, g=128, hb=4, lb=2)
 
 
-@pytest.mark.parametrize("shape,T", [("q30b", 64), ("q30b", 1), ("q30b", 37), ("q80b", 51), ("q80b", 64)])
+@pytest.mark.parametrize("shape,T", [("q30b", 64), ("q30b", 1), ("q30b", 37), ("q80b", 51), ("q80b", 64),
+                                     ("q30b", 300), ("q80b", 200)])
 def test_router_mode_logits_and_layer(dx, shape, T):
     s = _shape(shape)
     E, k, H, I, g, hb, lb = s["E"], s["k"], s["H"], s["I"], s["g"], s["hb"], s["lb"]
