@@ -20,9 +20,9 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-2
 C2 = dict(L=48, E=128, k=8, H=2048, I=768, g=128, high=16, low=4, budget=24 * 10**9, s=1, alpha=0.95, Tp=16,
           W=32, dwell=16, lag=4, B=64, zipf=1.2, drift=32, frac=0.25, n_top=24)
-LAYERS = (0, 47)              # sampled layers
-Y_STEPS = (31, 48, 53)        # warm-up (all LOW), the plan step (old tiers), after publication (new tiers)
-TOKENS = (0, 21, 63)          # sampled token rows
+LAYERS = (0, 23, 47)          # sampled layers
+Y_STEPS = (31, 40, 48, 53, 55)   # warm-up (all LOW), finalized, the plan step (old tiers), after publication
+TOKENS = (0, 9, 21, 38, 50, 63)  # sampled token rows
 
 
 @pytest.fixture(scope="module")
@@ -94,3 +94,40 @@ def test_c2_stack_sampled_parity(dx):
     assert all(v > 0 for v in n_trans.values()), n_trans
     print(f"C2 stack: transitions at sampled layers {n_trans}, worst sampled rel err {worst:.3e}")
     pool.close()
+
+
+def test_c2_stack_layers_entry_matches_per_layer_calls(dx):
+    """The bench's entry point -- dx_moe_step_layers over the 48 layers in router mode -- against
+    48 separate dx_moe_step calls on a second pool fed the same steps: every layer's output, every step, bitwise,
+    and the controller state (scores and tables) of every layer at the end, through warm-up, finalize and a plan
+    period with copy-engine promotions."""
+    p = C2
+    L, E, k, H, I, g, B = p["L"], p["E"], p["k"], p["H"], p["I"], p["g"], p["B"]
+    m = Masters(4, L, E, H, I)
+    cfg = make_cfg(dx, L, E, k, H, I, g, p["high"], p["low"], p["budget"], p["s"], p["alpha"], p["Tp"], p["W"],
+                   p["dwell"], p["lag"], B)
+    pa = dx.Pool(cfg, m.ptrs(), torch.cuda.current_stream())
+    pb = dx.Pool(cfg, m.ptrs(), torch.cuda.current_stream())
+    wr = torch.stack([bf16_dev(synth.router_bf16(4, l, E, H)) for l in range(L)])
+    bias = torch.stack([torch.from_numpy(synth.zipf_logp(synth.rank_perm(4, l, 0, E, 24, 0.25), 1.2)) for l in range(L)]).cuda()
+    ya = torch.zeros(L, B, H, dtype=torch.bfloat16, device="cuda")
+    yb = torch.zeros(L, B, H, dtype=torch.bfloat16, device="cuda")
+    P = dx.Pool.ptr_array
+    y_arr, wr_arr, b_arr = P([ya[l] for l in range(L)]), P([wr[l] for l in range(L)]), P([bias[l] for l in range(L)])
+    for step in range(p["W"] + 22):
+        x = bf16_dev(synth.normal_bf16(4, 7, step, 0, (B, H)))
+        pa.dx_moe_step_layers(0, L, P([x] * L), B, y_arr, router_w_arr=wr_arr, router_bias_arr=b_arr)
+        for l in range(L):
+            pb.dx_moe_step(l, x, B, yb[l], router_w=wr[l], router_bias=bias[l])
+        assert torch.equal(ya.view(torch.int16), yb.view(torch.int16)), step
+    pa.dx_sync()
+    pb.dx_sync()
+    for l in range(L):
+        ha, hb = pa.dx_get_hotness(l), pb.dx_get_hotness(l)
+        assert np.array_equal(ha["S"].view(np.uint64), hb["S"].view(np.uint64)), l
+        ta, tb = pa.dx_get_table(l), pb.dx_get_table(l)
+        for key in ("tier", "slot", "version"):
+            assert np.array_equal(ta[key], tb[key]), (l, key)
+    assert int(sum(pa.dx_get_table(l)["version"].sum() for l in range(L))) > 0      # transitions happened
+    pa.close()
+    pb.close()
