@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-q80b", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent full replicas instead of EP")
     ap.add_argument("--no-teleport", action="store_true", help="skip the zero-cost-transition replay (switch cost)")
+    ap.add_argument("--no-prefetch-leg", action="store_true", help="skip the f-1 cross-layer prefetch measurement")
     ap.add_argument("--per-layer-calls", action="store_true", help="one dx_moe_step call per layer instead of "
                     "dx_moe_step_layers per stack step")
     ap.add_argument("--ep-loopback", action="store_true",
@@ -493,6 +494,8 @@ def run_ours(a, rank, world, local_rank):
     if a.prefill_tokens > 0:
         out["extra"]["prefill"] = prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream)
     pool.close()
+    if not ep_mode and not a.no_prefetch_leg:
+        out["extra"]["prefetch"] = prefetch_leg(a, ptrs, L, E, k, H, I, g, c, dev, stream)
     if not ep_mode and not a.no_teleport:
         ms_tel = teleport_replay()
         sw = out["extra"]["switch"]
@@ -504,6 +507,70 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
     del arr
     return out
+
+
+def prefetch_leg(a, ptrs, L_all, E, k, H, I, g, c, dev, stream, L=8):
+    """f-1: an 8-layer C2-shaped stack (the first 8 layers' masters, C2's per-layer
+    budget -> n_hot 24) in trace mode with cross-layer-coupled routing (synth.coupled_trace_logits: layer l boosts
+    pi_l of layer l-1's choices; Zipf(1.2) with a quarter of the top-24 set drifting every 16 steps), B = 64,
+    Tp=16, L=4, run from fresh pools on identical inputs: cross-layer prefetch off, then on with fan-out 1 and 2
+    (lead 4).  Per run over the last 48 steps (3 plan periods): promotions, prefetch hits, mean side-stream switch
+    time per plan (issue -> ready), copy-engine bytes per plan and the device ms per step."""
+    import torch
+    import synth
+    from paper_2511_15015_b200 import dx
+    B, Tp, W, lag, steps_timed = 64, 16, 32, 4, 48
+    total = W + 8 + steps_timed
+    lgs = torch.empty(total, L, B, E, dtype=torch.float32, device=dev)
+    for s_ in range(total):
+        ls = synth.coupled_trace_logits(a.seed + 7, L, s_, B, E, k, 6.0, 1.2, 16, 0.25, 24)
+        for l in range(L):
+            lgs[s_, l].copy_(torch.from_numpy(ls[l]))
+    xs = torch.from_numpy(synth.normal_bf16(a.seed, 950, 0, 0, (2, B, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+    y = torch.empty(L, B, H, dtype=torch.bfloat16, device=dev)
+    res = {"workload": f"f-1: {L}-layer C2-shaped stack, trace mode with cross-layer coupled routing (boost 6 on "
+                       f"pi_l of layer l-1's top-{k}), drift 25 % of the top-24 set every 16 steps, B={B}, Tp={Tp}, "
+                       f"L={lag}; lead 4; last {steps_timed} steps"}
+    for mode, fan in (("off", 0), ("on_f1", 1), ("on_f2", 2)):
+        cfg = dx.dx_config()
+        cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = L, E, k, H, I, g
+        cfg.high_bits, cfg.low_bits = c["high"], c["low"]
+        cfg.expert_budget_bytes = c["budget"] * L // c["L"]
+        cfg.n_spare, cfg.ema_alpha = c["s"], c["alpha"]
+        cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = Tp, W, Tp, lag
+        cfg.max_tokens, cfg.ep_rank, cfg.ep_size = B, 0, 1
+        pool = dx.Pool(cfg, ptrs[:L * E], stream)
+        if fan:
+            pool.dx_set_prefetch(fan, 4)
+        P = pool.ptr_array
+        x_arr = [P([xs[i]] * L) for i in range(2)]
+        y_arr = P([y[l] for l in range(L)])
+
+        def st(s_):
+            pool.dx_moe_step_layers(0, L, x_arr[s_ & 1], B, y_arr, logits_arr=P([lgs[s_, l] for l in range(L)]))
+
+        for s_ in range(total - steps_timed):
+            st(s_)
+        pool.dx_sync()
+        pool.dx_profile_read()
+        pool.dx_profile_enable(PROF_EVERY)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s_ in range(total - steps_timed, total):
+            st(s_)
+        e1.record(stream)
+        pool.dx_sync()
+        ms = e0.elapsed_time(e1)
+        pr = pool.dx_profile_read()
+        pool.close()
+        res[mode] = {"ms_per_step": ms / steps_timed, "plans": pr["plans"], "promotions": pr["promotions"],
+                     "prefetch_issued": pr["prefetch_issued"], "prefetch_hits": pr["prefetch_hits"],
+                     "switch_ms_mean": pr["xfer_ms"] / max(pr["plans"], 1),
+                     "copy_mb_per_plan": pr["copy_bytes"] / max(pr["plans"], 1) / 1e6}
+    for m in ("on_f1", "on_f2"):
+        res[m]["hit_rate"] = res[m]["prefetch_hits"] / max(res[m]["promotions"], 1)
+    return res
 
 
 def q80b_leg(a, peak, L=8):

@@ -269,7 +269,24 @@ typedef struct {
     int64_t  promotions, demotions; /* transitions those plans issued */
     double   copy_ms;           /* summed side-stream time of the plans' copy-engine promotions (H2D) */
     uint64_t copy_bytes;        /* bytes those copies moved (copy_bytes / copy_ms = promotion bandwidth) */
+    int64_t  prefetch_issued;   /* f-1: HIGH images staged ahead of plans */
+    int64_t  prefetch_hits;     /* promotions whose image was already staged in their destination block */
 } dx_profile_t;
+/* f-1 cross-layer correlation prefetch.  fanout f in [0, 8] (0 = off), lead d in
+ * [1, Tp - L].  With f > 0 every dx_moe_forward / dx_moe_step of layer l (the stack called layer by layer on the
+ * same batch) adds, for each token, one count per pair (expert chosen at layer l-1, expert chosen at layer l) to
+ * the pair's correlation matrix corr[l-1][e][e'] (u32, device, SPEC update_correlation); d steps before layer
+ * l+1's next plan it scores every LOW, not-in-flight expert e' of layer l+1 by sum over layer l's current choices e
+ * of corr[l][e][e'] and stages the HIGH images of the top f (score desc, id asc) into the lowest free HIGH blocks on
+ * the copy engine (SPEC prefetch_candidates; the transient blocks are otherwise idle between plans).  A plan that
+ * then promotes a staged expert into its staged block skips the copy (dx_profile_t prefetch_hits).  Results are
+ * unchanged; only the promotion latency drops.  INVALID_ARG for EP pools. */
+dx_status dx_set_prefetch(dx_pool pool, int32_t fanout, int32_t lead);
+/* corr[layer][E_loc][E_loc] (the pair (layer, layer + 1)) into host memory; synchronising.  RANGE outside the stack. */
+dx_status dx_get_corr(dx_pool pool, int32_t layer, uint32_t* host_out);
+/* The layer's current prefetch: up to 8 {expert, HIGH block} pairs staged (or chosen and about to be) for its
+ * next plan; synchronising. */
+dx_status dx_get_prefetch(dx_pool pool, int32_t layer, int32_t* experts, int32_t* blocks, int32_t* n);
 /* TIMING BASELINE ONLY (SURVEY §8(d) C5 "teleport"): on != 0 makes runtime plans and their publication
  * happen exactly as scheduled but skips the side-stream transfers, so the per-step tier tables are the
  * same while switching costs nothing -- and the moved experts' weights are garbage.  The exposed switch

@@ -66,6 +66,8 @@ def _L():
         "or_ctrl_debug_set": ([vp, vp, vp, dbl, i64], None),
         "or_ledger_alloc": ([vp, i32, i32], i32),
         "or_ledger_free": ([vp, i32, i32, i32], i32),
+        "or_corr_update": ([vp, vp, vp, i32, i32, i32], None),
+        "or_prefetch_candidates": ([vp, vp, i32, i32, i32, vp, vp, vp, i32, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -279,3 +281,27 @@ def ledger_alloc(owner: np.ndarray, who: int) -> int:
 
 def ledger_free(owner: np.ndarray, slot: int, who: int) -> int:
     return _L().or_ledger_free(_p(owner), owner.size, slot, who)
+
+
+# ---------------------------------------------------------------- f-1 cross-layer correlation prefetch
+def corr_update(corr: np.ndarray, idx_a: np.ndarray, idx_b: np.ndarray):
+    """SPEC.md update_correlation on corr [E][E] (uint32, in place) from two layers' routing [T][k]."""
+    assert corr.dtype == np.uint32 and corr.flags.c_contiguous
+    a = np.ascontiguousarray(idx_a, dtype=np.int32)
+    b = np.ascontiguousarray(idx_b, dtype=np.int32)
+    T, k = a.shape
+    _L().or_corr_update(_p(corr), _p(a), _p(b), T, k, corr.shape[0])
+
+
+def prefetch_candidates(corr, idx, tier, in_flight, hi_owner, f):
+    """SPEC.md prefetch_candidates: list of (expert, HIGH block) for the next layer."""
+    corr = np.ascontiguousarray(corr, dtype=np.uint32)
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    tier = np.ascontiguousarray(tier, dtype=np.int32)
+    infl = np.ascontiguousarray(in_flight, dtype=np.int32)
+    own = np.ascontiguousarray(hi_owner, dtype=np.int32)
+    T, k = idx.shape
+    oe, ob = np.zeros(max(f, 1), np.int32), np.zeros(max(f, 1), np.int32)
+    n = _L().or_prefetch_candidates(_p(corr), _p(idx), T, k, corr.shape[0], _p(tier), _p(infl), _p(own), own.size, f,
+                                    _p(oe), _p(ob))
+    return list(zip(oe[:n].tolist(), ob[:n].tolist()))

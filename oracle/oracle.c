@@ -538,3 +538,49 @@ int32_t or_ctrl_owner(const or_ctrl* c, int32_t hi, int32_t slot) {
     if (hi) return (slot >= 0 && slot < c->cap_hi) ? c->hi_owner[slot] : -2;
     return (slot >= 0 && slot < c->cap_lo) ? c->lo_owner[slot] : -2;
 }
+
+/* ------------------------------------------------------------------ f-1 cross-layer correlation prefetch */
+/* update_correlation: for every token t and every pair of an expert a chosen at
+ * layer l (idx_a[t][j]) and an expert b chosen at layer l+1 (idx_b[t][j2]), corr[a][b] += 1: k*k increments
+ * per token. */
+void or_corr_update(uint32_t* corr, const int32_t* idx_a, const int32_t* idx_b, int32_t T, int32_t k, int32_t E) {
+    for (int32_t t = 0; t < T; ++t)
+        for (int32_t j = 0; j < k; ++j)
+            for (int32_t j2 = 0; j2 < k; ++j2) {
+                const int32_t a = idx_a[t * k + j], b = idx_b[t * k + j2];
+                corr[(int64_t)a * E + b] += 1u;
+            }
+}
+
+/* prefetch_candidates: up to f next-layer experts with the highest correlation to the current
+ * layer's activated experts -- score(e') = sum over the T*k chosen (t, j) of corr[idx[t][j]][e'] -- filtered to
+ * LOW-tier (tier 0) experts not in flight with score > 0, in (score desc, id asc) order; each paired with the next
+ * lowest free HIGH block (hi_owner[b] < 0, b < cap_hi) in ascending order, so at most min(f, free blocks).
+ * Returns the count. */
+int32_t or_prefetch_candidates(const uint32_t* corr, const int32_t* idx, int32_t T, int32_t k, int32_t E,
+                               const int32_t* tier, const int32_t* in_flight, const int32_t* hi_owner, int32_t cap_hi,
+                               int32_t f, int32_t* out_e, int32_t* out_b) {
+    uint64_t* score = (uint64_t*)calloc((size_t)E, sizeof(uint64_t));
+    int32_t* freeb = (int32_t*)malloc(sizeof(int32_t) * (size_t)(cap_hi > 0 ? cap_hi : 1));
+    int32_t nfree = 0;
+    for (int32_t b = 0; b < cap_hi; ++b)
+        if (hi_owner[b] < 0) freeb[nfree++] = b;
+    for (int32_t q = 0; q < T * k; ++q)
+        for (int32_t e = 0; e < E; ++e) score[e] += corr[(int64_t)idx[q] * E + e];
+    for (int32_t e = 0; e < E; ++e)
+        if (tier[e] != 0 || in_flight[e] != 0) score[e] = 0;
+    int32_t n = 0;
+    while (n < f && n < nfree) {
+        int32_t best = -1;
+        for (int32_t e = 0; e < E; ++e)            /* strictly greater: ties keep the lower id */
+            if (score[e] > 0 && (best < 0 || score[e] > score[best])) best = e;
+        if (best < 0) break;
+        out_e[n] = best;
+        out_b[n] = freeb[n];
+        score[best] = 0;
+        ++n;
+    }
+    free(score);
+    free(freeb);
+    return n;
+}

@@ -87,6 +87,12 @@ void     or_ctrl_debug_set(or_ctrl* c, const double* S, const int32_t* tier, dou
 int32_t or_ledger_alloc(int32_t* owner, int32_t cap, int32_t who);   /* lowest free, -1 exhausted */
 int32_t or_ledger_free(int32_t* owner, int32_t cap, int32_t slot, int32_t who); /* 0 ok, -1 corrupt */
 
+/* f-1 cross-layer correlation prefetch */
+void    or_corr_update(uint32_t* corr, const int32_t* idx_a, const int32_t* idx_b, int32_t T, int32_t k, int32_t E);
+int32_t or_prefetch_candidates(const uint32_t* corr, const int32_t* idx, int32_t T, int32_t k, int32_t E,
+                               const int32_t* tier, const int32_t* in_flight, const int32_t* hi_owner, int32_t cap_hi,
+                               int32_t f, int32_t* out_e, int32_t* out_b);
+
 #ifdef __cplusplus
 }
 #endif

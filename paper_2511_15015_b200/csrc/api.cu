@@ -101,6 +101,20 @@ struct dx_pool_s {
     int32_t* ep_pairs = nullptr;            // device [2][G] int2: my {count, T} per peer | received per peer
     int32_t* ep_pairs_host = nullptr;       // pinned mirror (the v1 host synchronisation point)
     u64 copy_promotions = 0;                // promotions issued as copy-engine H2D copies
+    // f-1 cross-layer correlation prefetch (dx_set_prefetch): device counts per layer pair, the last routing of
+    // each layer parity, candidates staged into free HIGH blocks ahead of the plan
+    uint32_t* corr = nullptr;               // [L-1][E][E]
+    int32_t* idx_last = nullptr;            // [2][max_tokens * k]
+    int T_last[2] = {-1, -1};
+    int pf_f = 0, pf_lead = 0;
+    int4* pf_dev = nullptr;                 // [L][8]
+    int32_t* pf_n_dev = nullptr;            // [L]
+    int4* pf_host = nullptr;                // pinned mirror
+    int32_t* pf_n_host = nullptr;
+    std::vector<cudaEvent_t> ev_pf;
+    std::vector<int> pf_pending;
+    std::vector<std::vector<int2>> staged;  // per layer: {expert, block} copies issued for the coming plan
+    u64 pf_issued = 0, pf_hits = 0;
     bool teleport = false;                  // timing baseline: plans and publications without the transfers
     // runtime plans reach the host through pinned memory; the host then issues the promotions' H2D copies on the
     // copy engine (cudaMemcpyAsync on the side stream) and the demotion kernel -- as soon as the plan is seen
@@ -376,7 +390,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
                     (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
     if (nccl_id) // NCCL exchange buffers: send / back rows (T*k), receive / result rows (n_ent), metadata, counts
         ws_bytes += (size_t)T * k * (2 * p->H * 2 + 8) + n_ent * (2 * p->H * 2 + 8) + (size_t)G * 16 + 6 * 256;
-    const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048;
+    const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048 +
+                               (size_t)(L > 1 ? L - 1 : 0) * E * E * 4 + (size_t)2 * T * k * 4 + (size_t)L * (8 * 16 + 4) + 4 * 256;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
     const size_t total = (size_t)L * p->layer_bytes + ctrl_bytes + ws_bytes + stage_bytes + ptr_bytes + 4096;
     cudaError_t ce = cudaMalloc(&p->arena, total);
@@ -462,6 +477,10 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     p->gemm_sched = carve<int32_t>(q, 4);
     p->manual_cmds = carve<int2>(q, 1024);
     p->manual_status = carve<int32_t>(q, 1024);
+    p->corr = carve<uint32_t>(q, (size_t)(L > 1 ? L - 1 : 0) * E * E);
+    p->idx_last = carve<int32_t>(q, (size_t)2 * T * k);
+    p->pf_dev = carve<int4>(q, (size_t)L * 8);
+    p->pf_n_dev = carve<int32_t>(q, (size_t)L);
     uint8_t* stage_master = carve<uint8_t>(q, (size_t)3 * p->I * p->H * 2);
     uint8_t* stage_high = carve<uint8_t>(q, (size_t)p->hi.bytes);
     p->hi_img_dev = carve<const uint8_t*>(q, (size_t)L * E);
@@ -503,6 +522,15 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         dx_pool_destroy(p);
         return code;
     };
+    p->ev_pf.resize(L);
+    for (int l = 0; l < L; ++l) cudaEventCreateWithFlags(&p->ev_pf[l], cudaEventDisableTiming);
+    p->pf_pending.assign(L, 0);
+    p->staged.assign(L, {});
+    if (cudaHostAlloc((void**)&p->pf_host, (size_t)L * 8 * sizeof(int4), cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc((void**)&p->pf_n_host, (size_t)L * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
+        dx_set_error("cudaHostAlloc(prefetch mirror) failed");
+        return fail(DX_ERR_OOM);
+    }
     if (cudaHostAlloc((void**)&p->plan_host, (size_t)L * E * sizeof(int4), cudaHostAllocDefault) != cudaSuccess ||
         cudaHostAlloc((void**)&p->plan_n_host, (size_t)L * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
         dx_set_error("cudaHostAlloc(plan mirror) failed");
@@ -577,11 +605,12 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
         DX_CUDA(cudaMemsetAsync(w.done, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(w.gbar, 0, 8, p->cs));
-        if (G > 1) {
+        if (p->ws_src.done) {                                // dispatch-side workspace (EP, loopback included)
             DX_CUDA(cudaMemsetAsync(p->ws_src.done, 0, 4, p->cs));
             DX_CUDA(cudaMemsetAsync(p->ws_src.gbar, 0, 8, p->cs));
         }
         DX_CUDA(cudaMemsetAsync(c.tstats, 0, 16, p->cs));
+        if (p->L > 1) DX_CUDA(cudaMemsetAsync(p->corr, 0, (size_t)(p->L - 1) * p->E_loc * p->E_loc * 4, p->cs));
         DX_CUDA(cudaStreamSynchronize(p->cs));
     }
     for (int ti = 0; ti < 2; ++ti) {
@@ -665,6 +694,9 @@ extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (p->comm) ep_nccl_destroy(p->comm);
     if (p->ep_pairs_host) cudaFreeHost(p->ep_pairs_host);
     for (auto ev : p->ev_planh) cudaEventDestroy(ev);
+    for (auto ev : p->ev_pf) cudaEventDestroy(ev);
+    if (p->pf_host) cudaFreeHost(p->pf_host);
+    if (p->pf_n_host) cudaFreeHost(p->pf_n_host);
     if (p->ss2) { cudaStreamSynchronize(p->ss2); cudaStreamDestroy(p->ss2); }
     if (p->ev_dem) cudaEventDestroy(p->ev_dem);
     for (auto ev : p->prof_copy_ev) cudaEventDestroy(ev);
@@ -678,6 +710,45 @@ extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (p->hi_cache) cudaFreeHost(p->hi_cache);
     if (p->arena) cudaFree(p->arena);
     delete p;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_set_prefetch(dx_pool p, int32_t fanout, int32_t lead) {
+    DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    DX_CHECK(fanout >= 0 && fanout <= 8, DX_ERR_INVALID_ARG, "fanout %d outside [0, 8]", (int)fanout);
+    DX_CHECK(fanout == 0 || (lead >= 1 && lead <= p->cfg.period - p->cfg.publish_lag), DX_ERR_INVALID_ARG,
+             "lead %d outside [1, Tp - L = %d]", (int)lead, p->cfg.period - p->cfg.publish_lag);
+    DX_CHECK(fanout == 0 || (p->cfg.ep_size == 1 && !p->comm), DX_ERR_INVALID_ARG,
+             "prefetch needs the whole stack on one GPU (ep_size 1)");
+    p->pf_f = fanout;
+    p->pf_lead = lead;
+    p->T_last[0] = p->T_last[1] = -1;
+    return DX_OK;
+}
+
+extern "C" dx_status dx_get_corr(dx_pool p, int32_t layer, uint32_t* host_out) {
+    DX_CHECK(p && host_out, DX_ERR_INVALID_ARG, "null pool/out");
+    DX_CHECK(layer >= 0 && layer + 1 < p->L, DX_ERR_RANGE, "layer pair (%d, %d) outside the stack", (int)layer,
+             (int)layer + 1);
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    DX_CUDA(cudaMemcpy(host_out, p->corr + (size_t)layer * p->E_loc * p->E_loc, (size_t)p->E_loc * p->E_loc * 4,
+                       cudaMemcpyDeviceToHost));
+    return DX_OK;
+}
+
+extern "C" dx_status dx_get_prefetch(dx_pool p, int32_t layer, int32_t* experts, int32_t* blocks, int32_t* n) {
+    DX_CHECK(p && experts && blocks && n, DX_ERR_INVALID_ARG, "null argument");
+    DX_CHECK(layer >= 0 && layer < p->L, DX_ERR_RANGE, "layer %d out of range", (int)layer);
+    DX_CUDA(cudaStreamSynchronize(p->cs));
+    *n = 0;
+    for (const int2& sg : p->staged[layer]) { experts[*n] = sg.x; blocks[*n] = sg.y; ++*n; }
+    if (*n == 0 && p->pf_pending[layer]) {          // made but not issued yet: report the candidates themselves
+        for (int i = 0; i < p->pf_n_host[layer]; ++i) {
+            experts[i] = p->pf_host[(size_t)layer * 8 + i].x;
+            blocks[i] = p->pf_host[(size_t)layer * 8 + i].y;
+        }
+        *n = p->pf_n_host[layer];
+    }
     return DX_OK;
 }
 
@@ -732,6 +803,9 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
         out->xfer_max_ms = a > out->xfer_max_ms ? a : out->xfer_max_ms;
         out->plans += 1;
     }
+    out->prefetch_issued = (int64_t)p->pf_issued;
+    out->prefetch_hits = (int64_t)p->pf_hits;
+    p->pf_issued = p->pf_hits = 0;
     for (size_t i = 0; i + 1 < p->prof_copy_ev.size(); i += 2) {
         float a = 0;
         DX_CUDA(cudaEventElapsedTime(&a, p->prof_copy_ev[i], p->prof_copy_ev[i + 1]));
@@ -804,6 +878,51 @@ static dx_status ep_forward(dx_pool p, int layer, const void* x, int T, const vo
                             const float* logits, void* y, int32_t* topk_idx, float* topk_gate, bool fuse_fold);
 static dx_status poll_transfers(dx_pool p, int wait_layer = -1);
 
+// f-1 after layer `layer`'s routing (idx [T][k] on the compute stream): the correlation counts of the pair
+// (layer - 1, layer) when the previous layer routed the same batch, this routing kept for the next layer, and --
+// `pf_lead` steps before layer + 1's next plan -- that layer's prefetch candidates, read back like a plan.
+static dx_status prefetch_hooks(dx_pool p, int layer, const int32_t* idx, int T) {
+    const int k = p->k, E = p->E_loc, par = layer & 1;
+    const bool upd = layer >= 1 && p->T_last[par ^ 1] == T;
+    launch_corr(upd ? p->idx_last + (size_t)(par ^ 1) * p->cfg.max_tokens * k : nullptr, idx, T, k, E,
+                upd ? p->corr + (size_t)(layer - 1) * E * E : nullptr, p->idx_last + (size_t)par * p->cfg.max_tokens * k,
+                p->cs);
+    p->launches += 1;
+    p->T_last[par] = T;
+    const int nl = layer + 1;
+    if (nl >= p->L || !p->finalized[nl] || p->pf_pending[nl] || p->publish_at[nl] >= 0) return DX_OK;
+    const i64 t = p->t[nl];                                   // layer nl's step count: this batch's step
+    if (t <= p->cfg.warmup_steps || (t + p->pf_lead) % p->cfg.period != 0) return DX_OK;
+    launch_prefetch(p->ctrl, nl, p->corr + (size_t)layer * E * E, idx, T, k, p->pf_f, p->pf_dev + (size_t)nl * 8,
+                    p->pf_n_dev + nl, p->cs);
+    DX_CUDA(cudaMemcpyAsync(p->pf_host + (size_t)nl * 8, p->pf_dev + (size_t)nl * 8, 8 * sizeof(int4),
+                            cudaMemcpyDeviceToHost, p->cs));
+    DX_CUDA(cudaMemcpyAsync(p->pf_n_host + nl, p->pf_n_dev + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, p->cs));
+    DX_CUDA(cudaEventRecord(p->ev_pf[nl], p->cs));
+    p->pf_pending[nl] = 1;
+    p->n_pending += 1;
+    p->launches += 1;
+    return DX_OK;
+}
+
+// the staged copies of layer `layer`'s prefetch candidates (H2D on the copy engine into free HIGH blocks)
+static dx_status issue_prefetch(dx_pool p, int layer) {
+    const size_t bytes = p->hi.bits == 16 ? (size_t)3 * p->I * p->H * 2 : (size_t)p->hi.bytes;
+    uint8_t* hi_region = p->weights + (size_t)layer * p->layer_bytes + p->hi_base;
+    const int n = p->pf_n_host[layer];
+    p->staged[layer].clear();
+    for (int i = 0; i < n; ++i) {
+        const int4 c = p->pf_host[(size_t)layer * 8 + i];
+        DX_CUDA(cudaMemcpyAsync(hi_region + (size_t)c.y * p->hi.bytes, p->hi_img_host[(size_t)layer * p->E_loc + c.x],
+                                bytes, cudaMemcpyHostToDevice, p->ss));
+        p->staged[layer].push_back(make_int2(c.x, c.y));
+    }
+    p->pf_issued += (u64)n;
+    p->pf_pending[layer] = 0;
+    p->n_pending -= 1;
+    return DX_OK;
+}
+
 static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T, const void* router_w,
                               const float* router_bias, const float* logits, void* y, int32_t* topk_idx,
                               float* topk_gate, bool fuse_fold) {
@@ -830,6 +949,10 @@ static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T
     p->last_logits_router = router_w != nullptr;
     p->last_T = T;
     route_tokens(p, layer, x, T, router_w, router_bias, logits, ws);
+    if (p->pf_f > 0) {
+        dx_status st = prefetch_hooks(p, layer, ws.idx, T);
+        if (st != DX_OK) return st;
+    }
     p->pend_tokens[layer] += (u64)T;
     return expert_ffn(p, layer, ws, x, T, p->k, y, ev, fuse_fold);
 }
@@ -1191,6 +1314,11 @@ static dx_status read_plan(dx_pool p, int layer, dx_plan* out) {
 // copy-engine H2D per promotion from the pinned HIGH image into its destination block; ev_side marks them done.
 static dx_status issue_transfers(dx_pool p, int layer) {
     const size_t E = (size_t)p->E_loc;
+    if (p->pf_pending[layer]) {                    // the layer's prefetch copies go first on the side stream
+        DX_CUDA(cudaEventSynchronize(p->ev_pf[layer]));
+        dx_status st = issue_prefetch(p, layer);
+        if (st != DX_OK) return st;
+    }
     cudaEvent_t x0 = nullptr;
     if (p->profiling) {
         x0 = prof_event(p);
@@ -1212,6 +1340,9 @@ static dx_status issue_transfers(dx_pool p, int layer) {
     for (int i = 0; i < n; ++i) {
         const int4 cmd = p->plan_host[layer * E + i];
         if (cmd.y != 1) continue;
+        bool hit = false;                          // staged by the prefetch into this very block already
+        for (const int2& sg : p->staged[layer]) hit |= sg.x == cmd.x && sg.y == cmd.z;
+        if (hit) { ++p->pf_hits; continue; }
         DX_CUDA(cudaMemcpyAsync(hi_region + (size_t)cmd.z * p->hi.bytes, p->hi_img_host[layer * E + cmd.x], bytes,
                                 cudaMemcpyHostToDevice, p->ss));
         ++np;
@@ -1230,6 +1361,7 @@ static dx_status issue_transfers(dx_pool p, int layer) {
         DX_CUDA(cudaEventRecord(x1, p->ss));
     }
     DX_CUDA(cudaEventRecord(p->ev_side[layer], p->ss));
+    p->staged[layer].clear();
     p->xfer_pending[layer] = 0;
     p->n_pending -= 1;
     return DX_OK;
@@ -1245,6 +1377,16 @@ static dx_status poll_transfers(dx_pool p, int wait_layer) {
         if (st != DX_OK) return st;
     }
     for (int l = 0; l < p->L && p->n_pending > 0; ++l) {
+        if (p->pf_pending[l]) {
+            const cudaError_t q = cudaEventQuery(p->ev_pf[l]);
+            if (q == cudaSuccess) {
+                dx_status st = issue_prefetch(p, l);
+                if (st != DX_OK) return st;
+            } else if (q != cudaErrorNotReady) {
+                dx_set_error("prefetch event: %s", cudaGetErrorString(q));
+                return DX_ERR_CUDA;
+            }
+        }
         if (!p->xfer_pending[l]) continue;
         const cudaError_t q = cudaEventQuery(p->ev_planh[l]);
         if (q == cudaErrorNotReady) continue;
@@ -1355,6 +1497,11 @@ extern "C" dx_status dx_demote(dx_pool p, int32_t layer, const int32_t* experts,
 extern "C" dx_status dx_sync(dx_pool p) {
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
     for (int l = 0; l < p->L; ++l) {
+        if (p->pf_pending[l]) {
+            DX_CUDA(cudaEventSynchronize(p->ev_pf[l]));
+            dx_status st = issue_prefetch(p, l);
+            if (st != DX_OK) return st;
+        }
         if (!p->xfer_pending[l]) continue;
         dx_status st = poll_transfers(p, l);
         if (st != DX_OK) return st;

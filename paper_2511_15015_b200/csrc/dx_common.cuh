@@ -358,6 +358,11 @@ void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, i
 // k_ctrl.cu
 void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st);
 void launch_plan(const Ctrl& c, int layer, int finalize, cudaStream_t st);
+// f-1 cross-layer correlation prefetch (k_ctrl.cu)
+void launch_corr(const int32_t* idx_prev, const int32_t* idx, int T, int k, int E, uint32_t* corr, int32_t* idx_save,
+                 cudaStream_t st);
+void launch_prefetch(const Ctrl& c, int layer, const uint32_t* corr, const int32_t* idx_cur, int T, int k, int f,
+                     int4* out, int32_t* n_out, cudaStream_t st);
 struct XferArgs {
     uint8_t* layer_base;
     i64 hi_base;

@@ -279,6 +279,76 @@ __global__ void __launch_bounds__(128, 10) k_xfer(Ctrl c, int layer, XferArgs x,
     }
 }
 
+// ------------------------------------------------------------------ f-1: cross-layer correlation prefetch
+// ("proactively prefetches experts predicted to become hot by leveraging cross-layer activation
+// correlations"; SPEC.md:337-392 CorrelationModel / update_correlation / prefetch_candidates.)
+// corr[e][e'] (pair of layers l, l+1) += 1 for every expert e layer l chose and e' layer l+1 chose for the same
+// token: k*k increments per token (SPEC.md update_correlation).  Integer sums: order-free, bit-exact.
+// idx_prev NULL: no update (the previous layer routed another batch); idx is also saved to idx_save for the next
+// layer.  Programmatic dependent launch keeps it inside the forward's launch chain.
+__global__ void k_corr(const int32_t* __restrict__ idx_prev, const int32_t* __restrict__ idx, int T, int k, int E,
+                       uint32_t* __restrict__ corr, int32_t* __restrict__ idx_save) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < T * k) idx_save[i] = idx[i];
+    if (!idx_prev || i >= T * k * k) return;
+    const int t = i / (k * k), j = (i / k) % k, j2 = i % k;
+    const int a = idx_prev[t * k + j], b = idx[t * k + j2];
+    if (a >= 0 && a < E && b >= 0 && b < E) atomicAdd(&corr[(size_t)a * E + b], 1u);
+}
+// Prefetch candidates for layer `layer` (= l + 1) from layer l's current routing idx_cur [T][k]: score(e') =
+// sum over the T*k chosen (t, j) of corr[idx_cur[t][j]][e'] (u64, exact); eligible e' are LOW-tier, not in flight,
+// score > 0; up to f of them by (score desc, id asc), each paired with the next lowest free HIGH block in ascending
+// order (the blocks the next plan's promotions take first).  out[i] = {expert, block}; *n_out = count.
+__global__ void __launch_bounds__(512) k_prefetch(Ctrl c, int layer, const uint32_t* __restrict__ corr,
+                                                  const int32_t* __restrict__ idx_cur, int T, int k, int f,
+                                                  int4* __restrict__ out, int32_t* __restrict__ n_out) {
+    __shared__ unsigned long long best[16];
+    __shared__ int32_t freeb[64];
+    __shared__ int32_t nfree;
+    const int E = c.E, base = layer * E, ob = layer * (E + c.s);
+    const int e = threadIdx.x;
+    unsigned long long sc = 0;
+    if (e < E) {
+        for (int q = 0; q < T * k; ++q) {
+            const int a = idx_cur[q];
+            if (a >= 0 && a < E) sc += corr[(size_t)a * E + e];
+        }
+        if (c.tier[base + e] != 0 || c.pend_dir[base + e] != 0) sc = 0;
+    }
+    if (threadIdx.x == 0) {
+        int nf = 0;
+        const int cap = c.cap_hi[layer];
+        for (int b = 0; b < cap && nf < 64; ++b)
+            if (c.hi_owner[ob + b] < 0) freeb[nf++] = b;
+        nfree = nf;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int n = 0;
+    const int fmax = min(f, nfree);
+    for (int r = 0; r < fmax; ++r) {
+        // key: score in the high bits, (E - 1 - id) in the low 16 bits: max key = highest score, lowest id
+        unsigned long long key = (sc > 0 && e < E) ? ((sc << 16) | (unsigned long long)(0xFFFF - e)) : 0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+            key = y > key ? y : key;
+        }
+        if (lane == 0) best[warp] = key;
+        __syncthreads();
+        unsigned long long m = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = best[w] > m ? best[w] : m;
+        __syncthreads();
+        if (m == 0) break;
+        const int pick = 0xFFFF - (int)(m & 0xFFFF);
+        if (e == pick) sc = 0;
+        if (threadIdx.x == 0) out[n] = make_int4(pick, freeb[n], 0, 0);
+        ++n;
+    }
+    if (threadIdx.x == 0) *n_out = n;
+}
+
 }  // namespace
 
 void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st) {
@@ -287,6 +357,18 @@ void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st) {
 
 void launch_plan(const Ctrl& c, int layer, int finalize, cudaStream_t st) {
     dx_launch(k_plan, dim3(1), dim3(CTRL_THREADS), 0, st, g_dx_pdl, c, layer, finalize);
+}
+
+void launch_corr(const int32_t* idx_prev, const int32_t* idx, int T, int k, int E, uint32_t* corr, int32_t* idx_save,
+                 cudaStream_t st) {
+    const int n = T * k * k;
+    if (n <= 0) return;
+    dx_launch(k_corr, dim3((n + 255) / 256), dim3(256), 0, st, g_dx_pdl, idx_prev, idx, T, k, E, corr, idx_save);
+}
+
+void launch_prefetch(const Ctrl& c, int layer, const uint32_t* corr, const int32_t* idx_cur, int T, int k, int f,
+                     int4* out, int32_t* n_out, cudaStream_t st) {
+    k_prefetch<<<1, 512, 0, st>>>(c, layer, corr, idx_cur, T, k, f, out, n_out);
 }
 
 void launch_manual(const Ctrl& c, int layer, const int2* cmds, int n, int32_t* status, cudaStream_t st) {

@@ -68,7 +68,7 @@ class dx_profile_t(ctypes.Structure):
                 ("route_ms", ctypes.c_double), ("exposed_ms", ctypes.c_double), ("publishes", ctypes.c_int64),
                 ("xfer_ms", ctypes.c_double), ("xfer_max_ms", ctypes.c_double), ("plans", ctypes.c_int64),
                 ("promotions", ctypes.c_int64), ("demotions", ctypes.c_int64), ("copy_ms", ctypes.c_double),
-                ("copy_bytes", ctypes.c_uint64)]
+                ("copy_bytes", ctypes.c_uint64), ("prefetch_issued", ctypes.c_int64), ("prefetch_hits", ctypes.c_int64)]
 
 
 class dx_plan(ctypes.Structure):
@@ -107,6 +107,9 @@ _SIG = {
     "dx_profile_enable": [_vp, _i32],
     "dx_set_ffn_path": [_vp, _i32],
     "dx_set_teleport": [_vp, _i32],
+    "dx_set_prefetch": [_vp, _i32, _i32],
+    "dx_get_corr": [_vp, _i32, _vp],
+    "dx_get_prefetch": [_vp, _i32, _vp, _vp, _vp],
     "dx_profile_read": [_vp, _P(dx_profile_t)],
 }
 for _n, _a in _SIG.items():
@@ -330,6 +333,22 @@ class Pool:
     def dx_set_ffn_path(self, path: int):
         _check(_lib.dx_set_ffn_path(self.h, path), "dx_set_ffn_path")
 
+    def dx_set_prefetch(self, fanout: int, lead: int = 2):
+        _check(_lib.dx_set_prefetch(self.h, fanout, lead), "dx_set_prefetch")
+
+    def dx_get_corr(self, layer: int):
+        import numpy as np
+        E = self.info.experts_local
+        out = np.zeros((E, E), dtype=np.uint32)
+        _check(_lib.dx_get_corr(self.h, layer, out.ctypes.data), "dx_get_corr")
+        return out
+
+    def dx_get_prefetch(self, layer: int):
+        import numpy as np
+        ex, bl, n = np.zeros(8, np.int32), np.zeros(8, np.int32), ctypes.c_int32()
+        _check(_lib.dx_get_prefetch(self.h, layer, ex.ctypes.data, bl.ctypes.data, ctypes.byref(n)), "dx_get_prefetch")
+        return list(zip(ex[:n.value].tolist(), bl[:n.value].tolist()))
+
     def dx_set_teleport(self, on: bool):
         """Timing baseline only: plans publish on schedule but no transfer runs (weights become garbage)."""
         _check(_lib.dx_set_teleport(self.h, 1 if on else 0), "dx_set_teleport")
@@ -346,4 +365,4 @@ class Pool:
                     active_experts=int(pr.active_experts), route_ms=pr.route_ms, exposed_ms=pr.exposed_ms,
                     publishes=pr.publishes, xfer_ms=pr.xfer_ms, xfer_max_ms=pr.xfer_max_ms, plans=pr.plans,
                     promotions=pr.promotions, demotions=pr.demotions, copy_ms=pr.copy_ms,
-                    copy_bytes=int(pr.copy_bytes))
+                    copy_bytes=int(pr.copy_bytes), prefetch_issued=pr.prefetch_issued, prefetch_hits=pr.prefetch_hits)

@@ -105,6 +105,24 @@ def trace_logits(seed, layer, step, T, E, zipf_s=1.2, drift_period=0, drift_frac
     return out
 
 
+def coupled_trace_logits(seed, L, step, T, E, k, boost=6.0, zipf_s=1.2, drift_period=0, drift_frac=0.0,
+                         n_top=16):
+    """Trace logits of L consecutive layers with cross-layer correlation (the input recipe of the f-1 prefetch
+    measurements): layer 0 is trace_logits; layer l adds `boost` to pi_l(e) for the k largest
+    logits e of layer l-1's row (ties: lower id), pi_l a seeded per-layer permutation.  Input generation only:
+    the selection here is a plain numpy sort of the generated values."""
+    out = [trace_logits(seed, 0, step, T, E, zipf_s, drift_period, drift_frac, n_top)]
+    for l in range(1, L):
+        pi = np.random.default_rng(seed * 1000 + l).permutation(E)
+        prev = out[-1]
+        top = np.argsort(-prev, axis=1, kind="stable")[:, :k]
+        lg = trace_logits(seed, l, step, T, E, zipf_s, drift_period, drift_frac, n_top).copy()
+        rows = np.repeat(np.arange(T), k)
+        lg[rows, pi[top.ravel()]] += np.float32(boost)
+        out.append(lg)
+    return out
+
+
 def bf16_to_f32(a: np.ndarray) -> np.ndarray:
     """Exact widening of bf16 bits to float32 (bit placement only, no rounding)."""
     return (a.astype(np.uint32) << 16).view(np.float32)
