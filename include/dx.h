@@ -57,6 +57,11 @@ typedef struct {
     int32_t publish_lag;        /* L: 1 <= L < Tp, transitions become stable L steps after issue (R-T1) */
     int32_t max_tokens;         /* max tokens per dx_moe_forward; sizes the workspace */
     int32_t ep_rank, ep_size;   /* expert parallelism: this GPU owns experts [r*E/G, (r+1)*E/G) */
+    int32_t n_shared;           /* f-3: shared experts per layer (0 or 1, Eq. 1's first sum PAPER.md:130, R-S1): an
+                                   always-on expert of every token, gate 1, kept at the HIGH tier in its own block
+                                   (outside the routed experts' budget M and the controller); master pointers
+                                   follow the routed ones (master[L * E_loc + l] = layer l's shared expert);
+                                   tcgen05 FFN path and ep_size == 1 only */
 } dx_config;
 
 typedef struct dx_pool_s* dx_pool;
@@ -128,7 +133,8 @@ dx_status dx_pool_create_ep(const dx_config* cfg, const void* const* master_bf16
 
 /* ---------------------------------------------------------------- the MoE layer (Eq. 1) */
 
-/* y = sum_{j in topk} g_j(x) E_j(x) for T tokens of one layer, each expert
+/* y = sum_{j in topk} g_j(x) E_j(x) (+ E^s(x) with n_shared = 1: y = bf16(E^s(x) + sum_j ...), the shared term
+ * first) for T tokens of one layer, each expert
  * read at its last stable version and tier.
  *   x_bf16      [T][H] bf16, device.
  *   router_w    [E][H] bf16, device, and router_bias [E] fp32 (may be NULL): router mode,

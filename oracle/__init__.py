@@ -68,6 +68,8 @@ def _L():
         "or_ledger_free": ([vp, i32, i32, i32], i32),
         "or_corr_update": ([vp, vp, vp, i32, i32, i32], None),
         "or_prefetch_candidates": ([vp, vp, i32, i32, i32, vp, vp, vp, i32, i32, vp, vp], i32),
+        "or_shared_ffn": ([vp, vp, i32, i32, i32, vp, i32], None),
+        "or_combine_shared": ([vp, vp, i32, i32, i32, vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -305,3 +307,18 @@ def prefetch_candidates(corr, idx, tier, in_flight, hi_owner, f):
     n = _L().or_prefetch_candidates(_p(corr), _p(idx), T, k, corr.shape[0], _p(tier), _p(infl), _p(own), own.size, f,
                                     _p(oe), _p(ob))
     return list(zip(oe[:n].tolist(), ob[:n].tolist()))
+
+
+# ---------------------------------------------------------------- f-3 shared expert
+def moe_ffn_shared(x_bf16, idx, gate, weights: dict, w_shared, H, I, nthreads=1):
+    """Eq. 1 with one shared expert (R-S1): (Ys [T][H], Y [T][k][H], y [T][H]); y = bf16(Ys + sum_j Y_j)."""
+    x = np.ascontiguousarray(x_bf16, dtype=np.uint16)
+    T = x.shape[0]
+    Y, _ = moe_ffn(x, idx, gate, weights, H, I, nthreads=nthreads)
+    ws = np.ascontiguousarray(w_shared, dtype=np.uint16)
+    Ys = np.zeros((T, H), dtype=np.uint16)
+    _L().or_shared_ffn(_p(x), _p(ws), T, H, I, _p(Ys), nthreads)
+    y = np.zeros((T, H), dtype=np.uint16)
+    k = np.asarray(idx).shape[1]
+    _L().or_combine_shared(_p(Ys), _p(np.ascontiguousarray(Y)), T, k, H, _p(y))
+    return Ys, Y, y

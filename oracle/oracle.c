@@ -584,3 +584,43 @@ int32_t or_prefetch_candidates(const uint32_t* corr, const int32_t* idx, int32_t
     free(freeb);
     return n;
 }
+
+/* ------------------------------------------------------------------ f-3 shared expert (Eq. 1) */
+/* The shared term of Eq. 1, y = sum_{i in S} E^s_i(x) + sum_{j in K} g_j E_j(x), with one shared expert per layer
+ * (R-S1): Ys[t] = bf16_rn(E^s(x_t)), the same SwiGLU FFN and rounding points as a routed expert with gate 1
+ * (u, v, o in fp64; a = bf16_rn(silu(u) v)).  W_s: the dequantised bf16 [3*I*H] image at the HIGH tier. */
+void or_shared_ffn(const uint16_t* x, const uint16_t* Ws, int32_t T, int32_t H, int32_t I, uint16_t* Ys,
+                   int32_t nthreads) {
+    const int64_t n = (int64_t)I * H;
+    #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int32_t t = 0; t < T; ++t) {
+        const uint16_t* xt = x + (size_t)t * H;
+        double* xd = (double*)malloc(sizeof(double) * (size_t)H);
+        double* a = (double*)malloc(sizeof(double) * (size_t)I);
+        for (int32_t h = 0; h < H; ++h) xd[h] = (double)or_bf16_to_f32(xt[h]);
+        for (int32_t i = 0; i < I; ++i) {
+            double u = 0.0, v = 0.0;
+            for (int32_t h = 0; h < H; ++h) {
+                u += (double)or_bf16_to_f32(Ws[(size_t)i * H + h]) * xd[h];
+                v += (double)or_bf16_to_f32(Ws[n + (size_t)i * H + h]) * xd[h];
+            }
+            const double silu = u / (1.0 + exp(-u));
+            a[i] = (double)or_bf16_to_f32(or_f64_to_bf16_rn(silu * v));
+        }
+        for (int32_t h = 0; h < H; ++h) {
+            double o = 0.0;
+            for (int32_t i = 0; i < I; ++i) o += (double)or_bf16_to_f32(Ws[2 * n + (size_t)h * I + i]) * a[i];
+            Ys[(size_t)t * H + h] = or_f64_to_bf16_rn(o);
+        }
+        free(xd); free(a);
+    }
+}
+/* y[t] = bf16_rn(Ys[t] + sum_j Y[t][j]): the shared term first, then the routed rows in rank order (R-S1). */
+void or_combine_shared(const uint16_t* Ys, const uint16_t* Y, int32_t T, int32_t k, int32_t H, uint16_t* y) {
+    for (int32_t t = 0; t < T; ++t)
+        for (int32_t h = 0; h < H; ++h) {
+            double acc = (double)or_bf16_to_f32(Ys[(size_t)t * H + h]);
+            for (int32_t j = 0; j < k; ++j) acc += (double)or_bf16_to_f32(Y[((size_t)t * k + j) * H + h]);
+            y[(size_t)t * H + h] = or_f64_to_bf16_rn(acc);
+        }
+}

@@ -93,6 +93,11 @@ int32_t or_prefetch_candidates(const uint32_t* corr, const int32_t* idx, int32_t
                                const int32_t* tier, const int32_t* in_flight, const int32_t* hi_owner, int32_t cap_hi,
                                int32_t f, int32_t* out_e, int32_t* out_b);
 
+/* f-3 shared expert (Eq. 1 first sum; DESIGN.md R-S1) */
+void or_shared_ffn(const uint16_t* x, const uint16_t* Ws, int32_t T, int32_t H, int32_t I, uint16_t* Ys,
+                   int32_t nthreads);
+void or_combine_shared(const uint16_t* Ys, const uint16_t* Y, int32_t T, int32_t k, int32_t H, uint16_t* y);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,8 @@ struct dx_pool_s {
     std::vector<std::vector<int2>> staged;  // per layer: {expert, block} copies issued for the coming plan
     u64 pf_issued = 0, pf_hits = 0;
     bool teleport = false;                  // timing baseline: plans and publications without the transfers
+    int hi_slots = 1;                       // HIGH blocks addressable by the tensor maps (incl. the shared one)
+    int shared_slot = 0;                    // f-3: the shared expert's HIGH block index
     // runtime plans reach the host through pinned memory; the host then issues the promotions' H2D copies on the
     // copy engine (cudaMemcpyAsync on the side stream) and the demotion kernel -- as soon as the plan is seen
     // done (polled at every library call), at the latest at the publication step
@@ -159,12 +161,12 @@ static dx_status build_maps(dx_pool p) {
         const uint8_t* lb = p->weights + (size_t)l * p->layer_bytes;
         bool ok = true;
         if (p->hi.bits == 16) {
-            const uint64_t d0[4] = {(uint64_t)H, (uint64_t)I, 2, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
+            const uint64_t d0[4] = {(uint64_t)H, (uint64_t)I, 2, (uint64_t)p->hi_slots};
             const uint64_t s0[3] = {(uint64_t)H * 2, (uint64_t)p->hi.codes_stride, (uint64_t)p->hi.bytes};
             const uint32_t b0[4] = {64, 64, 2, 1};           // 64 gate rows, then the 64 matching up rows
             ok &= make_map(&g.a16_gu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, lb + p->hi_base, d0, s0, b0,
                            CU_TENSOR_MAP_SWIZZLE_128B);
-            const uint64_t d1[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)(cap_hi > 0 ? cap_hi : 1)};
+            const uint64_t d1[3] = {(uint64_t)I, (uint64_t)H, (uint64_t)p->hi_slots};
             const uint64_t s1[2] = {(uint64_t)I * 2, (uint64_t)p->hi.bytes};
             const uint32_t b1[3] = {64, 128, 1};
             ok &= make_map(&g.a16_dn, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, lb + p->hi_base + (size_t)2 * I * H * 2, d1, s1,
@@ -174,7 +176,7 @@ static dx_status build_maps(dx_pool p) {
             const SlotLayout& Ls = t ? p->hi : p->lo;
             if (Ls.bits == 16) continue;
             const uint8_t* base = lb + (t ? p->hi_base : 0);
-            const uint64_t slots = t ? (uint64_t)(cap_hi > 0 ? cap_hi : 1) : (uint64_t)(E + s);
+            const uint64_t slots = t ? (uint64_t)p->hi_slots : (uint64_t)(E + s);
             const uint64_t rb0 = (uint64_t)H * Ls.bits / 8, rb1 = (uint64_t)I * Ls.bits / 8;
             const uint32_t kb = 64 * Ls.bits / 8;
             const uint64_t d0[4] = {rb0, (uint64_t)I, 2, slots};
@@ -225,7 +227,7 @@ static dx_status build_maps(dx_pool p) {
                 const SlotLayout& Ls = t ? p->hi : p->lo;
                 if (Ls.bits == 16) continue;
                 const uint8_t* base = lb + (t ? p->hi_base : 0);
-                const uint64_t slots = t ? (uint64_t)(cap_hi > 0 ? cap_hi : 1) : (uint64_t)(E + s);
+                const uint64_t slots = t ? (uint64_t)p->hi_slots : (uint64_t)(E + s);
                 const uint64_t rb0 = (uint64_t)H * Ls.bits / 8, rb1 = (uint64_t)I * Ls.bits / 8;
                 const uint64_t d0[4] = {rb0, (uint64_t)I, 2, slots}, s0[3] = {rb0, (uint64_t)Ls.codes_stride, (uint64_t)Ls.bytes};
                 const uint64_t d1[3] = {rb1, (uint64_t)H, slots}, s1[2] = {rb1, (uint64_t)Ls.bytes};
@@ -333,6 +335,8 @@ static dx_status validate(const dx_config* c) {
              DX_ERR_INVALID_ARG, "ep_size must divide num_experts and 0 <= ep_rank < ep_size");
     DX_CHECK(c->num_experts <= 512 && c->num_experts + c->n_spare <= 1024, DX_ERR_INVALID_ARG,
              "num_experts must be <= 512");
+    DX_CHECK(c->n_shared == 0 || c->n_shared == 1, DX_ERR_INVALID_ARG, "n_shared must be 0 or 1");
+    DX_CHECK(c->n_shared == 0 || c->ep_size == 1, DX_ERR_INVALID_ARG, "a shared expert needs ep_size == 1");
     return DX_OK;
 }
 
@@ -366,6 +370,13 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     p->hi_base = (i64)cap_lo * p->lo.bytes;
     i64 lb = p->hi_base + (i64)cap_hi * p->hi.bytes;
     if ((i64)E * p->lo.bytes > lb) lb = (i64)E * p->lo.bytes;   // warm-up layout (R-P3)
+    p->hi_slots = cap_hi > 0 ? cap_hi : 1;
+    if (cfg->n_shared) {
+        // f-3: the shared expert's HIGH block after everything else (never part of the warm-up LOW region)
+        p->shared_slot = (int)((lb - p->hi_base + p->hi.bytes - 1) / p->hi.bytes);
+        p->hi_slots = p->shared_slot + 1;
+        lb = p->hi_base + (i64)p->hi_slots * p->hi.bytes;
+    }
     p->layer_bytes = dx_up(lb, 1024);
 
     // ---- the one device allocation: weights | controller | workspace | staging
@@ -373,7 +384,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     const int G = cfg->ep_size;
     const bool ep = G > 1 || nccl_id != nullptr;     // dispatch-side workspace (and NCCL buffers with an id)
     // entries (rows) one forward can see: T*k locally; an EP owner receives up to G*T*min(k, E_loc) rows
-    const size_t n_ent = G > 1 ? std::max((size_t)T * k, (size_t)G * T * std::min(k, E)) : (size_t)T * k;
+    const int ns = cfg->n_shared;              // f-3: the shared expert's T rows follow the T*k routed entries
+    const size_t n_ent = G > 1 ? std::max((size_t)T * k, (size_t)G * T * std::min(k, E)) : (size_t)T * (k + ns);
     p->n_ent = n_ent;
     const int nblk = route_blocks((int)(ep ? n_ent : (size_t)T));   // the owner side routes up to n_ent rows
     const size_t Ek = (size_t)E;
@@ -432,8 +444,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     w.gate = carve<float>(q, n_ent);
     w.hist = carve<int32_t>(q, (size_t)nblk * p->E);
     w.base = carve<int32_t>(q, (size_t)nblk * p->E);
-    w.off = carve<int32_t>(q, p->E + 1);
-    w.act_e = carve<int32_t>(q, p->E);
+    w.off = carve<int32_t>(q, p->E + 1 + ns);
+    w.act_e = carve<int32_t>(q, p->E + ns);
     w.n_act = carve<int32_t>(q, 1);
     w.perm = carve<int32_t>(q, n_ent);
     w.inv = carve<int32_t>(q, n_ent);
@@ -636,6 +648,14 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
             }
             p->launches += cfg->high_bits == 16 ? 3 : 6;
         }
+    for (int l = 0; l < L && cfg->n_shared; ++l) {           // f-3: shared experts, HIGH tier, their own block
+        const void* m = master[(size_t)L * E + l];
+        if (!m) { dx_set_error("null shared-expert master pointer (layer %d)", l); return fail(DX_ERR_INVALID_ARG); }
+        uint8_t* blk = p->weights + (size_t)l * p->layer_bytes + p->hi_base + (size_t)p->shared_slot * p->hi.bytes;
+        DX_CUDA(cudaMemcpyAsync(stage_master, m, mbytes, cudaMemcpyHostToDevice, p->cs));
+        if (cfg->high_bits == 16) DX_CUDA(cudaMemcpyAsync(blk, stage_master, mbytes, cudaMemcpyDeviceToDevice, p->cs));
+        else launch_quantize_slot(stage_master, bf, blk, p->hi, p->H, p->I, p->g, p->cs);
+    }
     DX_CUDA(cudaStreamSynchronize(p->cs));
     DX_CUDA(cudaGetLastError());
 
@@ -666,6 +686,7 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
 
 extern "C" dx_status dx_set_ffn_path(dx_pool p, int32_t path) {
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
+    DX_CHECK(path == 0 || p->cfg.n_shared == 0, DX_ERR_INVALID_ARG, "the shared expert runs on the tcgen05 path only");
     DX_CHECK(path == 0 || path == 1, DX_ERR_INVALID_ARG, "path must be 0 (tcgen05) or 1 (mma.sync)");
     p->ffn_path = path;
     return DX_OK;
@@ -953,6 +974,11 @@ static dx_status forward_impl(dx_pool p, int32_t layer, const void* x, int32_t T
         dx_status st = prefetch_hooks(p, layer, ws.idx, T);
         if (st != DX_OK) return st;
     }
+    if (p->cfg.n_shared) {                                    // f-3: the shared expert's rows after the routed ones
+        launch_shared_rows(ws, T, p->k, p->E_loc, p->H, (const __nv_bfloat16*)x, p->ffn_path == 1 ? nullptr : p->Xp,
+                           p->wbytes[1][0], p->wbytes[1][1], p->cs);
+        p->launches += 1;
+    }
     p->pend_tokens[layer] += (u64)T;
     return expert_ffn(p, layer, ws, x, T, p->k, y, ev, fuse_fold);
 }
@@ -1013,7 +1039,8 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
     a.lo = p->lo;
     a.H = p->H; a.I = p->I; a.g = p->g; a.k = k;
     if (ev[1]) DX_CUDA(cudaEventRecord(ev[1], p->cs));
-    const int max_act = T * k < E ? T * k : E;
+    const int ns = k == p->k ? p->cfg.n_shared : 0;            // the owner-side (k = 1) EP path has no shared rows
+    const int max_act = (T * k < E ? T * k : E) + ns;
     if (p->ffn_path == 1) {
         launch_expert_ffn(a, (const __nv_bfloat16*)x, ws.gate, ws, T, E, p->act, p->Y, p->cs, ev[2]);
     } else {
@@ -1027,6 +1054,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
             da.tier = a.tier; da.slot = a.slot; da.off = ws.off; da.act_e = ws.act_e; da.n_act = ws.n_act;
             da.perm = ws.perm; da.gate = ws.gate; da.H = p->H; da.I = p->I; da.g = p->g; da.k = k;
             da.act = p->act; da.Y = p->Y; da.sched = p->gemm_sched;
+            da.E_loc = E; da.shared_slot = p->shared_slot;
             static const int dbg = [] { const char* s = getenv("DX_GEMM_DBG"); return s ? atoi(s) : 0; }();
             da.dbg = dbg;
             launch_dec(0, p->dec_maps[layer], p->dec_bmaps, da, max_act * (p->I / 64), p->cs);
@@ -1038,6 +1066,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         ga.tier = a.tier; ga.slot = a.slot; ga.off = ws.off; ga.act_e = ws.act_e; ga.n_act = ws.n_act;
         ga.perm = ws.perm; ga.gate = ws.gate; ga.H = p->H; ga.I = p->I; ga.g = p->g; ga.k = k;
         ga.act = p->act; ga.Y = p->Y; ga.sched = p->gemm_sched;
+        ga.E_loc = E; ga.shared_slot = p->shared_slot;
         static const int dbg = [] { const char* s = getenv("DX_GEMM_DBG"); return s ? atoi(s) : 0; }();
         ga.dbg = dbg;
         GemmMaps gm = p->gmaps[layer];
@@ -1056,9 +1085,9 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         FoldReq req;
         dx_status st = fold_prepare(p, layer, &req);
         if (st != DX_OK) return st;
-        launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs, nullptr, &p->ctrl, &req);
+        launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs, nullptr, &p->ctrl, &req, ns ? T * k : -1);
     } else {
-        launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs);
+        launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs, nullptr, nullptr, nullptr, ns ? T * k : -1);
     }
     p->launches += 3;
     cudaError_t ce = cudaGetLastError();

@@ -242,8 +242,14 @@ struct FoldReq {
     int layer;
     u64 B_tot;
 };
+// shared_base >= 0: row shared_base + t of Y holds token t's shared-expert term, summed first (f-3, R-S1)
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st,
-                    const int32_t* inv = nullptr, const Ctrl* ctrl = nullptr, const FoldReq* fold = nullptr);
+                    const int32_t* inv = nullptr, const Ctrl* ctrl = nullptr, const FoldReq* fold = nullptr,
+                    int shared_base = -1);
+// f-3: the shared expert's rows (entries T*k .. T*k+T-1: perm, gate 1, Xp = x) appended after the routed ones, the
+// shared expert (id E) listed first among the active experts; stats: its bytes added to the profiling counters
+void launch_shared_rows(const RouteWs& ws, int T, int k, int E, int H, const __nv_bfloat16* x, __nv_bfloat16* Xp,
+                        u64 b0, u64 b1, cudaStream_t st);
 // expert parallelism: owner-side routing from received (local expert, gate) rows (k = 1), and the
 // source-side dispatch metadata / per-owner counts
 void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
@@ -304,6 +310,7 @@ struct GemmArgs {
     const int32_t* perm;
     const float* gate;
     int H, I, g, k;
+    int E_loc, shared_slot;         // f-3: expert id E_loc is the layer's shared expert, HIGH tier, block shared_slot
     __nv_bfloat16* act;
     __nv_bfloat16* Y;
     int* sched;                     // [phase][ticket counter, CTAs done]: dynamic work-item hand-out, zero
@@ -338,6 +345,7 @@ struct DecArgs {
     const int32_t* perm;
     const float* gate;
     int H, I, g, k;
+    int E_loc, shared_slot;         // f-3 (as GemmArgs)
     __nv_bfloat16* act;
     __nv_bfloat16* Y;
     int* sched;

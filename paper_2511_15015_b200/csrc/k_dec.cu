@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const __grid_constant__ DecP
     for (int i = threadIdx.x; i < n_act && i < EMAX; i += THREADS) {
         const int e = a.act_e[i];
         const int r0 = a.off[e];
-        etab[i] = make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+        etab[i] = make_int4(r0, a.off[e + 1] - r0, e < a.E_loc ? a.slot[e] : a.shared_slot, e < a.E_loc ? a.tier[e] : 1);
     }
     tc_fence_before();
     __syncthreads();
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dec(const __grid_constant__ DecP
                     } else {
                         const int e = a.act_e[i];
                         const int r0 = a.off[e];
-                        v = make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+                        v = make_int4(r0, a.off[e + 1] - r0, e < a.E_loc ? a.slot[e] : a.shared_slot, e < a.E_loc ? a.tier[e] : 1);
                     }
                 }
                 ring[sl].v = v;

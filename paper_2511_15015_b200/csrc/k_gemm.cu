@@ -194,13 +194,13 @@ __device__ __forceinline__ int4 decode_tiled(const GemmArgs& a, const int32_t* t
     const int e = a.act_e[lo];
     const int r0 = a.off[e] + (q - tpre[lo]) * NT;
     const int m = min(NT, a.off[e + 1] - r0);
-    return make_int4(r0, m, a.slot[e], a.tier[e]);
+    return make_int4(r0, m, e < a.E_loc ? a.slot[e] : a.shared_slot, e < a.E_loc ? a.tier[e] : 1);
 }
 __device__ __forceinline__ int4 decode_raw(const GemmArgs& a, const int4* etab, int item, int nmb) {   // {r0, m, slot, ti}
     if (item / nmb < EMAX) return etab[item / nmb];
     const int e = a.act_e[item / nmb];
     const int r0 = a.off[e];
-    return make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+    return make_int4(r0, a.off[e + 1] - r0, e < a.E_loc ? a.slot[e] : a.shared_slot, e < a.E_loc ? a.tier[e] : 1);
 }
 // One published work item of the ring: decoded fields + the ticket (>= n_items: no more work).
 struct Tick {
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         for (int i = threadIdx.x; i < n_act && i < EMAX; i += Roles<DEC>::THREADS) {
             const int e = a.act_e[i];
             const int r0 = a.off[e];
-            etab[i] = make_int4(r0, a.off[e + 1] - r0, a.slot[e], a.tier[e]);
+            etab[i] = make_int4(r0, a.off[e + 1] - r0, e < a.E_loc ? a.slot[e] : a.shared_slot, e < a.E_loc ? a.tier[e] : 1);
         }
     }
     tc_fence_before();

@@ -631,6 +631,49 @@ __global__ void __launch_bounds__(256) k_place(const int32_t* __restrict__ idx, 
     for (int h = lane; h < H / 8; h += 32) dst[h] = __ldg(src + h);
 }
 
+// ------------------------------------------------------------------ f-3 shared expert rows (Eq. 1 first sum)
+// After routing: entries n .. n+T-1 (n = T*k) are the shared expert's rows, one per token in order: perm, gate 1.0
+// (bf16(1 * o) = bf16(o) exactly), Xp[n + t] = x[t]; off[E + 1] = n + T; the shared expert (id E) goes first in the
+// active list (the heaviest item); its algorithmic weight bytes join the profiling counters.  Block 0 rewrites the
+// active list; every block copies a share of the rows.
+__global__ void __launch_bounds__(256) k_shared_rows(int32_t* __restrict__ perm, float* __restrict__ gate,
+                                                     int32_t* __restrict__ off, int32_t* __restrict__ act_e,
+                                                     int32_t* __restrict__ n_act, u64* __restrict__ stats, u64 b0, u64 b1,
+                                                     int T, int k, int E, int H, const __nv_bfloat16* __restrict__ x,
+                                                     __nv_bfloat16* __restrict__ Xp) {
+    __shared__ int32_t lst[ROUTE_MAX_E];
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int n = T * k;
+    if (blockIdx.x == 0) {
+        const int na = *n_act;
+        for (int i = threadIdx.x; i < na; i += blockDim.x) lst[i] = act_e[i];
+        __syncthreads();
+        for (int i = threadIdx.x; i < na; i += blockDim.x) act_e[i + 1] = lst[i];
+        if (threadIdx.x == 0) {
+            act_e[0] = E;
+            *n_act = na + 1;
+            off[E + 1] = n + T;
+            if (stats) {
+                atomicAdd(&stats[0], b0);
+                atomicAdd(&stats[1], b1);
+                atomicAdd(&stats[2], 1ull);
+            }
+        }
+    }
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+        perm[n + t] = n + t;
+        gate[n + t] = 1.0f;
+    }
+    if (!Xp) return;
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < T; t += gridDim.x * wpb) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * H);
+        uint4* dst = reinterpret_cast<uint4*>(Xp + (size_t)(n + t) * H);
+        for (int h = lane; h < H / 8; h += 32) dst[h] = __ldg(src + h);
+    }
+}
+
 // ------------------------------------------------------------------ a8: y_t = bf16(sum_j Y[t,j])
 // inv == NULL: Y rows in entry order (t*k + j); else Y rows in permuted order, entry i at row inv[i]
 // (expert-parallel combine: the rows come back from their owners in dispatch order).  Block = (token,
@@ -639,7 +682,8 @@ __global__ void __launch_bounds__(256) k_place(const int32_t* __restrict__ idx, 
 // finished (griddepcontrol.wait), so the table flip never races the GEMMs that read the tables.
 __global__ void __launch_bounds__(128) k_combine(const __nv_bfloat16* __restrict__ Y, int k, int H, int nseg, int cthr,
                                                  __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ inv,
-                                                 const Ctrl c, int fold_on, int fold_layer_id, u64 B_tot, double oma) {
+                                                 const Ctrl c, int fold_on, int fold_layer_id, u64 B_tot, double oma,
+                                                 int shared_base) {
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
     if (fold_on && blockIdx.x == gridDim.x - 1) {
@@ -660,6 +704,12 @@ __global__ void __launch_bounds__(128) k_combine(const __nv_bfloat16* __restrict
     float acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+    if (shared_base >= 0) {                      // f-3: the shared expert's term first (R-S1)
+        const uint4 vs = __ldcg(reinterpret_cast<const uint4*>(Y + ((size_t)shared_base + t) * H + h));
+        const uint16_t* b = reinterpret_cast<const uint16_t*>(&vs);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], dx_bf2f(b[i]));
+    }
 #pragma unroll
     for (int j = 0; j < ROUTE_MAX_K; ++j) {
         if (j < k) {
@@ -832,13 +882,21 @@ void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x
               (const int32_t*)ws.base, (const int32_t*)ws.off, ws.perm, ws.inv, x, H, Xp);
 }
 
+void launch_shared_rows(const RouteWs& ws, int T, int k, int E, int H, const __nv_bfloat16* x, __nv_bfloat16* Xp,
+                        u64 b0, u64 b1, cudaStream_t st) {
+    if (T <= 0) return;
+    const int blocks = (T + 7) / 8 < 148 ? (T + 7) / 8 : 148;
+    dx_launch(k_shared_rows, dim3(blocks), dim3(256), 0, st, g_dx_pdl, ws.perm, ws.gate, ws.off, ws.act_e, ws.n_act,
+              ws.stats, b0, b1, T, k, E, H, x, Xp);
+}
+
 static void launch_scan_e(int nblk, int E, const RouteWs& ws, const RouteStats& rs, cudaStream_t st) {
     dx_launch(k_scan_e, dim3(E), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.hist, nblk, E, ws.base, ws.off,
               ws.act_e, ws.n_act, rs, ws.done);
 }
 
 void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* y, cudaStream_t st,
-                    const int32_t* inv, const Ctrl* ctrl, const FoldReq* fold) {
+                    const int32_t* inv, const Ctrl* ctrl, const FoldReq* fold, int shared_base) {
     if (T <= 0 && !fold) return;
     int nseg = 1;                               // segments of <= 128 threads x 8 columns that tile H exactly
     while ((H / 8) / nseg > 128 || (H / 8) % nseg) ++nseg;
@@ -849,7 +907,7 @@ void launch_combine(const __nv_bfloat16* Y, int T, int k, int H, __nv_bfloat16* 
     const int threads = fold ? (cthr > 128 ? cthr : 128) : cthr;
     dx_launch(k_combine, dim3(blocks), dim3(threads), 0, st, g_dx_pdl, Y, k, H, nseg, cthr, y,
               inv, c, fold ? 1 : 0, fold ? fold->layer : 0, fold ? fold->B_tot : (u64)0,
-              ctrl ? 1.0 - ctrl->alpha : 0.0);
+              ctrl ? 1.0 - ctrl->alpha : 0.0, shared_base);
 }
 
 void launch_route_given(const int2* meta, int R, int E, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,

@@ -47,7 +47,7 @@ class dx_config(ctypes.Structure):
                 ("expert_budget_bytes", ctypes.c_uint64), ("n_spare", ctypes.c_int32),
                 ("ema_alpha", ctypes.c_double), ("period", ctypes.c_int32), ("warmup_steps", ctypes.c_int32),
                 ("dwell_min", ctypes.c_int32), ("publish_lag", ctypes.c_int32), ("max_tokens", ctypes.c_int32),
-                ("ep_rank", ctypes.c_int32), ("ep_size", ctypes.c_int32)]
+                ("ep_rank", ctypes.c_int32), ("ep_size", ctypes.c_int32), ("n_shared", ctypes.c_int32)]
 
 
 class dx_info(ctypes.Structure):
