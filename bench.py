@@ -598,7 +598,12 @@ def q80b_leg(a, peak, L=8):
     cfg.n_spare, cfg.ema_alpha = s_sp, 0.95
     cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = 16, 32, 16, 4
     cfg.max_tokens, cfg.ep_rank, cfg.ep_size = 4096, 0, 1
-    pool = dx.Pool(cfg, ptrs, stream)
+    cfg.n_shared = 1                  # Qwen3-Next's shared expert (f-3, Eq. 1's first sum), int4 like the HIGH tier
+    sh = np.empty(L * 3 * I * H, dtype=np.uint16)
+    for l in range(L):
+        synth.expert_master_into(seed + 1, l, 0, H, I, sh[l * 3 * I * H:(l + 1) * 3 * I * H])
+    torch.cuda.cudart().cudaHostRegister(sh.ctypes.data, sh.nbytes, 0)
+    pool = dx.Pool(cfg, ptrs + [sh.ctypes.data + l * 3 * I * H * 2 for l in range(L)], stream)
     assert pool.info.n_hot == n_hot, (pool.info.n_hot, n_hot)
     wr = torch.empty(L, E, H, dtype=torch.bfloat16, device=dev)
     for l in range(L):
@@ -608,7 +613,8 @@ def q80b_leg(a, peak, L=8):
     for l in range(L):
         for ep in range(n_ep):
             bias[l, ep].copy_(torch.from_numpy(synth.zipf_logp(synth.rank_perm(seed, l, ep, E, n_hot, 0.25), 1.2)))
-    res = {"workload": f"C4 shape at G=1: {L}-layer Qwen3-Next-80B-A3B-shaped stack (E=512, top-10, H=2048, I=512), "
+    res = {"workload": f"C4 shape at G=1: {L}-layer Qwen3-Next-80B-A3B-shaped stack (E=512, top-10, H=2048, I=512, "
+                       f"one shared expert per layer at the HIGH tier), "
                        f"int4 HIGH / int2 LOW g=128, n_hot={n_hot} (25 %), s=1, {M / 1e6:.1f} MB per layer"}
     cnt = [0]
     for name, T, n_t in (("decode", 64, 10), ("prefill", 4096, 2)):
@@ -651,10 +657,11 @@ def q80b_leg(a, peak, L=8):
             r["ffn_weight_gbs"] = wb / ffn_s / 1e9 if ffn_s > 0 else 0.0
             r["ffn_hbm_frac"] = r["ffn_weight_gbs"] / peak
         else:
-            r["gemm_tflops"] = 2.0 * T * k * 3 * I * H * prof["forwards"] / ffn_s / 1e12 if ffn_s > 0 else 0.0
+            r["gemm_tflops"] = 2.0 * T * (k + 1) * 3 * I * H * prof["forwards"] / ffn_s / 1e12 if ffn_s > 0 else 0.0
         res[name] = r
     pool.close()
     torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
+    torch.cuda.cudart().cudaHostUnregister(sh.ctypes.data)
     return res
 
 

@@ -1092,6 +1092,18 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
     p->launches += 3;
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "launch failed: %s", cudaGetErrorString(ce));
+    static const bool log_bytes = getenv("DX_LOG_BYTES") != nullptr;
+    if (log_bytes && ws.stats) {   // evidence runs (ncu traffic pairing): this forward's algorithmic bytes per phase
+        static u64 prev[2] = {0, 0};
+        u64 st[2];
+        DX_CUDA(cudaStreamSynchronize(p->cs));
+        DX_CUDA(cudaMemcpy(st, ws.stats, sizeof(st), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 2; ++i) if (st[i] < prev[i]) prev[i] = 0;      // counters were reset in between
+        fprintf(stderr, "DX_LOG_BYTES layer %d T %d gateup %llu down %llu\n", layer, T,
+                (unsigned long long)(st[0] - prev[0]), (unsigned long long)(st[1] - prev[1]));
+        prev[0] = st[0];
+        prev[1] = st[1];
+    }
     return DX_OK;
 }
 
