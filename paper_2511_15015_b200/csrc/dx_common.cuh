@@ -316,7 +316,8 @@ struct GemmArgs {
     int* sched;                     // [phase][ticket counter, CTAs done]: dynamic work-item hand-out, zero
                                     // between launches (the last CTA of a launch resets it)
     int dbg;                        // performance experiments only (DX_GEMM_DBG): 4 skip the A-in-TMEM MMAs,
-                                    // 5 skip the dequant transform, 6 both
+                                    // 5 skip the dequant transform, 6 both, 13 = 6 with plain
+                                    // arrivals instead of tcgen05.commit on int stages
 };
 bool gemm_decode_cfg(int T);
 

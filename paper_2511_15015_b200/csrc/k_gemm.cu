@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                             const uint64_t bj = db + j0 * bstep;
                             const bool first = (kb0 | j0) == 0;
                             if (elect_one()) {
-                                if (a.dbg != 4 && a.dbg != 6) {
+                                if (a.dbg != 4 && a.dbg != 6 && a.dbg != 13) {
                                     if (jn == C::ACH) {
 #pragma unroll
                                         for (int q = 0; q < 4 * C::ACH; ++q)
@@ -445,13 +445,17 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                                                             !first || j || s);
                                     }
                                 }
-                                mma_commit(&aempty[ab]);
+                                if (a.dbg == 13) mbar_arrive(&aempty[ab]);   // timing only: no commit latency
+                                else mma_commit(&aempty[ab]);
                             }
                             __syncwarp();
                             if (++ab == C::NA) { ab = 0; aph ^= 1; }
                         }
                     }
-                    if (elect_one()) mma_commit(&empty[st]);
+                    if (elect_one()) {
+                        if (a.dbg == 13 && w.bits != 16) mbar_arrive(&empty[st]);
+                        else mma_commit(&empty[st]);
+                    }
                     __syncwarp();
                     if (++st == STAGES) { st = 0; ph ^= 1; }
                 }
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                             if (++ab == C::NA) { ab = 0; aph ^= 1; }
                             if (!DEC && (nbuf % NG) != grp) continue;  // prefill: another group's buffer
                             gwait(&aempty[cab], caph ^ 1, 8, DX_TBACK);
-                            if (a.dbg != 5 && a.dbg != 6) {
+                            if (a.dbg != 5 && a.dbg != 6 && a.dbg != 13) {
 #pragma unroll
                                 for (int h = 0; h < (DEC ? C::ACH / NG : 1); ++h) {
                                     const int jj = DEC ? (C::ACH / NG) * grp + h : 0;   // chunk within the buffer
