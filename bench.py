@@ -491,9 +491,13 @@ def run_ours(a, rank, world, local_rank):
         out["clocks"] = clock
     if not a.no_batch_sweep:
         out["extra"]["decode_batch_sweep"] = batch_sweep(a, pool, wr, bias, step_counter, L, H, dev, stream, peak)
+    if not a.no_batch_sweep:
+        out["extra"]["zipf_sweep"] = zipf_sweep(a, pool, wr, step_counter, L, E, H, dev, stream, peak)
     if a.prefill_tokens > 0:
         out["extra"]["prefill"] = prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream)
     pool.close()
+    if not ep_mode and not a.no_batch_sweep:
+        out["extra"]["tier_brackets"] = tier_brackets(a, cfg, ptrs, L, E, H, B, dev, stream, peak, wr_arr, bias_arr)
     if not ep_mode and not a.no_prefetch_leg:
         out["extra"]["prefetch"] = prefetch_leg(a, ptrs, L, E, k, H, I, g, c, dev, stream)
     if not ep_mode and not a.no_teleport:
@@ -673,7 +677,7 @@ def batch_sweep(a, pool, wr, bias, step_counter, L, H, dev, stream, peak):
     import synth
     c = C2
     rows = []
-    for B in (1, 4, 16, 64):
+    for B in (1, 2, 4, 8, 16, 32, 64):
         xs = [torch.from_numpy(synth.normal_bf16(a.seed, 800 + B, i, 0, (B, H)).view(np.int16)).to(dev).view(torch.bfloat16)
               for i in range(2)]
         y = torch.empty(B, H, dtype=torch.bfloat16, device=dev)
@@ -711,6 +715,108 @@ def batch_sweep(a, pool, wr, bias, step_counter, L, H, dev, stream, peak):
                      "weight_bytes_per_layer": wb / max(prof["forwards"], 1), "ffn_weight_gbs": gbs,
                      "ffn_hbm_frac": gbs / peak})
     return rows
+
+
+def zipf_sweep(a, pool, wr, step_counter, L, E, H, dev, stream, peak):
+    """SURVEY §8(d) C2 routing skew s in {0, 0.8, 1.2} (the bench's main line is 1.2): B = 64 decode on the same
+    stack and pool (HIGH set as the controller left it), 5 timed steps per s after 2 untimed; layer-tokens/s, touched
+    experts and the expert GEMMs' weight GB/s."""
+    import torch
+    import synth
+    B, rows = 64, []
+    xs = [torch.from_numpy(synth.normal_bf16(a.seed, 870, i, 0, (B, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+          for i in range(2)]
+    y = torch.empty(B, H, dtype=torch.bfloat16, device=dev)
+    P = pool.ptr_array
+    y_arr, wr_arr = P([y] * L), P([wr[l] for l in range(L)])
+    x_arrs = [P([x] * L) for x in xs]
+    for s in (0.0, 0.8, 1.2):
+        bias = torch.stack([torch.from_numpy(synth.zipf_logp(synth.rank_perm(a.seed, l, 0, E, 24, 0.25), s))
+                            for l in range(L)]).to(dev)
+        b_arr = P([bias[l] for l in range(L)])
+        for i in range(2):
+            pool.dx_moe_step_layers(0, L, x_arrs[i % 2], B, y_arr, router_w_arr=wr_arr, router_bias_arr=b_arr)
+            step_counter[0] += 1
+        pool.dx_sync()
+        pool.dx_profile_read()
+        pool.dx_profile_enable(True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n = 5
+        for i in range(n):
+            pool.dx_moe_step_layers(0, L, x_arrs[i % 2], B, y_arr, router_w_arr=wr_arr, router_bias_arr=b_arr)
+            step_counter[0] += 1
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        prof = pool.dx_profile_read()
+        pool.dx_profile_enable(False)
+        wb = prof["weight_bytes"][0] + prof["weight_bytes"][1]
+        ffn_s = (prof["ffn_ms"][0] + prof["ffn_ms"][1]) / 1e3
+        gbs = wb / ffn_s / 1e9 if ffn_s > 0 else 0.0
+        rows.append({"zipf_s": s, "value": B * L * n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / n,
+                     "active_experts_per_layer": prof["active_experts"] / max(prof["forwards"], 1),
+                     "weight_bytes_per_layer": wb / max(prof["forwards"], 1), "ffn_weight_gbs": gbs,
+                     "ffn_hbm_frac": gbs / peak})
+    return rows
+
+
+def tier_brackets(a, cfg0, ptrs, L, E, H, B, dev, stream, peak, wr_arr, bias_arr):
+    """The uniform brackets of the C2 decode line: every expert at bf16 (budget for n_hot = E) and
+    every expert at int4 (n_hot = 0), fresh pools over the same stack and inputs, router mode, 10 timed steps after
+    the warm-up and finalize; layer-tokens/s and the expert GEMMs' weight GB/s against the HBM peak."""
+    import ctypes
+    import torch
+    import synth
+    from paper_2511_15015_b200 import dx
+    S_h, S_l = dx.dx_slot_bytes(H, cfg0.inter, cfg0.group_size, 16), dx.dx_slot_bytes(H, cfg0.inter, cfg0.group_size, 4)
+    s_sp = cfg0.n_spare
+    out = {}
+    xs = [torch.from_numpy(synth.normal_bf16(a.seed, 880, i, 0, (B, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+          for i in range(2)]
+    y = torch.empty(2, B, H, dtype=torch.bfloat16, device=dev)
+    for name, n_hot in (("all_bf16", E), ("all_int4", 0)):
+        cfg = dx.dx_config()
+        ctypes.memmove(ctypes.addressof(cfg), ctypes.addressof(cfg0), ctypes.sizeof(cfg))
+        cfg.expert_budget_bytes = L * (n_hot * S_h + (E - n_hot) * S_l + s_sp * (S_h + S_l))
+        pool = dx.Pool(cfg, ptrs, stream)
+        assert pool.info.n_hot == n_hot, (pool.info.n_hot, n_hot)
+        P = pool.ptr_array
+        y_arr = P([y[l & 1] for l in range(L)])
+        x_arrs = [P([x] * L) for x in xs]
+
+        def st(i):
+            pool.dx_moe_step_layers(0, L, x_arrs[i & 1], B, y_arr, router_w_arr=wr_arr, router_bias_arr=bias_arr[0])
+
+        for i in range(cfg.warmup_steps):
+            st(i)
+        for l in range(L):
+            pool.dx_plan_precision(l)
+        for i in range(3):
+            st(i)
+        pool.dx_sync()
+        pool.dx_profile_read()
+        pool.dx_profile_enable(PROF_EVERY)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n = 10
+        for i in range(n):
+            st(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        prof = pool.dx_profile_read()
+        pool.close()
+        wb = prof["weight_bytes"][0] + prof["weight_bytes"][1]
+        ffn_s = (prof["ffn_ms"][0] + prof["ffn_ms"][1]) / 1e3
+        g0 = prof["weight_bytes"][0] / (prof["ffn_ms"][0] / 1e3) / 1e9 if prof["ffn_ms"][0] > 0 else 0.0
+        gbs = wb / ffn_s / 1e9 if ffn_s > 0 else 0.0
+        out[name] = {"n_hot": n_hot, "value": B * L * n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / n,
+                     "weight_bytes_per_layer": wb / max(prof["forwards"], 1), "gateup_gbs": g0, "gateup_frac": g0 / peak,
+                     "ffn_weight_gbs": gbs, "ffn_hbm_frac": gbs / peak}
+    return out
 
 
 def prefill_leg(a, pool, wr, bias, step_counter, L, E, H, I, k, c, dev, stream):
@@ -898,6 +1004,57 @@ def oracle_layer_sample(a, seconds=15.0, max_steps=None):
     return B / statistics.mean(times), nthreads, len(times), times
 
 
+def oracle_extra_timings(a):
+    """SURVEY §8(d)'s oracle timing plan beside the main cpu_baseline (the oracle as it stands, host cores):
+    C1 in full (300 steps: route, counters, fold, plan, FFN), the group quantiser on one Q30B expert, one plan at
+    E = 512, and one C3 layer (T = 4096, top-8) estimated from a bounded 64-token sample of it."""
+    import oracle
+    import synth
+    out = {"cores": os.cpu_count() or 1}
+    # C1 in full
+    E, k, H, I, g, T = 8, 2, 64, 128, 32, 32
+    W = {e: oracle.expert_tier(synth.expert_master(a.seed, 0, e, H, I), H, I, g, 16, 4, e < 2) for e in range(E)}
+    ctrl = oracle.Controller(E, 2, 1, 0.9, 8, 16, 16, 2)
+    t0 = time.perf_counter()
+    for step in range(300):
+        lg = synth.trace_logits(a.seed, 0, step, T, E, 1.2, 16, 0.5, 2)
+        idx, gate = oracle.route(lg, k)
+        oracle.moe_ffn(synth.normal_bf16(a.seed, 1, step, 0, (T, H)), idx, gate, W, H, I)
+        ctrl.fold(oracle.counts(idx, gate, E)[1], T)
+        ctrl.plan()
+    out["c1_300_steps_s"] = time.perf_counter() - t0
+    # quantiser on one Q30B expert (3 matrices of 768 x 2048, int4, g = 128)
+    m = synth.expert_master(a.seed, 0, 0, 2048, 768)
+    t0 = time.perf_counter()
+    oracle.expert_tier(m, 2048, 768, 128, 16, 4, False)
+    out["quantize_q30b_expert_s"] = time.perf_counter() - t0
+    # one plan at E = 512
+    c512 = oracle.Controller(512, 128, 1, 0.95, 16, 1, 16, 4)
+    rng = np.random.default_rng(0)
+    c512.fold(rng.integers(0, 1 << 24, 512, dtype=np.uint64), 64)
+    c512.plan()                                   # finalize
+    for _ in range(15):
+        c512.fold(rng.integers(0, 1 << 24, 512, dtype=np.uint64), 64)
+        c512.plan()
+    c512.fold(rng.integers(0, 1 << 24, 512, dtype=np.uint64), 64)
+    t0 = time.perf_counter()
+    c512.plan()
+    out["plan_e512_s"] = time.perf_counter() - t0
+    # C3: one T = 4096 layer from a 64-token sample
+    E, k, H, I = 128, 8, 2048, 768
+    lg = synth.trace_logits(a.seed, 0, 0, 64, E, 1.2)
+    idx, gate = oracle.route(lg, k)
+    Wc = {int(e): oracle.expert_tier(synth.expert_master(a.seed, 0, int(e), H, I), H, I, 128, 16, 4, int(e) % 5 == 0)
+          for e in np.unique(idx)}
+    x = synth.normal_bf16(a.seed, 2, 0, 0, (64, H))
+    t0 = time.perf_counter()
+    oracle.moe_ffn(x, idx, gate, Wc, H, I, nthreads=os.cpu_count() or 1)
+    dt = time.perf_counter() - t0
+    out["c3_layer_est_s"] = dt * 4096 / 64
+    out["c3_sample"] = "64 of the 4096 tokens (top-8 FFN over pre-dequantised images, all host threads), scaled x64"
+    return out
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return None
@@ -953,6 +1110,8 @@ def main():
             out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                    "sample": f"layer 0 of the C2 stack, batch {a.batch}, {nsteps} steps "
                                              "(router, top-k, FFN over pre-dequantised stable images, fold, plan)"}
+            if not a.no_batch_sweep:
+                out["cpu_baseline"]["extra_timings"] = oracle_extra_timings(a)
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist
