@@ -518,7 +518,7 @@ def prefetch_leg(a, ptrs, L_all, E, k, H, I, g, c, dev, stream, L=8):
     budget -> n_hot 24) in trace mode with cross-layer-coupled routing (synth.coupled_trace_logits: layer l boosts
     pi_l of layer l-1's choices; Zipf(1.2) with a quarter of the top-24 set drifting every 16 steps), B = 64,
     Tp=16, L=4, run from fresh pools on identical inputs: cross-layer prefetch off, then on with fan-out 1 and 2
-    (lead 4).  Per run over the last 48 steps (3 plan periods): promotions, prefetch hits, mean side-stream switch
+    (lead 4); and f-4, the same run with the HIGH images on the SSD tier behind a 16-image DRAM cache.  Per run over the last 48 steps (3 plan periods): promotions, prefetch hits, mean side-stream switch
     time per plan (issue -> ready), copy-engine bytes per plan and the device ms per step."""
     import torch
     import synth
@@ -535,7 +535,7 @@ def prefetch_leg(a, ptrs, L_all, E, k, H, I, g, c, dev, stream, L=8):
     res = {"workload": f"f-1: {L}-layer C2-shaped stack, trace mode with cross-layer coupled routing (boost 6 on "
                        f"pi_l of layer l-1's top-{k}), drift 25 % of the top-24 set every 16 steps, B={B}, Tp={Tp}, "
                        f"L={lag}; lead 4; last {steps_timed} steps"}
-    for mode, fan in (("off", 0), ("on_f1", 1), ("on_f2", 2)):
+    for mode, fan in (("off", 0), ("on_f1", 1), ("on_f2", 2), ("ssd_tier", 0)):
         cfg = dx.dx_config()
         cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = L, E, k, H, I, g
         cfg.high_bits, cfg.low_bits = c["high"], c["low"]
@@ -543,7 +543,11 @@ def prefetch_leg(a, ptrs, L_all, E, k, H, I, g, c, dev, stream, L=8):
         cfg.n_spare, cfg.ema_alpha = c["s"], c["alpha"]
         cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = Tp, W, Tp, lag
         cfg.max_tokens, cfg.ep_rank, cfg.ep_size = B, 0, 1
-        pool = dx.Pool(cfg, ptrs[:L * E], stream)
+        if mode == "ssd_tier":       # f-4: HIGH images in a file on the box's disk behind a 16-image DRAM cache
+            pool = dx.Pool(cfg, ptrs[:L * E], stream, ssd_path=os.path.join("/tmp", f"dx_bench_ssd_{os.getpid()}.bin"),
+                           dram_cache_images=16)
+        else:
+            pool = dx.Pool(cfg, ptrs[:L * E], stream)
         if fan:
             pool.dx_set_prefetch(fan, 4)
         P = pool.ptr_array
@@ -572,6 +576,10 @@ def prefetch_leg(a, ptrs, L_all, E, k, H, I, g, c, dev, stream, L=8):
                      "prefetch_issued": pr["prefetch_issued"], "prefetch_hits": pr["prefetch_hits"],
                      "switch_ms_mean": pr["xfer_ms"] / max(pr["plans"], 1),
                      "copy_mb_per_plan": pr["copy_bytes"] / max(pr["plans"], 1) / 1e6}
+        if mode == "ssd_tier":
+            res[mode].update({"ssd_reads": pr["ssd_reads"], "ssd_mb": pr["ssd_bytes"] / 1e6,
+                              "ssd_read_gbs": pr["ssd_bytes"] / (pr["ssd_read_ms"] / 1e3) / 1e9 if pr["ssd_read_ms"] > 0
+                              else None, "dram_cache_hits": pr["dram_cache_hits"]})
     for m in ("on_f1", "on_f2"):
         res[m]["hit_rate"] = res[m]["prefetch_hits"] / max(res[m]["promotions"], 1)
     return res

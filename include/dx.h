@@ -128,6 +128,14 @@ dx_status dx_pool_info(dx_pool pool, dx_info* out);
  * (DX_NCCL_LIB overrides).  Errors: NCCL (library missing, init or collective failure), plus
  * dx_pool_create's. */
 dx_status dx_get_unique_id(void* id128);
+/* f-4 SSD tier ("stored on SSD and cached in DRAM"): dx_pool_create plus a file at ssd_path that
+ * the library creates and fills with every expert's HIGH image at create time (it is removed at destroy), and a
+ * pinned DRAM cache of dram_cache_images HIGH images in front of it (LRU).  Every promotion (plans, the warm-up
+ * finalize, manual commands, prefetch staging) then takes its image from the cache, or reads it from the file
+ * (O_DIRECT when the image size allows, so a miss really reads the device) into the least recently used slot,
+ * then copies it to HBM on the copy engine.  Masters are read during create only.  ep_size 1 only. */
+dx_status dx_pool_create_ssd(const dx_config* cfg, const void* const* master_bf16_host, void* compute_stream,
+                             void* side_stream, const char* ssd_path, int32_t dram_cache_images, dx_pool* out);
 dx_status dx_pool_create_ep(const dx_config* cfg, const void* const* master_bf16_host, void* compute_stream,
                             void* side_stream, const void* nccl_id, dx_pool* out);
 
@@ -277,6 +285,10 @@ typedef struct {
     uint64_t copy_bytes;        /* bytes those copies moved (copy_bytes / copy_ms = promotion bandwidth) */
     int64_t  prefetch_issued;   /* f-1: HIGH images staged ahead of plans */
     int64_t  prefetch_hits;     /* promotions whose image was already staged in their destination block */
+    int64_t  ssd_reads;         /* f-4: HIGH images read from the SSD tier (DRAM-cache misses) */
+    uint64_t ssd_bytes;
+    double   ssd_read_ms;       /* host time spent in those reads */
+    int64_t  dram_cache_hits;   /* HIGH images served by the DRAM cache */
 } dx_profile_t;
 /* f-1 cross-layer correlation prefetch.  fanout f in [0, 8] (0 = off), lead d in
  * [1, Tp - L].  With f > 0 every dx_moe_forward / dx_moe_step of layer l (the stack called layer by layer on the

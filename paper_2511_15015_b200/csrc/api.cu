@@ -3,9 +3,13 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 #include <cmath>
 #include <algorithm>
+#include <chrono>
+#include <fcntl.h>
+#include <unistd.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include "dx_common.cuh"
@@ -101,6 +105,20 @@ struct dx_pool_s {
     int32_t* ep_pairs = nullptr;            // device [2][G] int2: my {count, T} per peer | received per peer
     int32_t* ep_pairs_host = nullptr;       // pinned mirror (the v1 host synchronisation point)
     u64 copy_promotions = 0;                // promotions issued as copy-engine H2D copies
+    // f-4 SSD tier (dx_pool_create_ssd): every HIGH image in one file, a pinned DRAM cache of `ssd_slots` images
+    // in front of it (LRU; a slot is reused only after the copies out of it completed)
+    int ssd_fd = -1;
+    std::string ssd_path;
+    bool ssd_direct = false;
+    int ssd_slots = 0;
+    size_t img_bytes = 0;                   // bytes of one HIGH image (the promotion copy size)
+    uint8_t* ssd_cache = nullptr;           // pinned [ssd_slots][img_bytes]
+    std::vector<int> cache_slot_of;         // [L * E_loc] -> slot or -1
+    std::vector<int> cache_owner;           // [slot] -> key or -1
+    std::vector<u64> cache_used;            // [slot] LRU clock
+    std::vector<cudaEvent_t> cache_ev;      // [slot] last copy out of the slot
+    u64 cache_clock = 0, ssd_reads = 0, ssd_bytes = 0, cache_hits = 0;
+    double ssd_read_ms = 0.0;
     // f-1 cross-layer correlation prefetch (dx_set_prefetch): device counts per layer pair, the last routing of
     // each layer parity, candidates staged into free HIGH blocks ahead of the plan
     uint32_t* corr = nullptr;               // [L-1][E][E]
@@ -340,8 +358,74 @@ static dx_status validate(const dx_config* c) {
     return DX_OK;
 }
 
+// ---------------------------------------------------------------- f-4 SSD tier
+static dx_status ssd_write(dx_pool p, size_t key, const void* src) {
+    const uint8_t* b = static_cast<const uint8_t*>(src);
+    size_t done = 0;
+    while (done < p->img_bytes) {
+        const ssize_t r = pwrite(p->ssd_fd, b + done, p->img_bytes - done, (off_t)(key * p->img_bytes + done));
+        DX_CHECK(r > 0, DX_ERR_INVALID_ARG, "SSD tier write failed (expert image %zu)", key);
+        done += (size_t)r;
+    }
+    return DX_OK;
+}
+
+// The pinned host image of HIGH image `key` = layer * E_loc + expert: a DRAM-cache hit, or an SSD read into the
+// least recently used slot (after the copies out of that slot completed).  *slot_out: the cache slot.
+static dx_status cached_image(dx_pool p, size_t key, const uint8_t** img, int* slot_out) {
+    int sl = p->cache_slot_of[key];
+    if (sl >= 0) {
+        ++p->cache_hits;
+    } else {
+        sl = -1;
+        for (int i = 0; i < p->ssd_slots && sl < 0; ++i)
+            if (p->cache_owner[i] < 0) sl = i;                      // a free slot first
+        if (sl < 0) {                                              // else the least recently used
+            sl = 0;
+            for (int i = 1; i < p->ssd_slots; ++i)
+                if (p->cache_used[i] < p->cache_used[sl]) sl = i;
+        }
+        DX_CUDA(cudaEventSynchronize(p->cache_ev[sl]));            // copies out of the victim slot are done
+        if (p->cache_owner[sl] >= 0) p->cache_slot_of[(size_t)p->cache_owner[sl]] = -1;
+        uint8_t* dst = p->ssd_cache + (size_t)sl * p->img_bytes;
+        const auto t0 = std::chrono::steady_clock::now();
+        size_t done = 0;
+        while (done < p->img_bytes) {
+            const ssize_t r = pread(p->ssd_fd, dst + done, p->img_bytes - done, (off_t)(key * p->img_bytes + done));
+            DX_CHECK(r > 0, DX_ERR_INVALID_ARG, "SSD tier read failed (expert image %zu)", key);
+            done += (size_t)r;
+        }
+        p->ssd_read_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ++p->ssd_reads;
+        p->ssd_bytes += p->img_bytes;
+        p->cache_owner[sl] = (int)key;
+        p->cache_slot_of[key] = sl;
+    }
+    p->cache_used[sl] = ++p->cache_clock;
+    *img = p->ssd_cache + (size_t)sl * p->img_bytes;
+    *slot_out = sl;
+    return DX_OK;
+}
+
+// H2D of HIGH image `key` into a HIGH block on `st` (copy engine): from the pinned masters / HIGH cache, or through
+// the SSD tier's DRAM cache
+static dx_status copy_high_image(dx_pool p, size_t key, uint8_t* dst, cudaStream_t st) {
+    if (p->ssd_fd < 0) {
+        DX_CUDA(cudaMemcpyAsync(dst, p->hi_img_host[key], p->img_bytes, cudaMemcpyHostToDevice, st));
+        return DX_OK;
+    }
+    const uint8_t* img;
+    int sl;
+    dx_status rc = cached_image(p, key, &img, &sl);
+    if (rc != DX_OK) return rc;
+    DX_CUDA(cudaMemcpyAsync(dst, img, p->img_bytes, cudaMemcpyHostToDevice, st));
+    DX_CUDA(cudaEventRecord(p->cache_ev[sl], st));
+    return DX_OK;
+}
+
 static dx_status pool_create(const dx_config* cfg, const void* const* master, void* compute_stream,
-                             void* side_stream, const void* nccl_id, dx_pool* out) {
+                             void* side_stream, const void* nccl_id, dx_pool* out, const char* ssd_path = nullptr,
+                             int ssd_slots = 0) {
     dx_status st = validate(cfg);
     if (st != DX_OK) return st;
     DX_CHECK(master && out, DX_ERR_INVALID_ARG, "null master/out");
@@ -559,18 +643,34 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     }
 
     // ---- HIGH image sources (the DRAM cache)
-    p->hi_img_host.resize((size_t)L * E);
-    if (cfg->high_bits < 16) {
+    p->img_bytes = p->hi.bits == 16 ? (size_t)3 * p->I * p->H * 2 : (size_t)p->hi.bytes;
+    p->hi_img_host.assign((size_t)L * E, nullptr);
+    const bool ssd = ssd_path != nullptr;
+    if (ssd) {
+        // f-4: every HIGH image in one file (written below), a pinned LRU cache of ssd_slots images in front
+        p->ssd_fd = open(ssd_path, O_RDWR | O_CREAT | O_TRUNC, 0600);
+        if (p->ssd_fd < 0) { dx_set_error("cannot create the SSD tier file %s", ssd_path); return fail(DX_ERR_INVALID_ARG); }
+        p->ssd_path = ssd_path;
+        p->ssd_slots = ssd_slots;
+        ce = cudaHostAlloc((void**)&p->ssd_cache, (size_t)ssd_slots * p->img_bytes, cudaHostAllocDefault);
+        if (ce != cudaSuccess) { dx_set_error("cudaHostAlloc SSD-tier DRAM cache: %s", cudaGetErrorString(ce)); return fail(DX_ERR_OOM); }
+        p->cache_slot_of.assign((size_t)L * E, -1);
+        p->cache_owner.assign(ssd_slots, -1);
+        p->cache_used.assign(ssd_slots, 0);
+        p->cache_ev.resize(ssd_slots);
+        for (int i = 0; i < ssd_slots; ++i) cudaEventCreateWithFlags(&p->cache_ev[i], cudaEventDisableTiming);
+    } else if (cfg->high_bits < 16) {
         ce = cudaHostAlloc((void**)&p->hi_cache, (size_t)L * E * p->hi.bytes, cudaHostAllocMapped | cudaHostAllocPortable);
         if (ce != cudaSuccess) { dx_set_error("cudaHostAlloc HIGH cache: %s", cudaGetErrorString(ce)); return fail(DX_ERR_OOM); }
     }
-    std::vector<const uint8_t*> img_dev((size_t)L * E);
+    std::vector<const uint8_t*> img_dev((size_t)L * E, nullptr);
     for (int l = 0; l < L; ++l)
         for (int e = 0; e < E; ++e) {
             const void* m = master[(size_t)l * E + e];
             if (!m) { dx_set_error("null master pointer (layer %d expert %d)", l, e); return fail(DX_ERR_INVALID_ARG); }
             const uint8_t* src_host;
             if (cfg->high_bits == 16) src_host = (const uint8_t*)m;
+            else if (ssd) continue;                  // int HIGH images go to the file as they are quantised
             else src_host = p->hi_cache + ((size_t)l * E + e) * p->hi.bytes;
             cudaPointerAttributes at;
             ce = cudaPointerGetAttributes(&at, src_host);
@@ -579,6 +679,7 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
                 dx_set_error("master image of layer %d expert %d is not pinned/mapped host memory", l, e);
                 return fail(DX_ERR_INVALID_ARG);
             }
+            if (ssd) continue;                       // promotions read the file through the cache, not the masters
             p->hi_img_host[(size_t)l * E + e] = src_host;
             img_dev[(size_t)l * E + e] = (const uint8_t*)at.devicePointer;
         }
@@ -640,11 +741,20 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
             uint8_t* low = p->weights + (size_t)l * p->layer_bytes + (size_t)e * p->lo.bytes;
             if (cfg->high_bits == 16) {
                 launch_quantize_slot(stage_master, bf, low, p->lo, p->H, p->I, p->g, p->cs);
+                if (ssd) {
+                    dx_status st2 = ssd_write(p, (size_t)l * E + e, master[(size_t)l * E + e]);
+                    if (st2 != DX_OK) return fail(st2);
+                }
             } else {
                 launch_quantize_slot(stage_master, bf, stage_high, p->hi, p->H, p->I, p->g, p->cs);
-                DX_CUDA(cudaMemcpyAsync(p->hi_cache + ((size_t)l * E + e) * p->hi.bytes, stage_high, p->hi.bytes,
-                                        cudaMemcpyDeviceToHost, p->cs));
+                uint8_t* dst = ssd ? p->ssd_cache : p->hi_cache + ((size_t)l * E + e) * p->hi.bytes;
+                DX_CUDA(cudaMemcpyAsync(dst, stage_high, p->hi.bytes, cudaMemcpyDeviceToHost, p->cs));
                 launch_quantize_slot(stage_high, p->hi, low, p->lo, p->H, p->I, p->g, p->cs);
+                if (ssd) {
+                    DX_CUDA(cudaStreamSynchronize(p->cs));
+                    dx_status st2 = ssd_write(p, (size_t)l * E + e, p->ssd_cache);
+                    if (st2 != DX_OK) return fail(st2);
+                }
             }
             p->launches += cfg->high_bits == 16 ? 3 : 6;
         }
@@ -658,6 +768,15 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     }
     DX_CUDA(cudaStreamSynchronize(p->cs));
     DX_CUDA(cudaGetLastError());
+    if (ssd) {
+        // the file is the SSD tier from here on: flush it and drop it from the page cache (reads are O_DIRECT when
+        // the image size allows, so a promotion that misses the DRAM cache really reads the device)
+        fsync(p->ssd_fd);
+        posix_fadvise(p->ssd_fd, 0, 0, POSIX_FADV_DONTNEED);
+        const int fd2 = open(ssd_path, O_RDONLY | O_DIRECT);
+        if (fd2 >= 0 && p->img_bytes % 4096 == 0) { close(p->ssd_fd); p->ssd_fd = fd2; p->ssd_direct = true; }
+        else if (fd2 >= 0) close(fd2);
+    }
 
     dx_info& inf = p->info;
     inf.n_hot = (int)n_hot;
@@ -703,6 +822,14 @@ extern "C" dx_status dx_pool_create_ep(const dx_config* cfg, const void* const* 
     return pool_create(cfg, master, compute_stream, side_stream, nccl_id, out);
 }
 
+extern "C" dx_status dx_pool_create_ssd(const dx_config* cfg, const void* const* master, void* compute_stream,
+                                        void* side_stream, const char* ssd_path, int32_t dram_cache_images, dx_pool* out) {
+    DX_CHECK(ssd_path && *ssd_path, DX_ERR_INVALID_ARG, "null SSD tier path");
+    DX_CHECK(dram_cache_images >= 1, DX_ERR_INVALID_ARG, "the DRAM cache needs at least one image slot");
+    DX_CHECK(cfg && cfg->ep_size == 1, DX_ERR_INVALID_ARG, "the SSD tier is for ep_size == 1 pools");
+    return pool_create(cfg, master, compute_stream, side_stream, nullptr, out, ssd_path, dram_cache_images);
+}
+
 extern "C" dx_status dx_get_unique_id(void* id128) {
     DX_CHECK(id128, DX_ERR_INVALID_ARG, "null id");
     return ep_nccl_unique_id(id128);
@@ -716,6 +843,9 @@ extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (p->ep_pairs_host) cudaFreeHost(p->ep_pairs_host);
     for (auto ev : p->ev_planh) cudaEventDestroy(ev);
     for (auto ev : p->ev_pf) cudaEventDestroy(ev);
+    for (auto ev : p->cache_ev) cudaEventDestroy(ev);
+    if (p->ssd_cache) cudaFreeHost(p->ssd_cache);
+    if (p->ssd_fd >= 0) { close(p->ssd_fd); unlink(p->ssd_path.c_str()); }
     if (p->pf_host) cudaFreeHost(p->pf_host);
     if (p->pf_n_host) cudaFreeHost(p->pf_n_host);
     if (p->ss2) { cudaStreamSynchronize(p->ss2); cudaStreamDestroy(p->ss2); }
@@ -824,6 +954,12 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
         out->xfer_max_ms = a > out->xfer_max_ms ? a : out->xfer_max_ms;
         out->plans += 1;
     }
+    out->ssd_reads = (int64_t)p->ssd_reads;
+    out->ssd_bytes = p->ssd_bytes;
+    out->ssd_read_ms = p->ssd_read_ms;
+    out->dram_cache_hits = (int64_t)p->cache_hits;
+    p->ssd_reads = p->ssd_bytes = p->cache_hits = 0;
+    p->ssd_read_ms = 0.0;
     out->prefetch_issued = (int64_t)p->pf_issued;
     out->prefetch_hits = (int64_t)p->pf_hits;
     p->pf_issued = p->pf_hits = 0;
@@ -934,8 +1070,8 @@ static dx_status issue_prefetch(dx_pool p, int layer) {
     p->staged[layer].clear();
     for (int i = 0; i < n; ++i) {
         const int4 c = p->pf_host[(size_t)layer * 8 + i];
-        DX_CUDA(cudaMemcpyAsync(hi_region + (size_t)c.y * p->hi.bytes, p->hi_img_host[(size_t)layer * p->E_loc + c.x],
-                                bytes, cudaMemcpyHostToDevice, p->ss));
+        dx_status rc = copy_high_image(p, (size_t)layer * p->E_loc + c.x, hi_region + (size_t)c.y * p->hi.bytes, p->ss);
+        if (rc != DX_OK) return rc;
         p->staged[layer].push_back(make_int2(c.x, c.y));
     }
     p->pf_issued += (u64)n;
@@ -1384,8 +1520,8 @@ static dx_status issue_transfers(dx_pool p, int layer) {
         bool hit = false;                          // staged by the prefetch into this very block already
         for (const int2& sg : p->staged[layer]) hit |= sg.x == cmd.x && sg.y == cmd.z;
         if (hit) { ++p->pf_hits; continue; }
-        DX_CUDA(cudaMemcpyAsync(hi_region + (size_t)cmd.z * p->hi.bytes, p->hi_img_host[layer * E + cmd.x], bytes,
-                                cudaMemcpyHostToDevice, p->ss));
+        dx_status rc = copy_high_image(p, layer * E + cmd.x, hi_region + (size_t)cmd.z * p->hi.bytes, p->ss);
+        if (rc != DX_OK) return rc;
         ++np;
     }
     if (x0 && np > 0) {
@@ -1447,7 +1583,24 @@ extern "C" dx_status dx_plan_precision(dx_pool p, int32_t layer, dx_plan* out) {
         // §3.5: tau_h and the initial HIGH set, installed synchronously before serving continues
         launch_plan(p->ctrl, layer, 1, p->cs);
         launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 1, p->cs);
-        launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 2, p->cs);
+        if (p->ssd_fd < 0) {
+            launch_transitions(p->ctrl, layer, xfer_args(p, layer), p->E_loc, 2, p->cs);
+        } else {
+            // f-4: the initial HIGH set comes from the SSD tier through the DRAM cache (copy engine, in order
+            // after the relayout moves on the compute stream)
+            const size_t E = (size_t)p->E_loc;
+            DX_CUDA(cudaMemcpyAsync(p->plan_n_host + layer, p->ctrl.plan_n + layer, 4, cudaMemcpyDeviceToHost, p->cs));
+            DX_CUDA(cudaMemcpyAsync(p->plan_host + layer * E, p->ctrl.plan_cmd + layer * E, E * sizeof(int4),
+                                    cudaMemcpyDeviceToHost, p->cs));
+            DX_CUDA(cudaStreamSynchronize(p->cs));
+            uint8_t* hi_region = p->weights + (size_t)layer * p->layer_bytes + p->hi_base;
+            for (int i = 0; i < p->plan_n_host[layer]; ++i) {
+                const int4 cmd = p->plan_host[layer * E + i];
+                if (cmd.y != 1) continue;
+                dx_status rc = copy_high_image(p, layer * E + cmd.x, hi_region + (size_t)cmd.z * p->hi.bytes, p->cs);
+                if (rc != DX_OK) return rc;
+            }
+        }
         p->launches += 3;
         p->finalized[layer] = 1;
         if (out) {
@@ -1508,7 +1661,23 @@ static dx_status manual(dx_pool p, int layer, const int32_t* experts, int n, int
     launch_manual(p->ctrl, layer, p->manual_cmds, n, p->manual_status, p->cs);
     DX_CUDA(cudaEventRecord(p->ev_plan, p->cs));
     DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_plan, 0));
-    launch_transitions(p->ctrl, layer, xfer_args(p, layer), n, 0, p->ss);
+    if (p->ssd_fd < 0) {
+        launch_transitions(p->ctrl, layer, xfer_args(p, layer), n, 0, p->ss);
+    } else {                                          // f-4: promotions through the SSD tier's DRAM cache
+        const size_t E = (size_t)p->E_loc;
+        launch_transitions(p->ctrl, layer, xfer_args(p, layer), n, 3, p->ss);     // demotions
+        DX_CUDA(cudaMemcpyAsync(p->plan_n_host + layer, p->ctrl.plan_n + layer, 4, cudaMemcpyDeviceToHost, p->cs));
+        DX_CUDA(cudaMemcpyAsync(p->plan_host + layer * E, p->ctrl.plan_cmd + layer * E, E * sizeof(int4),
+                                cudaMemcpyDeviceToHost, p->cs));
+        DX_CUDA(cudaStreamSynchronize(p->cs));
+        uint8_t* hi_region = p->weights + (size_t)layer * p->layer_bytes + p->hi_base;
+        for (int i = 0; i < p->plan_n_host[layer]; ++i) {
+            const int4 cmd = p->plan_host[layer * E + i];
+            if (cmd.y != 1) continue;
+            dx_status rc = copy_high_image(p, layer * E + cmd.x, hi_region + (size_t)cmd.z * p->hi.bytes, p->ss);
+            if (rc != DX_OK) return rc;
+        }
+    }
     DX_CUDA(cudaEventRecord(p->ev_side[layer], p->ss));
     p->launches += 2;
     p->publish_at[layer] = due;

@@ -68,7 +68,9 @@ class dx_profile_t(ctypes.Structure):
                 ("route_ms", ctypes.c_double), ("exposed_ms", ctypes.c_double), ("publishes", ctypes.c_int64),
                 ("xfer_ms", ctypes.c_double), ("xfer_max_ms", ctypes.c_double), ("plans", ctypes.c_int64),
                 ("promotions", ctypes.c_int64), ("demotions", ctypes.c_int64), ("copy_ms", ctypes.c_double),
-                ("copy_bytes", ctypes.c_uint64), ("prefetch_issued", ctypes.c_int64), ("prefetch_hits", ctypes.c_int64)]
+                ("copy_bytes", ctypes.c_uint64), ("prefetch_issued", ctypes.c_int64), ("prefetch_hits", ctypes.c_int64),
+                ("ssd_reads", ctypes.c_int64), ("ssd_bytes", ctypes.c_uint64), ("ssd_read_ms", ctypes.c_double),
+                ("dram_cache_hits", ctypes.c_int64)]
 
 
 class dx_plan(ctypes.Structure):
@@ -81,6 +83,7 @@ _P = ctypes.POINTER
 _SIG = {
     "dx_pool_create": [_P(dx_config), _vp, _vp, _vp, _P(_vp)],
     "dx_pool_create_ep": [_P(dx_config), _vp, _vp, _vp, _vp, _P(_vp)],
+    "dx_pool_create_ssd": [_P(dx_config), _vp, _vp, _vp, ctypes.c_char_p, _i32, _P(_vp)],
     "dx_get_unique_id": [_vp],
     "dx_pool_destroy": [_vp],
     "dx_pool_info": [_vp, _P(dx_info)],
@@ -191,13 +194,19 @@ def dx_dequantize(codes, scales, zeros, N, K, g, bits, w, stream=None):
 class Pool:
     """Owns one dx_pool; methods are the dx_* calls of include/dx.h with the pool bound."""
 
-    def __init__(self, cfg: dx_config, master_ptrs, compute_stream=None, side_stream=None, nccl_id: bytes = None):
-        """nccl_id (bytes from dx_get_unique_id): dx_pool_create_ep -- a collective over cfg.ep_size ranks."""
+    def __init__(self, cfg: dx_config, master_ptrs, compute_stream=None, side_stream=None, nccl_id: bytes = None,
+                 ssd_path: str = None, dram_cache_images: int = 0):
+        """nccl_id (bytes from dx_get_unique_id): dx_pool_create_ep -- a collective over cfg.ep_size ranks.
+        ssd_path: dx_pool_create_ssd with a DRAM cache of dram_cache_images HIGH images."""
         arr = (ctypes.c_void_p * len(master_ptrs))(*[int(p) for p in master_ptrs])
         self._keep = arr
         h = ctypes.c_void_p()
         self.cfg = cfg
-        if nccl_id is None:
+        if ssd_path is not None:
+            _check(_lib.dx_pool_create_ssd(ctypes.byref(cfg), ctypes.cast(arr, ctypes.c_void_p), _stream(compute_stream),
+                                           _stream(side_stream), ssd_path.encode(), dram_cache_images, ctypes.byref(h)),
+                   "dx_pool_create_ssd")
+        elif nccl_id is None:
             _check(_lib.dx_pool_create(ctypes.byref(cfg), ctypes.cast(arr, ctypes.c_void_p), _stream(compute_stream),
                                        _stream(side_stream), ctypes.byref(h)), "dx_pool_create")
         else:
@@ -365,4 +374,6 @@ class Pool:
                     active_experts=int(pr.active_experts), route_ms=pr.route_ms, exposed_ms=pr.exposed_ms,
                     publishes=pr.publishes, xfer_ms=pr.xfer_ms, xfer_max_ms=pr.xfer_max_ms, plans=pr.plans,
                     promotions=pr.promotions, demotions=pr.demotions, copy_ms=pr.copy_ms,
-                    copy_bytes=int(pr.copy_bytes), prefetch_issued=pr.prefetch_issued, prefetch_hits=pr.prefetch_hits)
+                    copy_bytes=int(pr.copy_bytes), prefetch_issued=pr.prefetch_issued, prefetch_hits=pr.prefetch_hits,
+                    ssd_reads=pr.ssd_reads, ssd_bytes=int(pr.ssd_bytes), ssd_read_ms=pr.ssd_read_ms,
+                    dram_cache_hits=pr.dram_cache_hits)
