@@ -126,8 +126,22 @@ dx_status dx_pool_info(dx_pool pool, dx_info* out);
  * layers in the same order (T may differ per rank, max_tokens may not).  ep_size = 1 with a communicator is a
  * valid loopback (self send/recv) that runs the same path on one GPU.  libnccl.so.2 is loaded at run time
  * (DX_NCCL_LIB overrides).  Errors: NCCL (library missing, init or collective failure), plus
- * dx_pool_create's. */
+ * dx_pool_create's.
+ * f-2: the dispatch sends each token's x row ONCE per owner rank however many of its k experts that
+ * rank owns, with per-entry metadata {local expert, gate, row}; results still return one row per entry.
+ * nccl_id = NULL creates a member of a LOCAL group instead (several ranks' pools in one process on one device,
+ * ep_rank = its index, sharing one compute stream): the same layer runs through dx_moe_step_group with the
+ * exchange done by device copies. */
 dx_status dx_get_unique_id(void* id128);
+/* dx_moe_step for all n = ep_size pools of a local group (created with dx_pool_create_ep(nccl_id = NULL)), one
+ * layer: host arrays of n entries (pool r serves x[r] [T[r]][H] -> y[r]; router_w / router_bias or logits per
+ * pool).  Same results as n processes running dx_moe_step over NCCL. */
+dx_status dx_moe_step_group(dx_pool* pools, int32_t n, int32_t layer, const void* const* x, const int32_t* T,
+                            const void* const* router_w, const float* const* router_bias, const float* const* logits,
+                            void* const* y);
+/* f-2 accounting of an EP pool since creation: x rows this rank sent (deduplicated) and dispatch entries (rows an
+ * undeduplicated exchange would have sent). */
+dx_status dx_ep_traffic(dx_pool pool, uint64_t* rows_sent, uint64_t* entries_sent);
 /* f-4 SSD tier ("stored on SSD and cached in DRAM"): dx_pool_create plus a file at ssd_path that
  * the library creates and fills with every expert's HIGH image at create time (it is removed at destroy), and a
  * pinned DRAM cache of dram_cache_images HIGH images in front of it (LRU).  Every promotion (plans, the warm-up

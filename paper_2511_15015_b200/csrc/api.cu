@@ -101,9 +101,14 @@ struct dx_pool_s {
     // expert parallelism over NCCL (ep_nccl.cu): library-owned communicator and exchange buffers
     void* comm = nullptr;
     __nv_bfloat16 *ep_send_rows = nullptr, *ep_recv_rows = nullptr, *ep_y_rows = nullptr, *ep_back_rows = nullptr;
-    int2 *ep_send_meta = nullptr, *ep_recv_meta = nullptr;
-    int32_t* ep_pairs = nullptr;            // device [2][G] int2: my {count, T} per peer | received per peer
+    int4 *ep_send_meta = nullptr, *ep_recv_meta = nullptr;   // per entry {local expert, gate bits, row in block}
+    int2* ep_meta2 = nullptr;               // owner side: {expert, gate} of the received entries
+    int32_t* ep_rowmap = nullptr;           // owner side: the received row of each received entry (f-2)
+    int32_t* ep_mark = nullptr;             // source side: [G][T] dedup marks -> rows within owner blocks
+    int32_t* ep_pairs = nullptr;            // device [2][G][3]: my {unique rows, entries, T} per peer | received
     int32_t* ep_pairs_host = nullptr;       // pinned mirror (the v1 host synchronisation point)
+    bool ep_group = false;                  // EP buffers without a communicator: member of a local pool group
+    u64 ep_rows_sent = 0, ep_entries_sent = 0;   // f-2 accounting (rows actually moved vs one row per entry)
     u64 copy_promotions = 0;                // promotions issued as copy-engine H2D copies
     // f-4 SSD tier (dx_pool_create_ssd): every HIGH image in one file, a pinned DRAM cache of `ssd_slots` images
     // in front of it (LRU; a slot is reused only after the copies out of it completed)
@@ -425,7 +430,7 @@ static dx_status copy_high_image(dx_pool p, size_t key, uint8_t* dst, cudaStream
 
 static dx_status pool_create(const dx_config* cfg, const void* const* master, void* compute_stream,
                              void* side_stream, const void* nccl_id, dx_pool* out, const char* ssd_path = nullptr,
-                             int ssd_slots = 0) {
+                             int ssd_slots = 0, bool ep_group = false) {
     dx_status st = validate(cfg);
     if (st != DX_OK) return st;
     DX_CHECK(master && out, DX_ERR_INVALID_ARG, "null master/out");
@@ -466,7 +471,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     // ---- the one device allocation: weights | controller | workspace | staging
     const int T = cfg->max_tokens, k = p->k, L = p->L;
     const int G = cfg->ep_size;
-    const bool ep = G > 1 || nccl_id != nullptr;     // dispatch-side workspace (and NCCL buffers with an id)
+    const bool ep_bufs = nccl_id != nullptr || ep_group;   // exchange buffers (NCCL or a local pool group)
+    const bool ep = G > 1 || ep_bufs;                // dispatch-side workspace
     // entries (rows) one forward can see: T*k locally; an EP owner receives up to G*T*min(k, E_loc) rows
     const int ns = cfg->n_shared;              // f-3: the shared expert's T rows follow the T*k routed entries
     const size_t n_ent = G > 1 ? std::max((size_t)T * k, (size_t)G * T * std::min(k, E)) : (size_t)T * (k + ns);
@@ -484,8 +490,9 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     if (ep)      // dispatch-side routing workspace (global experts, local tokens)
         ws_bytes += lg_rows * p->E * 4 + (size_t)T * k * 22 + 3 * 256 + (size_t)route_blocks(T) * p->E * 8 +
                     (size_t)(p->E + 1) * 8 + (size_t)p->E * 4 + 64 * 256;
-    if (nccl_id) // NCCL exchange buffers: send / back rows (T*k), receive / result rows (n_ent), metadata, counts
-        ws_bytes += (size_t)T * k * (2 * p->H * 2 + 8) + n_ent * (2 * p->H * 2 + 8) + (size_t)G * 16 + 6 * 256;
+    if (ep_bufs) // EP exchange buffers: send / back rows (T*k), receive / result rows (n_ent), metadata, counts, marks
+        ws_bytes += (size_t)T * k * (2 * p->H * 2 + 16) + n_ent * (2 * p->H * 2 + 16 + 8 + 4) + (size_t)G * 24 +
+                    (size_t)G * T * 4 + 8 * 256;
     const size_t stage_bytes = (size_t)3 * p->I * p->H * 2 + p->hi.bytes + 2048 +
                                (size_t)(L > 1 ? L - 1 : 0) * E * E * 4 + (size_t)2 * T * k * 4 + (size_t)L * (8 * 16 + 4) + 4 * 256;
     const size_t ptr_bytes = (size_t)L * E * sizeof(void*) + 256;
@@ -556,14 +563,18 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         v.gm = carve<uint32_t>(q, (size_t)T * k);
         v.gbar = carve<unsigned>(q, 2);
     }
-    if (nccl_id) {
+    if (ep_bufs) {
         p->ep_send_rows = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
         p->ep_back_rows = carve<__nv_bfloat16>(q, (size_t)T * k * p->H);
-        p->ep_send_meta = carve<int2>(q, (size_t)T * k);
+        p->ep_send_meta = carve<int4>(q, (size_t)T * k);
         p->ep_recv_rows = carve<__nv_bfloat16>(q, n_ent * p->H);
         p->ep_y_rows = carve<__nv_bfloat16>(q, n_ent * p->H);
-        p->ep_recv_meta = carve<int2>(q, n_ent);
-        p->ep_pairs = carve<int32_t>(q, (size_t)4 * G);
+        p->ep_recv_meta = carve<int4>(q, n_ent);
+        p->ep_meta2 = carve<int2>(q, n_ent);
+        p->ep_rowmap = carve<int32_t>(q, n_ent);
+        p->ep_mark = carve<int32_t>(q, (size_t)G * T);
+        p->ep_pairs = carve<int32_t>(q, (size_t)6 * G);
+        p->ep_group = ep_group;
     }
     p->act = carve<__nv_bfloat16>(q, n_ent * p->I);
     p->Y = carve<__nv_bfloat16>(q, n_ent * p->H);
@@ -632,12 +643,14 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         dx_set_error("cudaHostAlloc(plan mirror) failed");
         return fail(DX_ERR_OOM);
     }
-    if (nccl_id) {
-        // collective: every rank of the EP group creates its pool with the same id (blocks until all joined)
-        if (cudaHostAlloc((void**)&p->ep_pairs_host, (size_t)4 * G * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
+    if (ep_bufs) {
+        if (cudaHostAlloc((void**)&p->ep_pairs_host, (size_t)6 * G * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
             dx_set_error("cudaHostAlloc(EP counts) failed");
             return fail(DX_ERR_OOM);
         }
+    }
+    if (nccl_id) {
+        // collective: every rank of the EP group creates its pool with the same id (blocks until all joined)
         st = ep_nccl_init(nccl_id, G, cfg->ep_rank, &p->comm);
         if (st != DX_OK) return fail(st);
     }
@@ -806,6 +819,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
 extern "C" dx_status dx_set_ffn_path(dx_pool p, int32_t path) {
     DX_CHECK(p, DX_ERR_INVALID_ARG, "null pool");
     DX_CHECK(path == 0 || p->cfg.n_shared == 0, DX_ERR_INVALID_ARG, "the shared expert runs on the tcgen05 path only");
+    DX_CHECK(path == 0 || !(p->comm || p->ep_group), DX_ERR_INVALID_ARG,
+             "the in-library EP layer (deduplicated rows) runs on the tcgen05 path only");
     DX_CHECK(path == 0 || path == 1, DX_ERR_INVALID_ARG, "path must be 0 (tcgen05) or 1 (mma.sync)");
     p->ffn_path = path;
     return DX_OK;
@@ -818,8 +833,8 @@ extern "C" dx_status dx_pool_create(const dx_config* cfg, const void* const* mas
 
 extern "C" dx_status dx_pool_create_ep(const dx_config* cfg, const void* const* master, void* compute_stream,
                                        void* side_stream, const void* nccl_id, dx_pool* out) {
-    DX_CHECK(nccl_id, DX_ERR_INVALID_ARG, "null nccl_id (use dx_pool_create without expert parallelism)");
-    return pool_create(cfg, master, compute_stream, side_stream, nccl_id, out);
+    // nccl_id NULL: a member of a local pool group (several ranks' pools in one process, dx_moe_step_group)
+    return pool_create(cfg, master, compute_stream, side_stream, nccl_id, out, nullptr, 0, nccl_id == nullptr);
 }
 
 extern "C" dx_status dx_pool_create_ssd(const dx_config* cfg, const void* const* master, void* compute_stream,
@@ -1304,7 +1319,7 @@ extern "C" dx_status dx_ep_dispatch(dx_pool p, int32_t layer, const void* x, int
 }
 
 static dx_status routed_impl(dx_pool p, int32_t layer, const void* rows, int32_t R, const void* meta, void* y_rows,
-                             int64_t tokens_global) {
+                             int64_t tokens_global, const int32_t* rowmap = nullptr) {
     CHECK_LAYER(p, layer);
     DX_CHECK(R >= 0 && (size_t)R <= p->n_ent, DX_ERR_RANGE, "R=%d exceeds the workspace (%zu rows)", R, p->n_ent);
     DX_CHECK(tokens_global >= 0, DX_ERR_INVALID_ARG, "tokens_global < 0");
@@ -1320,7 +1335,7 @@ static dx_status routed_impl(dx_pool p, int32_t layer, const void* rows, int32_t
     // the sticky device error that the next dx_sync reports as DX_ERR_RANGE
     launch_route_given((const int2*)meta, R, p->E_loc, ws, p->ctrl.cnt + base, p->ctrl.mass + base,
                        p->ctrl.tier + base, p->wbytes, p->dev_err, p->cs);
-    launch_place(R, p->E_loc, 1, ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs);
+    launch_place(R, p->E_loc, 1, ws, (const __nv_bfloat16*)rows, p->H, p->ffn_path == 1 ? nullptr : p->Xp, p->cs, rowmap);
     p->launches += 3;
     // an expert receives at most one row per token of the step: m_e <= min(R, tokens_global)
     return expert_ffn(p, layer, ws, rows, R, 1, y_rows, ev, false,
@@ -1333,54 +1348,213 @@ extern "C" dx_status dx_moe_forward_routed(dx_pool p, int32_t layer, const void*
     return routed_impl(p, layer, rows, R, meta, y_rows, tokens_global);
 }
 
-// One EP layer inside the library (SURVEY §8(e) collective v1): dispatch over the global experts, NCCL count
-// exchange + one host synchronisation, grouped send/recv of rows and metadata, the owner-side FFN on the received
-// rows (hotness counted here, B_tot = the global token count), the return exchange, the rank-order combine.
+// Source side of the in-library EP layer: routing over the global experts and the placement (entries sorted by
+// expert = grouped by owner), then the f-2 deduplication: one x row per (token, owner) into ep_send_rows, per-entry
+// metadata {local expert, gate bits, row within the owner block} into ep_send_meta, and the per-owner triples
+// {unique rows, entries, T} into ep_pairs[0 .. 3G).
+static dx_status ep_dispatch_dedup(dx_pool p, int layer, const void* x, int T, const void* router_w,
+                                   const float* router_bias, const float* logits, int32_t* topk_idx, float* topk_gate) {
+    const int G = p->cfg.ep_size;
+    p->ep_T = T;
+    if (T == 0) {
+        DX_CUDA(cudaMemsetAsync(p->ep_pairs, 0, sizeof(int32_t) * 3 * G, p->cs));
+        return DX_OK;
+    }
+    RouteWs ws = p->ws_src;
+    if (topk_idx) ws.idx = topk_idx;
+    if (topk_gate) ws.gate = topk_gate;
+    p->ws_src_live = ws;
+    const float* lg = logits;
+    if (router_w) {
+        launch_router((const __nv_bfloat16*)x, (const __nv_bfloat16*)router_w, router_bias, T, p->E, p->H, ws.logits,
+                      p->cs);
+        lg = ws.logits;
+        p->launches += 1;
+    }
+    const u64 nob[2][2] = {{0, 0}, {0, 0}};
+    launch_route(lg, T, p->E, p->k, 0, ws, nullptr, nullptr, nullptr, nob, p->cs);
+    launch_place(T, p->E, p->k, ws, nullptr, p->H, nullptr, p->cs);          // perm / inv only
+    launch_dedup_dispatch(ws, T, p->k, p->E_loc, G, (const __nv_bfloat16*)x, p->H, p->ep_mark, p->ep_pairs,
+                          p->ep_send_rows, p->ep_send_meta, p->cs);
+    p->launches += 7;
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "EP dispatch launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+// Host bookkeeping of one local pool's exchange: rows (deduplicated) and entries to / from every peer.
+struct EpPlan {
+    std::vector<int> su, se, suoff, seoff, ru, re, ruoff, reoff;
+    int64_t tokens_global = 0;
+    int R = 0, U = 0;
+};
+static void ep_plan_from(int G, const int32_t* send3, const int32_t* recv3, EpPlan& q) {
+    q.su.assign(G, 0); q.se.assign(G, 0); q.suoff.assign(G + 1, 0); q.seoff.assign(G + 1, 0);
+    q.ru.assign(G, 0); q.re.assign(G, 0); q.ruoff.assign(G + 1, 0); q.reoff.assign(G + 1, 0);
+    q.tokens_global = 0;
+    for (int r = 0; r < G; ++r) {
+        q.su[r] = send3[3 * r]; q.se[r] = send3[3 * r + 1];
+        q.ru[r] = recv3[3 * r]; q.re[r] = recv3[3 * r + 1];
+        q.tokens_global += recv3[3 * r + 2];
+        q.suoff[r + 1] = q.suoff[r] + q.su[r]; q.seoff[r + 1] = q.seoff[r] + q.se[r];
+        q.ruoff[r + 1] = q.ruoff[r] + q.ru[r]; q.reoff[r + 1] = q.reoff[r] + q.re[r];
+    }
+    q.R = q.reoff[G];
+    q.U = q.ruoff[G];
+}
+
+// One expert-parallel layer (SURVEY §8(e) collective v1 + f-2 row deduplication) for n local pools: n = 1 with an
+// NCCL communicator (one process per GPU), or all G ranks' pools of a local group (one process, one device, the
+// exchange done by device copies).  Dispatch, the count exchange and ONE host synchronisation, the exchange of
+// deduplicated rows and per-entry metadata, the owner-side FFN (hotness counted there with B_tot = the global
+// token count), the return of one result row per entry, the rank-order combine (and fold).
+static dx_status ep_layer(dx_pool* P, int n, int layer, const void* const* x, const int* T, const void* const* rw,
+                          const float* const* rb, const float* const* lg, void* const* y, int32_t* const* topk_idx,
+                          float* const* topk_gate, bool fuse_fold) {
+    dx_pool p0 = P[0];
+    const int G = p0->cfg.ep_size, k = p0->k, H = p0->H;
+    const bool nccl = p0->comm != nullptr;
+    DX_CHECK(nccl ? n == 1 : n == G, DX_ERR_INVALID_ARG, "an EP group call needs all %d ranks' pools (got %d)", G, n);
+    for (int r = 0; r < n; ++r) {
+        DX_CHECK(P[r] && (P[r]->comm || P[r]->ep_group) && P[r]->cfg.ep_size == G, DX_ERR_INVALID_ARG,
+                 "pool %d is not an EP pool of size %d", r, G);
+        DX_CHECK(nccl || (P[r]->cfg.ep_rank == r && P[r]->cs == p0->cs), DX_ERR_INVALID_ARG,
+                 "local group: pool %d must have ep_rank %d and share the first pool's compute stream", r, r);
+        DX_CHECK(layer >= 0 && layer < P[r]->L, DX_ERR_RANGE, "layer %d out of range", layer);
+        DX_CHECK(T[r] >= 0 && T[r] <= P[r]->cfg.max_tokens, DX_ERR_RANGE, "T=%d outside [0, max_tokens]", T[r]);
+        DX_CHECK(T[r] == 0 || (x[r] && y[r] && ((rw && rw[r]) != (lg && lg[r]))), DX_ERR_INVALID_ARG,
+                 "pool %d: null x/y or not exactly one of router_w / logits", r);
+        dx_status st = poll_transfers(P[r]);
+        if (st != DX_OK) return st;
+    }
+    // 1. dispatch
+    for (int r = 0; r < n; ++r) {
+        dx_status st = ep_dispatch_dedup(P[r], layer, x[r], T[r], rw ? rw[r] : nullptr, rb ? rb[r] : nullptr,
+                                         lg ? lg[r] : nullptr, topk_idx ? topk_idx[r] : nullptr,
+                                         topk_gate ? topk_gate[r] : nullptr);
+        if (st != DX_OK) return st;
+    }
+    // 2. counts: {unique rows, entries, T} per peer, then the host synchronisation
+    std::vector<EpPlan> plan(n);
+    if (nccl) {
+        dx_pool p = p0;
+        dx_status st = ep_nccl_exchange_counts(p->comm, G, 3, p->ep_pairs, p->ep_pairs + 3 * G, p->cs);
+        if (st != DX_OK) return st;
+        DX_CUDA(cudaMemcpyAsync(p->ep_pairs_host, p->ep_pairs, sizeof(int32_t) * 6 * G, cudaMemcpyDeviceToHost, p->cs));
+        DX_CUDA(cudaStreamSynchronize(p->cs));
+        ep_plan_from(G, p->ep_pairs_host, p->ep_pairs_host + 3 * G, plan[0]);
+    } else {
+        for (int r = 0; r < n; ++r)
+            DX_CUDA(cudaMemcpyAsync(P[r]->ep_pairs_host, P[r]->ep_pairs, sizeof(int32_t) * 3 * G, cudaMemcpyDeviceToHost,
+                                    p0->cs));
+        DX_CUDA(cudaStreamSynchronize(p0->cs));
+        for (int d = 0; d < n; ++d) {
+            std::vector<int32_t> recv3(3 * G);
+            for (int s = 0; s < n; ++s)
+                for (int c = 0; c < 3; ++c) recv3[3 * s + c] = P[s]->ep_pairs_host[3 * d + c];
+            ep_plan_from(G, P[d]->ep_pairs_host, recv3.data(), plan[d]);
+        }
+    }
+    for (int r = 0; r < n; ++r) {
+        DX_CHECK(plan[r].seoff[G] == T[r] * k, DX_ERR_INVALID_ARG, "internal: %d entries dispatched != T*k = %d",
+                 plan[r].seoff[G], T[r] * k);
+        DX_CHECK((size_t)plan[r].R <= P[r]->n_ent, DX_ERR_RANGE,
+                 "received %d entries > workspace %zu (max_tokens must be the same on every rank)", plan[r].R, P[r]->n_ent);
+        P[r]->ep_rows_sent += (u64)plan[r].suoff[G];
+        P[r]->ep_entries_sent += (u64)plan[r].seoff[G];
+    }
+    // 3. rows + metadata
+    if (nccl) {
+        dx_pool p = p0;
+        const EpPlan& q = plan[0];
+        dx_status st = ep_nccl_exchange_rows(p->comm, G, H, p->ep_send_rows, q.su.data(), q.suoff.data(), p->ep_recv_rows,
+                                             q.ru.data(), q.ruoff.data(), p->ep_send_meta, q.se.data(), q.seoff.data(),
+                                             p->ep_recv_meta, q.re.data(), q.reoff.data(), 4, p->cs);
+        if (st != DX_OK) return st;
+    } else {
+        for (int s = 0; s < n; ++s)
+            for (int d = 0; d < n; ++d) {
+                const EpPlan &qs = plan[s], &qd = plan[d];
+                if (qs.su[d] > 0)
+                    DX_CUDA(cudaMemcpyAsync(P[d]->ep_recv_rows + (size_t)qd.ruoff[s] * H,
+                                            P[s]->ep_send_rows + (size_t)qs.suoff[d] * H, (size_t)qs.su[d] * H * 2,
+                                            cudaMemcpyDeviceToDevice, p0->cs));
+                if (qs.se[d] > 0)
+                    DX_CUDA(cudaMemcpyAsync(P[d]->ep_recv_meta + qd.reoff[s], P[s]->ep_send_meta + qs.seoff[d],
+                                            (size_t)qs.se[d] * sizeof(int4), cudaMemcpyDeviceToDevice, p0->cs));
+            }
+    }
+    // 4. owner-side FFN on the received entries (rows gathered through the dedup row map)
+    for (int r = 0; r < n; ++r) {
+        dx_pool p = P[r];
+        const EpPlan& q = plan[r];
+        launch_dedup_fix(p->ep_recv_meta, q.R, G, q.reoff.data(), q.ruoff.data(), p->ep_meta2, p->ep_rowmap, p->cs);
+        p->launches += 1;
+        dx_status st = routed_impl(p, layer, p->ep_recv_rows, q.R, p->ep_meta2, p->ep_y_rows, q.tokens_global,
+                                   p->ep_rowmap);
+        if (st != DX_OK) return st;
+    }
+    // 5. one result row per entry back to its source, in the source's dispatch order
+    if (nccl) {
+        dx_pool p = p0;
+        const EpPlan& q = plan[0];
+        dx_status st = ep_nccl_exchange_rows(p->comm, G, H, p->ep_y_rows, q.re.data(), q.reoff.data(), p->ep_back_rows,
+                                             q.se.data(), q.seoff.data(), nullptr, nullptr, nullptr, nullptr, nullptr,
+                                             nullptr, 0, p->cs);
+        if (st != DX_OK) return st;
+    } else {
+        for (int s = 0; s < n; ++s)
+            for (int d = 0; d < n; ++d) {
+                const EpPlan &qs = plan[s], &qd = plan[d];
+                if (qs.se[d] > 0)
+                    DX_CUDA(cudaMemcpyAsync(P[s]->ep_back_rows + (size_t)qs.seoff[d] * H,
+                                            P[d]->ep_y_rows + (size_t)qd.reoff[s] * H, (size_t)qs.se[d] * H * 2,
+                                            cudaMemcpyDeviceToDevice, p0->cs));
+            }
+    }
+    // 6. combine (+ fold)
+    for (int r = 0; r < n; ++r) {
+        dx_pool p = P[r];
+        if (fuse_fold) {
+            FoldReq req;
+            dx_status st = fold_prepare(p, layer, &req);
+            if (st != DX_OK) return st;
+            launch_combine(p->ep_back_rows, T[r], k, H, (__nv_bfloat16*)y[r], p->cs, p->ws_src_live.inv, &p->ctrl, &req);
+        } else if (T[r] > 0) {
+            launch_combine(p->ep_back_rows, T[r], k, H, (__nv_bfloat16*)y[r], p->cs, p->ws_src_live.inv);
+        }
+        p->launches += 1;
+    }
+    cudaError_t ce = cudaGetLastError();
+    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "EP layer launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
 static dx_status ep_forward(dx_pool p, int layer, const void* x, int T, const void* router_w, const float* router_bias,
                             const float* logits, void* y, int32_t* topk_idx, float* topk_gate, bool fuse_fold) {
-    const int G = p->cfg.ep_size, k = p->k;
-    dx_status st = ep_dispatch_impl(p, layer, x, T, router_w, router_bias, logits, p->ep_send_rows, p->ep_send_meta,
-                                    nullptr, p->ep_pairs, topk_idx, topk_gate);
+    DX_CHECK(p->comm, DX_ERR_INVALID_ARG, "a local-group EP pool runs through dx_moe_step_group");
+    return ep_layer(&p, 1, layer, &x, &T, router_w ? &router_w : nullptr, router_w ? &router_bias : nullptr,
+                    logits ? &logits : nullptr, &y, topk_idx ? &topk_idx : nullptr, topk_gate ? &topk_gate : nullptr,
+                    fuse_fold);
+}
+
+extern "C" dx_status dx_moe_step_group(dx_pool* pools, int32_t n, int32_t layer, const void* const* x, const int32_t* T,
+                                       const void* const* router_w, const float* const* router_bias,
+                                       const float* const* logits, void* const* y) {
+    DX_CHECK(pools && n >= 1 && n <= 8 && x && T && y, DX_ERR_INVALID_ARG, "bad group arguments");
+    dx_status st = ep_layer(pools, n, layer, x, T, router_w, router_bias, logits, y, nullptr, nullptr, true);
     if (st != DX_OK) return st;
-    int32_t* recv_pairs = p->ep_pairs + 2 * G;
-    st = ep_nccl_exchange_counts(p->comm, G, p->ep_pairs, recv_pairs, p->cs);
-    if (st != DX_OK) return st;
-    DX_CUDA(cudaMemcpyAsync(p->ep_pairs_host, p->ep_pairs, sizeof(int32_t) * 4 * G, cudaMemcpyDeviceToHost, p->cs));
-    DX_CUDA(cudaStreamSynchronize(p->cs));
-    std::vector<int> sc(G), rc(G), soff(G), roff(G);
-    int64_t tokens_global = 0;
-    int ns = 0, R = 0;
-    for (int r = 0; r < G; ++r) {
-        sc[r] = p->ep_pairs_host[2 * r];
-        rc[r] = p->ep_pairs_host[2 * G + 2 * r];
-        tokens_global += p->ep_pairs_host[2 * G + 2 * r + 1];
-        soff[r] = ns;
-        roff[r] = R;
-        ns += sc[r];
-        R += rc[r];
-    }
-    DX_CHECK(ns == T * k, DX_ERR_INVALID_ARG, "internal: dispatched %d rows != T*k = %d", ns, T * k);
-    DX_CHECK(R >= 0 && (size_t)R <= p->n_ent, DX_ERR_RANGE, "received %d rows > workspace %zu (max_tokens per rank "
-             "must be the same on every rank)", R, p->n_ent);
-    st = ep_nccl_exchange_rows(p->comm, G, p->H, p->ep_send_rows, p->ep_send_meta, sc.data(), soff.data(),
-                               p->ep_recv_rows, p->ep_recv_meta, rc.data(), roff.data(), p->cs);
-    if (st != DX_OK) return st;
-    st = routed_impl(p, layer, p->ep_recv_rows, R, p->ep_recv_meta, p->ep_y_rows, tokens_global);
-    if (st != DX_OK) return st;
-    st = ep_nccl_exchange_rows(p->comm, G, p->H, p->ep_y_rows, nullptr, rc.data(), roff.data(), p->ep_back_rows, nullptr,
-                               sc.data(), soff.data(), p->cs);
-    if (st != DX_OK) return st;
-    if (fuse_fold) {
-        FoldReq req;
-        st = fold_prepare(p, layer, &req);
+    for (int r = 0; r < n; ++r) {
+        st = dx_plan_precision(pools[r], layer, nullptr);
         if (st != DX_OK) return st;
-        launch_combine(p->ep_back_rows, T, k, p->H, (__nv_bfloat16*)y, p->cs, p->ws_src_live.inv, &p->ctrl, &req);
-    } else if (T > 0) {
-        launch_combine(p->ep_back_rows, T, k, p->H, (__nv_bfloat16*)y, p->cs, p->ws_src_live.inv);
     }
-    p->launches += 1;
-    cudaError_t ce = cudaGetLastError();
-    DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "EP combine launch failed: %s", cudaGetErrorString(ce));
+    return DX_OK;
+}
+
+extern "C" dx_status dx_ep_traffic(dx_pool p, uint64_t* rows_sent, uint64_t* entries_sent) {
+    DX_CHECK(p && rows_sent && entries_sent, DX_ERR_INVALID_ARG, "null argument");
+    *rows_sent = p->ep_rows_sent;
+    *entries_sent = p->ep_entries_sent;
     return DX_OK;
 }
 

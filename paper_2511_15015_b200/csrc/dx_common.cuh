@@ -235,8 +235,18 @@ void launch_route_dec(const __nv_bfloat16* x, const __nv_bfloat16* wr, const flo
                       int T, int E, int k, int H, int e_lo, const RouteWs& ws, uint32_t* cnt_acc, u64* mass_acc,
                       const int32_t* tier, const u64 (&bytes)[2][2], __nv_bfloat16* Xp, cudaStream_t st);
 // stable placement of every (t, j) entry; Xp != NULL also gathers x rows in permuted order
+// rowmap != NULL: entry i's source row is rowmap[i] (f-2 deduplicated EP rows) instead of i / k
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
-                  cudaStream_t st);
+                  cudaStream_t st, const int32_t* rowmap = nullptr);
+// f-2 deduplicated EP dispatch (source side, after routing + placement over global experts): mark [G][T] scratch,
+// triples [G][3] {unique rows, entries, T_src} per owner, send_rows (owner blocks in order), meta [T*k] int4
+// {local expert, gate bits, row within the owner block}
+void launch_dedup_dispatch(const RouteWs& ws, int T, int k, int E_loc, int G, const __nv_bfloat16* x, int H,
+                           int32_t* mark, int32_t* triples, __nv_bfloat16* send_rows, int4* meta, cudaStream_t st);
+// owner side: meta4 [R] (source order) -> meta2 {expert, gate} and rowmap (row among the received rows); eoff / roff:
+// per-source entry / row offsets, G + 1 values each (G <= 8)
+void launch_dedup_fix(const int4* meta4, int R, int G, const int32_t* eoff, const int32_t* roff, int2* meta2,
+                      int32_t* rowmap, cudaStream_t st);
 // a8 combine; with fold != NULL one extra block also runs the layer's EMA fold + publication (a10, a14)
 struct FoldReq {
     int layer;
@@ -264,10 +274,11 @@ int ep_nccl_version();
 dx_status ep_nccl_unique_id(void* id128);
 dx_status ep_nccl_init(const void* id128, int G, int rank, void** comm);
 void ep_nccl_destroy(void* comm);
-dx_status ep_nccl_exchange_counts(void* comm, int G, const int32_t* pairs, int32_t* recv_pairs, cudaStream_t st);
-dx_status ep_nccl_exchange_rows(void* comm, int G, int H, const void* send_rows, const void* send_meta,
-                                const int* sc, const int* soff, void* recv_rows, void* recv_meta, const int* rc,
-                                const int* roff, cudaStream_t st);
+dx_status ep_nccl_exchange_counts(void* comm, int G, int per, const int32_t* tup, int32_t* recv_tup, cudaStream_t st);
+dx_status ep_nccl_exchange_rows(void* comm, int G, int H, const void* send_rows, const int* sc, const int* soff,
+                                void* recv_rows, const int* rc, const int* roff, const void* send_meta, const int* se,
+                                const int* seoff, void* recv_meta, const int* re, const int* reoff, int mi,
+                                cudaStream_t st);
 // E: global expert count (range check), e_cnt: local experts counted ([e_lo, e_lo + e_cnt))
 void launch_counts_from(const int32_t* idx, const float* gate, int T, int E, int e_cnt, int k, int e_lo,
                         uint32_t* cnt_acc, u64* mass_acc, int32_t* err, cudaStream_t st);

@@ -127,45 +127,45 @@ void ep_nccl_destroy(void* comm) {
     if (comm && api().ok) api().CommDestroy(comm);
 }
 
-// pairs[d] = {rows for peer d, my T} -> recv_pairs[s] = {rows peer s sends me, peer s's T}
-dx_status ep_nccl_exchange_counts(void* comm, int G, const int32_t* pairs, int32_t* recv_pairs, cudaStream_t st) {
+// per-peer count tuples of `per` int32: tup[d] for peer d -> recv_tup[s] from peer s
+dx_status ep_nccl_exchange_counts(void* comm, int G, int per, const int32_t* tup, int32_t* recv_tup, cudaStream_t st) {
     NcclApi& a = api();
     if (a.AlltoAll) {
-        NCHECK(a.AlltoAll(pairs, recv_pairs, 2, NCCL_INT32, comm, st), "ncclAlltoAll(counts)");
+        NCHECK(a.AlltoAll(tup, recv_tup, (size_t)per, NCCL_INT32, comm, st), "ncclAlltoAll(counts)");
         return DX_OK;
     }
     NCHECK(a.GroupStart(), "ncclGroupStart");               // NCCL < 2.28: the same exchange as grouped send/recv
     for (int p = 0; p < G; ++p) {
-        NCHECK(a.Send(pairs + 2 * p, 2, NCCL_INT32, p, comm, st), "ncclSend(counts)");
-        NCHECK(a.Recv(recv_pairs + 2 * p, 2, NCCL_INT32, p, comm, st), "ncclRecv(counts)");
+        NCHECK(a.Send(tup + per * p, (size_t)per, NCCL_INT32, p, comm, st), "ncclSend(counts)");
+        NCHECK(a.Recv(recv_tup + per * p, (size_t)per, NCCL_INT32, p, comm, st), "ncclRecv(counts)");
     }
     NCHECK(a.GroupEnd(), "ncclGroupEnd");
     return DX_OK;
 }
 
-// rows of H bf16 plus one int2 of metadata per row (meta may be NULL: the return leg carries no metadata).
-// send block for peer d: rows [soff[d], soff[d] + sc[d]); receive block from peer s: [roff[s], roff[s] + rc[s])
-dx_status ep_nccl_exchange_rows(void* comm, int G, int H, const void* send_rows, const void* send_meta,
-                                const int* sc, const int* soff, void* recv_rows, void* recv_meta, const int* rc,
-                                const int* roff, cudaStream_t st) {
+// rows of H bf16 (block for peer p: [soff[p], soff[p] + sc[p]) out, [roff[p], roff[p] + rc[p]) in) and, when
+// send_meta != NULL, `mi` int32 of metadata per entry with separate entry counts/offsets (se/seoff, re/reoff: with
+// deduplicated rows a peer gets fewer rows than entries)
+dx_status ep_nccl_exchange_rows(void* comm, int G, int H, const void* send_rows, const int* sc, const int* soff,
+                                void* recv_rows, const int* rc, const int* roff, const void* send_meta, const int* se,
+                                const int* seoff, void* recv_meta, const int* re, const int* reoff, int mi,
+                                cudaStream_t st) {
     NcclApi& a = api();
     const size_t rb = (size_t)H * 2;
     NCHECK(a.GroupStart(), "ncclGroupStart");
     for (int p = 0; p < G; ++p) {
-        if (sc[p] > 0) {
+        if (sc[p] > 0)
             NCHECK(a.Send(static_cast<const uint8_t*>(send_rows) + (size_t)soff[p] * rb, (size_t)sc[p] * H, NCCL_BF16, p,
                           comm, st), "ncclSend(rows)");
-            if (send_meta)
-                NCHECK(a.Send(static_cast<const int2*>(send_meta) + soff[p], (size_t)sc[p] * 2, NCCL_INT32, p, comm, st),
-                       "ncclSend(meta)");
-        }
-        if (rc[p] > 0) {
+        if (send_meta && se[p] > 0)
+            NCHECK(a.Send(static_cast<const int32_t*>(send_meta) + (size_t)seoff[p] * mi, (size_t)se[p] * mi, NCCL_INT32,
+                          p, comm, st), "ncclSend(meta)");
+        if (rc[p] > 0)
             NCHECK(a.Recv(static_cast<uint8_t*>(recv_rows) + (size_t)roff[p] * rb, (size_t)rc[p] * H, NCCL_BF16, p, comm,
                           st), "ncclRecv(rows)");
-            if (recv_meta)
-                NCHECK(a.Recv(static_cast<int2*>(recv_meta) + roff[p], (size_t)rc[p] * 2, NCCL_INT32, p, comm, st),
-                       "ncclRecv(meta)");
-        }
+        if (recv_meta && re[p] > 0)
+            NCHECK(a.Recv(static_cast<int32_t*>(recv_meta) + (size_t)reoff[p] * mi, (size_t)re[p] * mi, NCCL_INT32, p,
+                          comm, st), "ncclRecv(meta)");
     }
     NCHECK(a.GroupEnd(), "ncclGroupEnd");
     return DX_OK;

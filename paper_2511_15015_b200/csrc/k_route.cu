@@ -608,7 +608,8 @@ __global__ void __launch_bounds__(256) k_scan_e(const int32_t* __restrict__ hist
 __global__ void __launch_bounds__(256) k_place(const int32_t* __restrict__ idx, int n, int nblk, int k,
                                                const int32_t* __restrict__ base, const int32_t* __restrict__ off,
                                                int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-                                               const __nv_bfloat16* __restrict__ x, int H, __nv_bfloat16* __restrict__ Xp) {
+                                               const __nv_bfloat16* __restrict__ x, int H, __nv_bfloat16* __restrict__ Xp,
+                                               const int32_t* __restrict__ rowmap) {
     DX_GRID_WAIT();
     DX_GRID_LAUNCH();
     const int lane = threadIdx.x & 31;
@@ -626,10 +627,91 @@ __global__ void __launch_bounds__(256) k_place(const int32_t* __restrict__ idx, 
         inv[i] = pos;
     }
     if (!Xp) return;
-    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)(i / k) * H);
+    const int srow = rowmap ? __ldcg(rowmap + i) : i / k;        // f-2: deduplicated EP rows
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)srow * H);
     uint4* dst = reinterpret_cast<uint4*>(Xp + (size_t)pos * H);
     for (int h = lane; h < H / 8; h += 32) dst[h] = __ldg(src + h);
 }
+
+// ------------------------------------------------------------------ f-2 deduplicated EP dispatch
+// Source side, after the routing over global experts and the placement (perm: entries sorted by expert, so owner d's
+// entries are positions [off[d*E_loc], off[(d+1)*E_loc])): token t is sent to owner d ONCE however many of its k
+// experts d owns.  mark[d][t] -> per-owner exclusive scan urow[d][t] (U_d rows) -> unique rows copied to the send
+// buffer (owner blocks in order) -> per-entry metadata {local expert, gate bits, row within the owner block}.
+__global__ void k_dedup_mark(const int32_t* __restrict__ idx, int n, int k, int E_loc, int T, int32_t* __restrict__ mark) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) mark[(size_t)(idx[i] / E_loc) * T + i / k] = 1;
+}
+__global__ void __launch_bounds__(256) k_dedup_scan(int32_t* __restrict__ mark, int T, const int32_t* __restrict__ off,
+                                                    int E_loc, int32_t* __restrict__ triples, int T_src) {
+    __shared__ int32_t tmp[32];
+    __shared__ int32_t total_s;
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int d = blockIdx.x;
+    int32_t run = 0;
+    for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
+        const int32_t v = t < T ? mark[(size_t)d * T + t] : 0;
+        const int32_t x = block_excl_scan<int32_t>(v, tmp, &total_s);
+        if (t < T) mark[(size_t)d * T + t] = v ? run + x : -1;      // row within owner d's block, -1: not sent
+        run += total_s;
+    }
+    if (threadIdx.x == 0) {                                         // {unique rows, entries, my T} for owner d
+        triples[3 * d] = run;
+        triples[3 * d + 1] = off[(d + 1) * E_loc] - off[d * E_loc];
+        triples[3 * d + 2] = T_src;
+    }
+}
+__global__ void k_dedup_rows(const int32_t* __restrict__ urow, int T, int G, const int32_t* __restrict__ triples,
+                             const __nv_bfloat16* __restrict__ x, int H, __nv_bfloat16* __restrict__ send_rows) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int lane = threadIdx.x & 31;
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= G * T) return;
+    const int d = w / T, t = w % T;
+    const int r = urow[(size_t)d * T + t];
+    if (r < 0) return;
+    int base = 0;
+    for (int q = 0; q < d; ++q) base += triples[3 * q];
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * H);
+    uint4* dst = reinterpret_cast<uint4*>(send_rows + (size_t)(base + r) * H);
+    for (int h = lane; h < H / 8; h += 32) dst[h] = __ldg(src + h);
+}
+__global__ void k_dedup_meta(const int32_t* __restrict__ perm, const int32_t* __restrict__ idx,
+                             const float* __restrict__ gate, const int32_t* __restrict__ urow, int n, int k, int E_loc,
+                             int T, int4* __restrict__ meta) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= n) return;
+    const int i = perm[pos];
+    const int e = idx[i];
+    const int d = e / E_loc;
+    meta[pos] = make_int4(e % E_loc, __float_as_int(gate[i]), urow[(size_t)d * T + i / k], 0);
+}
+// Owner side: received entries meta4[R] (in source order) with rows relative to their source's block; sources' entry
+// and row offsets in `so` ({entry offset, row offset} per source, G + 1 entries) -> meta2 {expert, gate} for the
+// owner-side routing and rowmap[i] = the entry's row among the received rows.
+struct SrcOffs {
+    int32_t e[9], r[9];
+};
+__global__ void k_dedup_fix(const int4* __restrict__ meta4, int R, int G, SrcOffs so, int2* __restrict__ meta2,
+                            int32_t* __restrict__ rowmap) {
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R) return;
+    int s = 0;
+    while (s + 1 < G && i >= so.e[s + 1]) ++s;
+    const int4 m = meta4[i];
+    meta2[i] = make_int2(m.x, m.y);
+    rowmap[i] = so.r[s] + m.z;
+}
+
 
 // ------------------------------------------------------------------ f-3 shared expert rows (Eq. 1 first sum)
 // After routing: entries n .. n+T-1 (n = T*k) are the shared expert's rows, one per token in order: perm, gate 1.0
@@ -875,11 +957,32 @@ void launch_route_dec(const __nv_bfloat16* x, const __nv_bfloat16* wr, const flo
 }
 
 void launch_place(int T, int E, int k, const RouteWs& ws, const __nv_bfloat16* x, int H, __nv_bfloat16* Xp,
-                  cudaStream_t st) {
+                  cudaStream_t st, const int32_t* rowmap) {
     if (T <= 0) return;
     const int n = T * k;
     dx_launch(k_place, dim3((n + 7) / 8), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.idx, n, route_blocks(T), k,
-              (const int32_t*)ws.base, (const int32_t*)ws.off, ws.perm, ws.inv, x, H, Xp);
+              (const int32_t*)ws.base, (const int32_t*)ws.off, ws.perm, ws.inv, x, H, Xp, rowmap);
+}
+
+void launch_dedup_dispatch(const RouteWs& ws, int T, int k, int E_loc, int G, const __nv_bfloat16* x, int H,
+                           int32_t* mark, int32_t* triples, __nv_bfloat16* send_rows, int4* meta, cudaStream_t st) {
+    if (T <= 0) return;
+    const int n = T * k;
+    cudaMemsetAsync(mark, 0, (size_t)G * T * sizeof(int32_t), st);
+    dx_launch(k_dedup_mark, dim3((n + 255) / 256), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.idx, n, k, E_loc, T, mark);
+    dx_launch(k_dedup_scan, dim3(G), dim3(256), 0, st, g_dx_pdl, mark, T, (const int32_t*)ws.off, E_loc, triples, T);
+    dx_launch(k_dedup_rows, dim3((G * T + 7) / 8), dim3(256), 0, st, g_dx_pdl, (const int32_t*)mark, T, G,
+              (const int32_t*)triples, x, H, send_rows);
+    dx_launch(k_dedup_meta, dim3((n + 255) / 256), dim3(256), 0, st, g_dx_pdl, (const int32_t*)ws.perm,
+              (const int32_t*)ws.idx, (const float*)ws.gate, (const int32_t*)mark, n, k, E_loc, T, meta);
+}
+
+void launch_dedup_fix(const int4* meta4, int R, int G, const int32_t* eoff, const int32_t* roff, int2* meta2,
+                      int32_t* rowmap, cudaStream_t st) {
+    if (R <= 0) return;
+    SrcOffs so{};
+    for (int s = 0; s <= G && s < 9; ++s) { so.e[s] = eoff[s]; so.r[s] = roff[s]; }
+    dx_launch(k_dedup_fix, dim3((R + 255) / 256), dim3(256), 0, st, g_dx_pdl, meta4, R, G, so, meta2, rowmap);
 }
 
 void launch_shared_rows(const RouteWs& ws, int T, int k, int E, int H, const __nv_bfloat16* x, __nv_bfloat16* Xp,

@@ -85,6 +85,8 @@ _SIG = {
     "dx_pool_create_ep": [_P(dx_config), _vp, _vp, _vp, _vp, _P(_vp)],
     "dx_pool_create_ssd": [_P(dx_config), _vp, _vp, _vp, ctypes.c_char_p, _i32, _P(_vp)],
     "dx_get_unique_id": [_vp],
+    "dx_moe_step_group": [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "dx_ep_traffic": [_vp, _vp, _vp],
     "dx_pool_destroy": [_vp],
     "dx_pool_info": [_vp, _P(dx_info)],
     "dx_moe_forward": [_vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -181,6 +183,16 @@ def dx_get_unique_id() -> bytes:
     return buf.raw
 
 
+def dx_moe_step_group(pools, layer, xs, Ts, ys, router_w=None, router_bias=None, logits=None):
+    """dx_moe_step for every pool of a local EP group (lists, one entry per rank)."""
+    n = len(pools)
+    arr = lambda v: None if v is None else (ctypes.c_void_p * n)(*[_ptr(q) for q in v])
+    hp = (ctypes.c_void_p * n)(*[q.h for q in pools])
+    Ta = (ctypes.c_int32 * n)(*Ts)
+    _check(_lib.dx_moe_step_group(hp, n, layer, arr(xs), Ta, arr(router_w), arr(router_bias), arr(logits), arr(ys)),
+           "dx_moe_step_group")
+
+
 def dx_quantize(w, N, K, g, bits, codes, scales, zeros, stream=None):
     _check(_lib.dx_quantize(_ptr(w), N, K, g, bits, _ptr(codes), _ptr(scales), _ptr(zeros), _stream(stream)),
            "dx_quantize")
@@ -196,13 +208,17 @@ class Pool:
 
     def __init__(self, cfg: dx_config, master_ptrs, compute_stream=None, side_stream=None, nccl_id: bytes = None,
                  ssd_path: str = None, dram_cache_images: int = 0):
-        """nccl_id (bytes from dx_get_unique_id): dx_pool_create_ep -- a collective over cfg.ep_size ranks.
+        """nccl_id (bytes from dx_get_unique_id): dx_pool_create_ep -- a collective over cfg.ep_size ranks;
+        nccl_id = b"local": a member of a local EP group (dx_moe_step_group).
         ssd_path: dx_pool_create_ssd with a DRAM cache of dram_cache_images HIGH images."""
         arr = (ctypes.c_void_p * len(master_ptrs))(*[int(p) for p in master_ptrs])
         self._keep = arr
         h = ctypes.c_void_p()
         self.cfg = cfg
-        if ssd_path is not None:
+        if nccl_id == b"local":
+            _check(_lib.dx_pool_create_ep(ctypes.byref(cfg), ctypes.cast(arr, ctypes.c_void_p), _stream(compute_stream),
+                                          _stream(side_stream), None, ctypes.byref(h)), "dx_pool_create_ep(local)")
+        elif ssd_path is not None:
             _check(_lib.dx_pool_create_ssd(ctypes.byref(cfg), ctypes.cast(arr, ctypes.c_void_p), _stream(compute_stream),
                                            _stream(side_stream), ssd_path.encode(), dram_cache_images, ctypes.byref(h)),
                    "dx_pool_create_ssd")
@@ -357,6 +373,11 @@ class Pool:
         ex, bl, n = np.zeros(8, np.int32), np.zeros(8, np.int32), ctypes.c_int32()
         _check(_lib.dx_get_prefetch(self.h, layer, ex.ctypes.data, bl.ctypes.data, ctypes.byref(n)), "dx_get_prefetch")
         return list(zip(ex[:n.value].tolist(), bl[:n.value].tolist()))
+
+    def dx_ep_traffic(self):
+        rows, ents = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_lib.dx_ep_traffic(self.h, ctypes.byref(rows), ctypes.byref(ents)), "dx_ep_traffic")
+        return dict(rows_sent=rows.value, entries_sent=ents.value)
 
     def dx_set_teleport(self, on: bool):
         """Timing baseline only: plans publish on schedule but no transfer runs (weights become garbage)."""

@@ -128,3 +128,60 @@ def test_ep_nccl_loopback_matches_single_pool(dx, router):
     assert transitions > 0
     ep_pool.close()
     plain.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_ep_local_group_dedup_in_library(dx, G):
+    """The in-library EP layer (the same code as the NCCL path, f-2 deduplicated dispatch) for G ranks' pools in one
+    process (dx_moe_step_group: the exchange by device copies): owner-side counters and EMA scores bit-exact to the
+    oracle over the global batch, plans and tables equal to the oracle controller per rank, y within 2e-2 of the
+    oracle, bitwise equal to a single pool while every expert is LOW; and fewer x rows sent than dispatch entries."""
+    E, k, H, I, g, T, W = 16, 4, 256, 128, 64, 24, 3
+    e_loc = E // G
+    n_hot_loc = max(1, e_loc // 4)
+    m = Masters(6, 1, E, H, I)
+    ptrs = m.ptrs()
+    pools = []
+    for r in range(G):
+        cfg = make_cfg(dx, 1, E, k, H, I, g, 16, 4, budget_for(e_loc, H, I, g, 16, 4, n_hot_loc, 1), 1, 0.9, 2, W, 2, 1, T)
+        cfg.ep_rank, cfg.ep_size = r, G
+        pools.append(dx.Pool(cfg, ptrs[r * e_loc:(r + 1) * e_loc], torch.cuda.current_stream(), nccl_id=b"local"))
+    cfg1 = make_cfg(dx, 1, E, k, H, I, g, 16, 4, budget_for(E, H, I, g, 16, 4, G * n_hot_loc, 1), 1, 0.9, 2, W, 2, 1,
+                    G * T)
+    single = dx.Pool(cfg1, ptrs, torch.cuda.current_stream())
+    ctrls = [oracle.Controller(e_loc, pools[r].info.n_hot, 1, 0.9, 2, W, 2, 1) for r in range(G)]
+    ys = [torch.zeros(T, H, dtype=torch.bfloat16, device="cuda") for _ in range(G)]
+    y1 = torch.zeros(G * T, H, dtype=torch.bfloat16, device="cuda")
+    for step in range(10):
+        lgs = [synth.trace_logits(6, 0, step * G + r, T, E, 1.2) for r in range(G)]
+        xs = [synth.normal_bf16(6, 1, step * G + r, 0, (T, H)) for r in range(G)]
+        tabs = [pools[r].dx_get_table(0) for r in range(G)]
+        xd = [bf16_dev(x) for x in xs]
+        dx.dx_moe_step_group(pools, 0, xd, [T] * G, ys, logits=[torch.from_numpy(lg).cuda() for lg in lgs])
+        lg_all, x_all = np.concatenate(lgs), np.concatenate(xs)
+        idx_o, gate_o = oracle.route(lg_all, k)
+        tier_of = {r * e_loc + e: bool(tabs[r]["tier"][e]) for r in range(G) for e in range(e_loc)}
+        Wt = {int(e): oracle.expert_tier(m.get(0, int(e)), H, I, g, 16, 4, tier_of[int(e)]) for e in np.unique(idx_o)}
+        _, y_o = oracle.moe_ffn(x_all, idx_o, gate_o, Wt, H, I, nthreads=8)
+        y_ep = np.concatenate([to_u16(y) for y in ys])
+        assert rel_err(y_ep, y_o) <= 2e-2, step
+        if step < W:                       # all LOW on both sides: bitwise the single-pool layer
+            single.dx_moe_forward(0, bf16_dev(x_all), G * T, y1, logits=torch.from_numpy(lg_all).cuda())
+            single.dx_hotness_update(0)
+            assert np.array_equal(to_u16(y1), y_ep), step
+        _, mass_all = oracle.counts(idx_o, gate_o, E)
+        for r in range(G):
+            ctrls[r].fold(mass_all[r * e_loc:(r + 1) * e_loc], G * T)
+            ctrls[r].plan()
+            st = ctrls[r].state()
+            hot = pools[r].dx_get_hotness(0)
+            assert np.array_equal(hot["S"].view(np.uint64), st["S"].view(np.uint64)), (step, r)
+            tab = pools[r].dx_get_table(0)
+            assert np.array_equal(tab["tier"], st["tier"]) and np.array_equal(tab["slot"], st["slot"]), (step, r)
+    tr = [p.dx_ep_traffic() for p in pools]
+    rows, ents = sum(t["rows_sent"] for t in tr), sum(t["entries_sent"] for t in tr)
+    print(f"EP local group G={G}: {rows} x rows sent for {ents} dispatch entries ({ents / max(rows, 1):.2f}x fewer)")
+    assert ents == 10 * G * T * k and rows < ents
+    for p in pools:
+        p.close()
+    single.close()
