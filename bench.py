@@ -513,6 +513,92 @@ def run_ours(a, rank, world, local_rank):
     return out
 
 
+def c4_ep_local_leg(a, peak, L=4):
+    """C4 on ONE GPU: the Qwen3-Next-80B-A3B-shaped layer (E=512, top-10, H=2048, I=512, g=128, int4
+    HIGH / int2 LOW) partitioned over G in {1, 2, 4, 8} ranks with C4's per-GPU budgets (n_hot = 25 % of E_loc, s = 1:
+    543.6 / 273.0 / 137.8 / 70.1 MB per layer per rank), every rank's pool in this process (a local EP group: the
+    library's EP layer with the deduplicated exchange done by device copies), B = 64 tokens per rank, router mode with
+    a drifting Zipf(1.2) bias, 10 timed steps after the warm-up and finalize.  All ranks share the one GPU, so this is
+    not a scaling curve: it measures the EP layer's correctness-path cost, the per-rank weight bytes and the
+    deduplication at each G (the multi-GPU curve is bench.py --gpus N under torchrun)."""
+    import torch
+    import synth
+    from paper_2511_15015_b200 import dx
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    E, k, H, I, g, hb, lb, s_sp, B = 512, 10, 2048, 512, 128, 4, 2, 1, 64
+    seed = a.seed + 3
+    arr, ptrs = host_masters(seed, L, E, H, I, 0, 1)
+    S_h, S_l = dx.dx_slot_bytes(H, I, g, hb), dx.dx_slot_bytes(H, I, g, lb)
+    wr = torch.stack([torch.from_numpy(router_weights(seed, l, E, H, a.router_scale).view(np.int16)).view(torch.bfloat16)
+                      for l in range(L)]).to(dev)
+    out = {"workload": f"C4 on one GPU: {L}-layer Qwen3-Next-80B-A3B-shaped stack (E=512, top-10, I=512, int4/int2), "
+                       f"G ranks' pools as a local EP group, B={B} per rank, per-rank budget n_hot = 25 % of E/G, s=1"}
+    for G in (1, 2, 4, 8):
+        e_loc = E // G
+        n_hot = e_loc // 4
+        M = n_hot * S_h + (e_loc - n_hot) * S_l + s_sp * (S_h + S_l)
+        pools = []
+        for r in range(G):
+            cfg = dx.dx_config()
+            cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden, cfg.inter, cfg.group_size = L, E, k, H, I, g
+            cfg.high_bits, cfg.low_bits = hb, lb
+            cfg.expert_budget_bytes = M * L
+            cfg.n_spare, cfg.ema_alpha = s_sp, 0.95
+            cfg.period, cfg.warmup_steps, cfg.dwell_min, cfg.publish_lag = 16, 32, 16, 4
+            cfg.max_tokens, cfg.ep_rank, cfg.ep_size = B, r, G
+            rp = [ptrs[l * E + r * e_loc + e] for l in range(L) for e in range(e_loc)]
+            pools.append(dx.Pool(cfg, rp, stream, nccl_id=b"local"))
+        bias = [torch.stack([torch.from_numpy(synth.zipf_logp(synth.rank_perm(seed, l, ep, E, 128, 0.25), 1.2))
+                             for ep in range(4)]).to(dev) for l in range(L)]
+        xs = [[torch.from_numpy(synth.normal_bf16(seed, 960 + r, i, 0, (B, H)).view(np.int16)).to(dev).view(torch.bfloat16)
+               for i in range(2)] for r in range(G)]
+        ys = [torch.empty(B, H, dtype=torch.bfloat16, device=dev) for _ in range(G)]
+        cnt = [0]
+
+        def st():
+            ep = min(cnt[0] // 16, 3)
+            for l in range(L):
+                dx.dx_moe_step_group(pools, l, [xs[r][cnt[0] & 1] for r in range(G)], [B] * G, ys,
+                                     router_w=[wr[l]] * G, router_bias=[bias[l][ep]] * G)
+            cnt[0] += 1
+
+        for _ in range(32):
+            st()
+        for l in range(L):
+            for p in pools:
+                p.dx_plan_precision(l)
+        for _ in range(3):
+            st()
+        for p in pools:
+            p.dx_sync()
+            p.dx_profile_read()
+            p.dx_profile_enable(True)
+        t0 = [p.dx_ep_traffic() for p in pools]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n = 10
+        for _ in range(n):
+            st()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        prof = [p.dx_profile_read() for p in pools]
+        t1 = [p.dx_ep_traffic() for p in pools]
+        rows = sum(b["rows_sent"] - a_["rows_sent"] for a_, b in zip(t0, t1))
+        ents = sum(b["entries_sent"] - a_["entries_sent"] for a_, b in zip(t0, t1))
+        wb = sum(pr["weight_bytes"][0] + pr["weight_bytes"][1] for pr in prof)
+        fw = sum(pr["forwards"] for pr in prof)
+        out[f"G{G}"] = {"per_rank_budget_mb": M / 1e6, "n_hot_per_rank": n_hot, "value": G * B * L * n / (ms / 1e3),
+                        "unit": UNIT, "ms_per_step": ms / n, "x_rows_sent": rows, "dispatch_entries": ents,
+                        "dedup_factor": ents / max(rows, 1), "weight_bytes_per_rank_layer": wb / max(fw, 1)}
+        for p in pools:
+            p.close()
+    torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
+    return out
+
+
 def prefetch_leg(a, ptrs, L_all, E, k, H, I, g, c, dev, stream, L=8):
     """f-1: an 8-layer C2-shaped stack (the first 8 layers' masters, C2's per-layer
     budget -> n_hot 24) in trace mode with cross-layer-coupled routing (synth.coupled_trace_logits: layer l boosts
@@ -1112,8 +1198,9 @@ def main():
     out = run_ours(a, rank, world, local_rank)
     if rank == 0 and world == 1 and not a.no_q80b:
         out["extra"]["q80b"] = q80b_leg(a, out["roofline"]["peak"])
+        out["extra"]["c4_ep_local"] = c4_ep_local_leg(a, out["roofline"]["peak"])
     if rank == 0:
-        if not a.no_cpu_baseline:
+        if not a.no_cpu_baseline and world == 1:          # the oracle baseline is an N = 1 figure
             v, cores, nsteps, _ = oracle_layer_sample(a, seconds=15.0)
             out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                    "sample": f"layer 0 of the C2 stack, batch {a.batch}, {nsteps} steps "
