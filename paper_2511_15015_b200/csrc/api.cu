@@ -3,7 +3,11 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 #include <cmath>
 #include <algorithm>
@@ -124,6 +128,24 @@ struct dx_pool_s {
     std::vector<cudaEvent_t> cache_ev;      // [slot] last copy out of the slot
     u64 cache_clock = 0, ssd_reads = 0, ssd_bytes = 0, cache_hits = 0;
     double ssd_read_ms = 0.0;
+    // SSD reads of runtime plans run on an I/O thread so the issuing host thread never blocks on the device: it
+    // hands over {layer, copies}; the worker reads, copies on the side stream and records the layer's ev_side;
+    // publication waits for the hand-over to finish before waiting on ev_side.  The cache is guarded by io_mu.
+    struct IoJob {
+        int layer;
+        std::vector<std::pair<size_t, uint8_t*>> copies;
+        bool wait_dem;
+        cudaEvent_t xc, x1;
+    };
+    int device = 0;
+    std::thread io_thread;
+    std::mutex io_mu;
+    std::condition_variable io_cv;
+    std::deque<IoJob> io_q;
+    std::vector<int> io_pending;            // per layer: a job handed over and not finished
+    int io_inflight = 0;
+    bool io_stop = false;
+    dx_status io_err = DX_OK;
     // f-1 cross-layer correlation prefetch (dx_set_prefetch): device counts per layer pair, the last routing of
     // each layer parity, candidates staged into free HIGH blocks ahead of the plan
     uint32_t* corr = nullptr;               // [L-1][E][E]
@@ -421,11 +443,58 @@ static dx_status copy_high_image(dx_pool p, size_t key, uint8_t* dst, cudaStream
     }
     const uint8_t* img;
     int sl;
+    std::lock_guard<std::mutex> lk(p->io_mu);
     dx_status rc = cached_image(p, key, &img, &sl);
     if (rc != DX_OK) return rc;
     DX_CUDA(cudaMemcpyAsync(dst, img, p->img_bytes, cudaMemcpyHostToDevice, st));
     DX_CUDA(cudaEventRecord(p->cache_ev[sl], st));
     return DX_OK;
+}
+
+static void io_worker(dx_pool p) {
+    cudaSetDevice(p->device);
+    for (;;) {
+        dx_pool_s::IoJob job;
+        {
+            std::unique_lock<std::mutex> lk(p->io_mu);
+            p->io_cv.wait(lk, [&] { return p->io_stop || !p->io_q.empty(); });
+            if (p->io_q.empty()) return;
+            job = std::move(p->io_q.front());
+            p->io_q.pop_front();
+        }
+        dx_status st = DX_OK;
+        for (auto& c : job.copies) {
+            std::lock_guard<std::mutex> lk(p->io_mu);
+            const uint8_t* img;
+            int sl;
+            st = cached_image(p, c.first, &img, &sl);
+            if (st != DX_OK) break;
+            if (cudaMemcpyAsync(c.second, img, p->img_bytes, cudaMemcpyHostToDevice, p->ss) != cudaSuccess ||
+                cudaEventRecord(p->cache_ev[sl], p->ss) != cudaSuccess) { st = DX_ERR_CUDA; break; }
+        }
+        if (job.xc) cudaEventRecord(job.xc, p->ss);
+        if (job.wait_dem) cudaStreamWaitEvent(p->ss, p->ev_dem, 0);
+        if (job.x1) cudaEventRecord(job.x1, p->ss);
+        cudaEventRecord(p->ev_side[job.layer], p->ss);
+        {
+            std::lock_guard<std::mutex> lk(p->io_mu);
+            if (st != DX_OK && p->io_err == DX_OK) p->io_err = st;
+            p->io_pending[job.layer] = 0;
+            --p->io_inflight;
+        }
+        p->io_cv.notify_all();
+    }
+}
+
+// the I/O worker finished the layer's hand-over (or, layer < 0, every hand-over); its first error, if any
+static dx_status io_wait(dx_pool p, int layer) {
+    if (p->ssd_fd < 0 || !p->io_thread.joinable()) return DX_OK;
+    std::unique_lock<std::mutex> lk(p->io_mu);
+    p->io_cv.wait(lk, [&] { return layer >= 0 ? p->io_pending[layer] == 0 : p->io_inflight == 0; });
+    const dx_status e = p->io_err;
+    p->io_err = DX_OK;
+    if (e != DX_OK) dx_set_error("SSD tier: a background read or copy failed");
+    return e;
 }
 
 static dx_status pool_create(const dx_config* cfg, const void* const* master, void* compute_stream,
@@ -789,6 +858,9 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         const int fd2 = open(ssd_path, O_RDONLY | O_DIRECT);
         if (fd2 >= 0 && p->img_bytes % 4096 == 0) { close(p->ssd_fd); p->ssd_fd = fd2; p->ssd_direct = true; }
         else if (fd2 >= 0) close(fd2);
+        cudaGetDevice(&p->device);
+        p->io_pending.assign(L, 0);
+        p->io_thread = std::thread(io_worker, p);
     }
 
     dx_info& inf = p->info;
@@ -852,6 +924,14 @@ extern "C" dx_status dx_get_unique_id(void* id128) {
 
 extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (!p) return DX_OK;
+    if (p->io_thread.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(p->io_mu);
+            p->io_stop = true;
+        }
+        p->io_cv.notify_all();
+        p->io_thread.join();
+    }
     if (p->cs) cudaStreamSynchronize(p->cs);
     if (p->ss) cudaStreamSynchronize(p->ss);
     if (p->comm) ep_nccl_destroy(p->comm);
@@ -941,6 +1021,10 @@ extern "C" dx_status dx_profile_enable(dx_pool p, int32_t enable) {
 }
 
 extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
+    {
+        dx_status st = io_wait(p, -1);                      // SSD tier: every hand-over recorded its events
+        if (st != DX_OK) return st;
+    }
     DX_CHECK(p && out, DX_ERR_INVALID_ARG, "null pool/out");
     DX_CUDA(cudaStreamSynchronize(p->cs));
     DX_CUDA(cudaStreamSynchronize(p->ss));
@@ -1580,6 +1664,8 @@ static dx_status fold_prepare(dx_pool p, int layer, FoldReq* req) {
     if (p->publish_at[layer] == t_new) {
         dx_status st = poll_transfers(p, layer);        // the plan's transfers must have been issued by now
         if (st != DX_OK) return st;
+        st = io_wait(p, layer);                          // (SSD tier: the I/O thread's hand-over too)
+        if (st != DX_OK) return st;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (p->profiling) {
             e0 = prof_event(p);
@@ -1688,6 +1774,39 @@ static dx_status issue_transfers(dx_pool p, int layer) {
     const size_t bytes = p->hi.bits == 16 ? (size_t)3 * p->I * p->H * 2 : (size_t)p->hi.bytes;
     uint8_t* hi_region = p->weights + (size_t)layer * p->layer_bytes + p->hi_base;
     u64 np = 0;
+    if (p->ssd_fd >= 0 && p->io_thread.joinable()) {
+        // f-4: hand the SSD reads and their copies to the I/O thread; it records ev_side when they are issued
+        dx_pool_s::IoJob job{layer, {}, nd > 0, nullptr, nullptr};
+        for (int i = 0; i < n; ++i) {
+            const int4 cmd = p->plan_host[layer * E + i];
+            if (cmd.y != 1) continue;
+            bool hit = false;
+            for (const int2& sg : p->staged[layer]) hit |= sg.x == cmd.x && sg.y == cmd.z;
+            if (hit) { ++p->pf_hits; continue; }
+            job.copies.emplace_back(layer * E + cmd.x, hi_region + (size_t)cmd.z * p->hi.bytes);
+        }
+        if (x0) {
+            job.x1 = prof_event(p);
+            p->prof_xfer_ev.push_back(job.x1);
+            if (!job.copies.empty()) {
+                job.xc = prof_event(p);
+                p->prof_copy_ev.push_back(x0);
+                p->prof_copy_ev.push_back(job.xc);
+                p->prof_copy_bytes.push_back(job.copies.size() * bytes);
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lk(p->io_mu);
+            p->io_pending[layer] = 1;
+            ++p->io_inflight;
+            p->io_q.push_back(std::move(job));
+        }
+        p->io_cv.notify_all();
+        p->staged[layer].clear();
+        p->xfer_pending[layer] = 0;
+        p->n_pending -= 1;
+        return DX_OK;
+    }
     for (int i = 0; i < n; ++i) {
         const int4 cmd = p->plan_host[layer * E + i];
         if (cmd.y != 1) continue;
@@ -1830,7 +1949,11 @@ static dx_status manual(dx_pool p, int layer, const int32_t* experts, int n, int
     for (int i = 0; i < n; ++i) cmds[i] = make_int2(experts[i], dir);
     // k_manual rewrites the layer's command list (plan_cmd / plan_n): transitions issued earlier for this
     // layer must have finished reading it on the side stream first
-    if (p->publish_at[layer] >= 0) DX_CUDA(cudaStreamWaitEvent(p->cs, p->ev_side[layer], 0));
+    if (p->publish_at[layer] >= 0) {
+        dx_status st = io_wait(p, layer);
+        if (st != DX_OK) return st;
+        DX_CUDA(cudaStreamWaitEvent(p->cs, p->ev_side[layer], 0));
+    }
     DX_CUDA(cudaMemcpyAsync(p->manual_cmds, cmds.data(), n * sizeof(int2), cudaMemcpyHostToDevice, p->cs));
     launch_manual(p->ctrl, layer, p->manual_cmds, n, p->manual_status, p->cs);
     DX_CUDA(cudaEventRecord(p->ev_plan, p->cs));
@@ -1888,6 +2011,10 @@ extern "C" dx_status dx_sync(dx_pool p) {
         }
         if (!p->xfer_pending[l]) continue;
         dx_status st = poll_transfers(p, l);
+        if (st != DX_OK) return st;
+    }
+    {
+        dx_status st = io_wait(p, -1);
         if (st != DX_OK) return st;
     }
     DX_CUDA(cudaStreamSynchronize(p->ss2));
