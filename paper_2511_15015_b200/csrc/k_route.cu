@@ -5,6 +5,7 @@
 // Readings: R-G1 (ties -> lower id, gates = softmax over the k selected logits), R-G2 (dx_expf),
 // R-H1 (cnt u32, mass = sum rint(g * 2^24) u64: integer sums are order-free => bit-exact).
 #include "dx_common.cuh"
+#include "dx_sm100.cuh"
 #include <cstdio>
 
 #define ROUTE_TOK_PER_BLK 8
@@ -282,43 +283,72 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
 }
 
 // ------------------------------------------------------------------ a1-a4 in ONE launch (decode batches)
-// T*k <= RDEC_MAX_ENT entries.  Grid of up to 128 CTAs x 512 threads, three phases separated by grid-wide
-// barriers (every CTA is resident: the grid is smaller than the SM count and the next kernel is released
-// with griddepcontrol.launch_dependents only after the last barrier):
-//   A (router mode) logits = x W_r^T + b, tiles of 16 tokens x 8 experts spread over the CTAs (mma.sync,
-//     exact bf16 products, fp32 sums in a fixed order: deterministic);
-//   B top-k + gates, one warp per token (R-G1, R-G2), written to idx/gate and to the per-entry exchange;
-//   C every CTA recomputes the per-chunk expert histograms of all entries (match_any, integer sums), the
-//     offsets scan and the chunk bases in shared memory (identical in every CTA), CTA 0 publishes off /
-//     active list / hotness counters, and each CTA places and gathers its share of the entries
-//     (perm / inv, Xp[pos] = x[t]) -- the stable order (t asc, j asc) of a4.
+// T*k <= RDEC_MAX_ENT entries.  The grid is ceil(T/16) clusters of CS CTAs x 512 threads (CS = 8 for H = 2048;
+// every CTA is resident: the grid is far below the SM count and the next kernel is released with
+// griddepcontrol.launch_dependents only after the grid barrier):
+//   A (router mode) cluster c owns tokens [16c, 16c+16); CTA rank r computes partial logits over the K slice
+//     [r H/CS, (r+1) H/CS) for all E experts (mma.sync m16n8k16: exact bf16 products, fp32 accumulation in K
+//     order) into its shared memory;
+//   B after a cluster barrier, CTA r takes tokens r, r + CS, ... of the tile (one warp per token): logit = the
+//     CS partials read over distributed shared memory and summed in rank order (+ b), written to the logits
+//     buffer; top-k + gates (R-G1, R-G2) to idx/gate and the per-entry exchange; the hotness counters take
+//     integer atomics per entry (u32 cnt, u64 mass: order-free, R-H1);
+//   one grid barrier (all entries routed), then
+//   C every CTA recomputes the per-chunk expert histograms of all entries (match_any), the offsets scan and the
+//     chunk bases in shared memory (identical in every CTA), CTA 0 publishes off / active list, and each CTA
+//     places and gathers its share of the entries (perm / inv, Xp[pos] = x[t]) -- the stable order
+//     (t asc, j asc) of a4.
+// The router logits are deterministic (fixed slice partition and summation order per H).
 #define RDEC_MAX_ENT 512
 #define RDEC_CHUNKS (RDEC_MAX_ENT / 32)
 template <typename Tv>
 __device__ Tv block_excl_scan(Tv v, Tv* tmp, Tv* total);
 
-// Grid-wide barrier over a {arrivals, generation} pair that resets itself (reusable across phases and
-// launches).  Release: __threadfence before arriving; acquire: fence after observing the new generation.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acqrel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+// Grid-wide barrier over a {arrivals, generation} pair that resets itself (reusable across launches): read the
+// generation, arrive (acq_rel), the last arrival resets the count and releases the next generation; the others
+// poll the generation with acquire loads (no sleep: the wait is one L2 round trip after the last arrival).
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+        const unsigned g = ld_acquire_gpu(bar + 1);
+        if (atom_add_acqrel_gpu(bar, 1u) == gridDim.x - 1) {
             atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
+            st_release_gpu(bar + 1, g + 1u);
         } else {
-            long long t0 = clock64();
-            while (*gen == g) {
-                __nanosleep(20);
+            const long long t0 = clock64();
+            while (ld_acquire_gpu(bar + 1) == g)
                 if (clock64() - t0 > 4000000000ll) __trap();   // ~2 s: a protocol bug, fail the launch
-            }
         }
-        __threadfence();
     }
     __syncthreads();
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t local_addr, uint32_t rank) {
+    uint32_t ra;
+    float v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra));
+    return v;
 }
 
 struct RouteDecArgs {
@@ -326,7 +356,7 @@ struct RouteDecArgs {
     const __nv_bfloat16* wr;      // router mode (else logits_in)
     const float* bias;
     const float* logits_in;
-    int T, E, k, H, e_lo, e_cnt;
+    int T, E, k, H, e_lo, e_cnt, cs, ech;
     RouteWs ws;
     uint32_t* cnt_acc;
     u64* mass_acc;
@@ -334,114 +364,171 @@ struct RouteDecArgs {
     __nv_bfloat16* Xp;
 };
 
+#ifdef DX_RDEC_PROF
+__device__ unsigned g_rdec_n = 0;
+#define RDEC_T(i) if (threadIdx.x == 0) tstamp[i] = globaltimer_ns_r();
+__device__ __forceinline__ unsigned long long globaltimer_ns_r() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#else
+#define RDEC_T(i)
+#endif
 template <int NVT>
 __global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
+#ifdef DX_RDEC_PROF
+    __shared__ unsigned long long tstamp[12];
+#endif
+    RDEC_T(0)
     extern __shared__ __align__(16) uint8_t dyn_s[];
-    __shared__ float red[16][16][9];                         // phase A: [warp][token][expert] partials
     __shared__ int16_t ent_s[RDEC_MAX_ENT];
     __shared__ int16_t rk_s[RDEC_MAX_ENT];
-    __shared__ uint32_t gm_s[RDEC_MAX_ENT];
     __shared__ int32_t tmp[32];
     __shared__ int32_t total_s, na_s, nhi_s;
-    uint32_t* cmass = reinterpret_cast<uint32_t*>(dyn_s);                       // [chunk][E]
-    int16_t* chist = reinterpret_cast<int16_t*>(cmass + RDEC_CHUNKS * a.E);      // [chunk][E] counts -> bases
+    __shared__ __align__(8) uint64_t abar;
+    __shared__ float bias_s[ROUTE_MAX_E];
+    float* part = reinterpret_cast<float*>(dyn_s);                              // A/B: [16][E] partial logits
+    int16_t* chist = reinterpret_cast<int16_t*>(dyn_s);                         // C: [chunk][E] counts -> bases
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int T = a.T, E = a.E, k = a.k, H = a.H;
-    for (int i = threadIdx.x; i < RDEC_CHUNKS * E; i += blockDim.x) { chist[i] = 0; cmass[i] = 0; }
-    DX_GRID_WAIT();
-    const float* lgs = a.logits_in;
+    const int T = a.T, E = a.E, k = a.k, H = a.H, CS = a.cs;
+    const uint32_t rank = CS > 1 ? cluster_rank() : 0u;
+    const int t0 = (blockIdx.x / CS) * 16;                                      // this cluster's token tile
+    // Router mode: the W_r slice of the first expert round (and the bias) are constant inputs, so their bulk copies
+    // are issued before griddepcontrol.wait and overlap the previous kernel's tail; the x rows follow the wait.
+    const int Hs = H / CS, pitch = Hs + 8;
+    __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(dyn_s + (size_t)16 * E * 4);   // [16][pitch]
+    __nv_bfloat16* wsm = xs + 16 * pitch;                                               // [ECH][pitch]
+    const int ECH = a.ech;
     if (a.wr) {
-        // ---------------- A: router logits (the router stays full precision)
-        const int g = lane >> 2, q = lane & 3;
-        const int nunit = ((T + 15) / 16) * (E / 8);
-        const int nsteps = H / 16;
-        for (int u = blockIdx.x; u < nunit; u += gridDim.x) {
-            const int e0 = (u % (E / 8)) * 8, t0 = (u / (E / 8)) * 16;
-            const int ta = t0 + g, tb = t0 + g + 8, e = e0 + g;
-            const uint32_t* xa = reinterpret_cast<const uint32_t*>(a.x + (size_t)min(ta, T - 1) * H) + q;
-            const uint32_t* xb = reinterpret_cast<const uint32_t*>(a.x + (size_t)min(tb, T - 1) * H) + q;
-            const uint32_t* we = reinterpret_cast<const uint32_t*>(a.wr + (size_t)e * H) + q;
-            float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-            constexpr int U = 8;
-            for (int s0 = warp; s0 < nsteps; s0 += 16 * U) {
-                uint32_t f[U][6];
-#pragma unroll
-                for (int uu = 0; uu < U; ++uu) {
-                    const int s = s0 + 16 * uu;
-                    if (s < nsteps) {
-                        const int kk = s * 8;
-                        f[uu][0] = __ldg(xa + kk); f[uu][1] = __ldg(xb + kk);
-                        f[uu][2] = __ldg(xa + kk + 4); f[uu][3] = __ldg(xb + kk + 4);
-                        f[uu][4] = __ldg(we + kk); f[uu][5] = __ldg(we + kk + 4);
-                    }
-                }
-#pragma unroll
-                for (int uu = 0; uu < U; ++uu)
-                    if (s0 + 16 * uu < nsteps) mma16816(c, f[uu][0], f[uu][1], f[uu][2], f[uu][3], f[uu][4], f[uu][5]);
-            }
-            red[warp][g][2 * q] = c[0];
-            red[warp][g][2 * q + 1] = c[1];
-            red[warp][g + 8][2 * q] = c[2];
-            red[warp][g + 8][2 * q + 1] = c[3];
-            __syncthreads();
-            if (threadIdx.x < 128) {
-                const int tl = threadIdx.x >> 3, el = threadIdx.x & 7;
-                const int t = t0 + tl, ee = e0 + el;
-                if (t < T) {
-                    float v = red[0][tl][el];
-#pragma unroll
-                    for (int w = 1; w < 16; ++w) v += red[w][tl][el];
-                    a.ws.logits[(size_t)t * E + ee] = a.bias ? v + a.bias[ee] : v;
-                }
-            }
-            __syncthreads();
+        if (threadIdx.x == 0) {
+            sm100::mbar_init(&abar, 1);
+            sm100::fence_mbar_init();
+            sm100::mbar_arrive_expect_tx(&abar, (uint32_t)((16 + min(ECH, E)) * Hs * 2));
         }
-        grid_sync(a.ws.gbar);
-        lgs = a.ws.logits;
+        __syncthreads();
+        for (int r = threadIdx.x; r < min(ECH, E); r += blockDim.x)
+            sm100::bulk_load(wsm + r * pitch, a.wr + (size_t)r * H + (size_t)rank * Hs, (uint32_t)(Hs * 2), &abar);
+        if (a.bias && threadIdx.x < E) bias_s[threadIdx.x] = __ldg(a.bias + threadIdx.x);
     }
-    // ---------------- B: top-k + gates, one warp per token (R-G1, R-G2)
-    for (int t = warp * gridDim.x + blockIdx.x; t < T; t += gridDim.x * 16) {    // spread over the SMs first
-        float v[NVT];
-        uint32_t taken = 0;
-        const float* lrow = lgs + (size_t)t * E;
-#pragma unroll
-        for (int i = 0; i < NVT; ++i) {
-            const int e = lane + 32 * i;
-            v[i] = e < E ? __ldcg(lrow + e) : -INFINITY;
-            if (e >= E) taken |= 1u << i;
+    DX_GRID_WAIT();
+    RDEC_T(1)
+    if (a.wr) {
+        // ---------------- A: partial router logits over this CTA's K slice (router in full precision).
+        // The slice of the tile's 16 x rows and of W_r (ECH experts per round) is staged in shared memory by bulk
+        // copies (one per row, rows padded by 16 B so the ldmatrix row groups hit distinct banks), then warp w
+        // takes expert tiles w, w + 16, ... (mma.sync m16n8k16, fp32 accumulation in K order).
+        uint32_t aph = 0;
+        for (int e0 = 0; e0 < E; e0 += ECH) {
+            const int ne = min(ECH, E - e0);
+            if (e0 > 0) {                                     // later rounds: W_r and x after the previous compute
+                if (threadIdx.x == 0) sm100::mbar_arrive_expect_tx(&abar, (uint32_t)((16 + ne) * Hs * 2));
+                __syncthreads();
+            }
+            for (int r = e0 > 0 ? threadIdx.x : threadIdx.x + ne; r < 16 + ne; r += blockDim.x) {
+                // round 0: only the 16 x rows (r = ne .. ne + 15); later rounds: x rows r < 16, then W rows
+                const int rr = e0 > 0 ? r : r - ne;
+                const __nv_bfloat16* src = rr < 16 ? a.x + (size_t)min(t0 + rr, T - 1) * H + (size_t)rank * Hs
+                                                   : a.wr + (size_t)(e0 + rr - 16) * H + (size_t)rank * Hs;
+                __nv_bfloat16* dst = rr < 16 ? xs + rr * pitch : wsm + (rr - 16) * pitch;
+                sm100::bulk_load(dst, src, (uint32_t)(Hs * 2), &abar);
+            }
+            sm100::mbar_wait(&abar, aph);
+            aph ^= 1u;
+            const int g = lane >> 2, q = lane & 3;
+            for (int et = warp; et < ne / 8; et += 16) {
+                float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                const uint32_t xa = (uint32_t)__cvta_generic_to_shared(xs + (lane & 15) * pitch + 8 * (lane >> 4));
+                const uint32_t wa = (uint32_t)__cvta_generic_to_shared(wsm + (et * 8 + (lane & 7)) * pitch + 8 * ((lane >> 3) & 1));
+                for (int ks = 0; ks < Hs; ks += 16) {
+                    uint32_t a0, a1, a2, a3, b0, b1;
+                    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(xa + 2 * ks));
+                    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(b0), "=r"(b1) : "r"(wa + 2 * ks));
+                    mma16816(c, a0, a1, a2, a3, b0, b1);
+                }
+                const int ee = e0 + et * 8 + 2 * q;
+                part[g * E + ee] = c[0];
+                part[g * E + ee + 1] = c[1];
+                part[(g + 8) * E + ee] = c[2];
+                part[(g + 8) * E + ee + 1] = c[3];
+            }
+            __syncthreads();                                  // staging buffers free for the next round
         }
-        float sel_v[ROUTE_MAX_K];
-        int sel_e[ROUTE_MAX_K];
-        topk_warp<NVT>(v, taken, k, lane, sel_v, sel_e);
-        float my_v = sel_v[0];
-        int my_e = 0;
+        if (CS > 1) cluster_barrier();
+    }
+    RDEC_T(2)
+    // ---------------- B: logits (rank-ordered sum of the cluster's partials) + top-k + gates, one warp per token
+    if (warp < 16 / CS) {
+        const int tl = (int)rank + CS * warp;
+        const int t = t0 + tl;
+        if (t < T) {
+            float v[NVT];
+            uint32_t taken = 0;
+            const uint32_t prow = (uint32_t)__cvta_generic_to_shared(part + tl * E);
 #pragma unroll
-        for (int j = 0; j < ROUTE_MAX_K; ++j)
-            if (j == lane) { my_v = sel_v[j]; my_e = sel_e[j]; }
-        const float my_ev = lane < k ? dx_expf(__fsub_rn(my_v, sel_v[0])) : 0.0f;
-        float part[ROUTE_MAX_K];
+            for (int i = 0; i < NVT; ++i) {
+                const int e = lane + 32 * i;
+                if (e >= E) {
+                    v[i] = -INFINITY;
+                    taken |= 1u << i;
+                } else if (a.wr) {
+                    float pv[8];
 #pragma unroll
-        for (int j = 0; j < ROUTE_MAX_K; ++j) part[j] = __shfl_sync(0xffffffffu, my_ev, j);
-        float sum = part[0];
+                    for (int r = 0; r < 8; ++r)                 // every remote load in flight, then the ordered sum
+                        if (r < CS) pv[r] = CS > 1 ? ld_cluster_f32(prow + 4 * e, r) : part[tl * E + e];
+                    float sum = 0.0f;
 #pragma unroll
-        for (int j = 1; j < ROUTE_MAX_K; ++j)
-            if (j < k) sum = __fadd_rn(sum, part[j]);
-        if (lane < k) {
-            const float gte = __fdiv_rn(my_ev, sum);
-            a.ws.idx[(size_t)t * k + lane] = my_e;
-            a.ws.gate[(size_t)t * k + lane] = gte;
-            a.ws.ent[t * k + lane] = (int16_t)my_e;
-            a.ws.gm[t * k + lane] = (uint32_t)rintf(__fmul_rn(gte, 16777216.0f));
+                    for (int r = 0; r < 8; ++r)
+                        if (r < CS) sum += pv[r];
+                    v[i] = a.bias ? sum + bias_s[e] : sum;
+                    a.ws.logits[(size_t)t * E + e] = v[i];
+                } else {
+                    v[i] = __ldg(a.logits_in + (size_t)t * E + e);
+                }
+            }
+            RDEC_T(8)
+            float sel_v[ROUTE_MAX_K];
+            int sel_e[ROUTE_MAX_K];
+            topk_warp<NVT>(v, taken, k, lane, sel_v, sel_e);
+            RDEC_T(9)
+            float my_v = sel_v[0];
+            int my_e = 0;
+#pragma unroll
+            for (int j = 0; j < ROUTE_MAX_K; ++j)
+                if (j == lane) { my_v = sel_v[j]; my_e = sel_e[j]; }
+            const float my_ev = lane < k ? dx_expf(__fsub_rn(my_v, sel_v[0])) : 0.0f;
+            float part_e[ROUTE_MAX_K];
+#pragma unroll
+            for (int j = 0; j < ROUTE_MAX_K; ++j) part_e[j] = __shfl_sync(0xffffffffu, my_ev, j);
+            float sum = part_e[0];
+#pragma unroll
+            for (int j = 1; j < ROUTE_MAX_K; ++j)
+                if (j < k) sum = __fadd_rn(sum, part_e[j]);
+            if (lane < k) {
+                const float gte = __fdiv_rn(my_ev, sum);
+                const uint32_t gm = (uint32_t)rintf(__fmul_rn(gte, 16777216.0f));
+                a.ws.idx[(size_t)t * k + lane] = my_e;
+                a.ws.gate[(size_t)t * k + lane] = gte;
+                a.ws.ent[t * k + lane] = (int16_t)my_e;
+                const int le = my_e - a.e_lo;                   // a3: integer atomics, order-free (R-H1)
+                if (a.cnt_acc && le >= 0 && le < a.e_cnt) {
+                    atomicAdd(&a.cnt_acc[le], 1u);
+                    atomicAdd(&a.mass_acc[le], (u64)gm);
+                }
+            }
         }
     }
+    RDEC_T(10)
+    if (a.wr && CS > 1) cluster_barrier();               // the cluster's partials are no longer read
+    RDEC_T(3)
+    for (int i = threadIdx.x; i < RDEC_CHUNKS * E; i += blockDim.x) chist[i] = 0;
     grid_sync(a.ws.gbar);
-    DX_GRID_LAUNCH();                       // every CTA is resident and past its last barrier
-    // ---------------- C: histograms, offsets, active list, counters (every CTA, identical results)
+    RDEC_T(4)
+    DX_GRID_LAUNCH();                       // every CTA is resident and past the barrier
+    // ---------------- C: histograms, offsets, active list (every CTA, identical results)
     const int n = T * k;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        ent_s[i] = __ldcg(a.ws.ent + i);
-        gm_s[i] = __ldcg(a.ws.gm + i);
-    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ent_s[i] = __ldcg(a.ws.ent + i);
     __syncthreads();
     {
         const int ci = warp, i = warp * 32 + lane;            // n <= 512 = 16 warps x 32 entries
@@ -449,30 +536,15 @@ __global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
         const int ei = have ? ent_s[i] : -1 - lane;
         const unsigned same = __match_any_sync(0xffffffffu, ei);
         const int rk = __popc(same & ((1u << lane) - 1u));
-        const uint32_t gsum = __reduce_add_sync(same, have ? gm_s[i] : 0u);
         if (have) rk_s[i] = (int16_t)rk;
-        if (have && rk == 0) {
-            chist[ci * E + ei] = (int16_t)__popc(same);
-            cmass[ci * E + ei] = gsum;
-        }
+        if (have && rk == 0) chist[ci * E + ei] = (int16_t)__popc(same);
     }
     __syncthreads();
     const int e = threadIdx.x;                                // E <= 512 = blockDim
     uint32_t c = 0;
-    u64 m = 0;
     if (e < E) {
 #pragma unroll
-        for (int c2 = 0; c2 < RDEC_CHUNKS; ++c2) {
-            c += (uint32_t)chist[c2 * E + e];
-            m += cmass[c2 * E + e];
-        }
-        if (c && blockIdx.x == 0) {
-            const int le = e - a.e_lo;
-            if (le >= 0 && le < a.e_cnt && a.cnt_acc) {
-                atomicAdd(&a.cnt_acc[le], c);
-                atomicAdd(&a.mass_acc[le], m);
-            }
-        }
+        for (int c2 = 0; c2 < RDEC_CHUNKS; ++c2) c += (uint32_t)chist[c2 * E + e];
     }
     const int32_t o = block_excl_scan<int32_t>((int32_t)c, tmp, &total_s);
     const int32_t ac = block_excl_scan<int32_t>(c > 0 ? 1 : 0, tmp, &na_s);
@@ -503,6 +575,7 @@ __global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
         }
     }
     __syncthreads();
+    RDEC_T(5)
     // a4: stable placement (pos = off[e] + earlier chunks + in-chunk rank) and the x-row gather, one warp
     // per entry, entries spread over all CTAs
     for (int i = warp * gridDim.x + blockIdx.x; i < n; i += gridDim.x * 16) {
@@ -518,6 +591,16 @@ __global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
             for (int h = lane; h < H / 8; h += 32) dst[h] = __ldg(src + h);
         }
     }
+    RDEC_T(7)
+#ifdef DX_RDEC_PROF
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x == 0 && (atomicAdd(&g_rdec_n, 1) % 64) == 63)
+        printf("rdec us: wait %.2f A %.2f B %.2f [logits %.2f topk %.2f rest %.2f cbar %.2f] sync %.2f C %.2f place %.2f total %.2f\n", (tstamp[1] - tstamp[0]) * 1e-3,
+               (tstamp[2] - tstamp[1]) * 1e-3, (tstamp[3] - tstamp[2]) * 1e-3, (tstamp[8] - tstamp[2]) * 1e-3,
+               (tstamp[9] - tstamp[8]) * 1e-3, (tstamp[10] - tstamp[9]) * 1e-3, (tstamp[3] - tstamp[10]) * 1e-3,
+               (tstamp[4] - tstamp[3]) * 1e-3,
+               (tstamp[5] - tstamp[4]) * 1e-3, (tstamp[7] - tstamp[5]) * 1e-3, (tstamp[7] - tstamp[0]) * 1e-3);
+#endif
 }
 
 // ------------------------------------------------------------------ a4: offsets + stable scatter
@@ -928,9 +1011,27 @@ template <int NVT>
 static void launch_rdec(const RouteDecArgs& a, int grid, size_t smem, cudaStream_t st) {
     static unsigned long long attr_mask = 0;
     if (dx_first_on_device(attr_mask))
-        cudaFuncSetAttribute(k_route_dec<NVT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             RDEC_CHUNKS * ROUTE_MAX_E * 6);
-    dx_launch(k_route_dec<NVT>, dim3(grid), dim3(512), smem, st, g_dx_pdl, a);
+        cudaFuncSetAttribute(k_route_dec<NVT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = a.cs;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+    if (g_dx_pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, k_route_dec<NVT>, a);
 }
 
 void launch_route_dec(const __nv_bfloat16* x, const __nv_bfloat16* wr, const float* bias, const float* logits_in,
@@ -943,14 +1044,18 @@ void launch_route_dec(const __nv_bfloat16* x, const __nv_bfloat16* wr, const flo
     a.ws = ws; a.cnt_acc = cnt_acc; a.mass_acc = mass_acc;
     a.rs = RouteStats{tier, bytes[0][0], bytes[0][1], bytes[1][0], bytes[1][1], ws.stats};
     a.Xp = Xp;
-    // enough CTAs for the router tiles (16 tokens x 8 experts each) and for one warp per token / entry
-    const int units = wr ? ((T + 15) / 16) * (E / 8) : 0;
-    int grid = units;
-    const int need_warps = (T * k + 15) / 16;
-    if (grid < need_warps) grid = need_warps;
-    if (grid < 1) grid = 1;
-    if (grid > 128) grid = 128;
-    const size_t smem = (size_t)RDEC_CHUNKS * E * 6;
+    // clusters of cs CTAs per 16-token tile (router mode: they split K, each slice a multiple of 16)
+    int cs = 8;
+    if (wr)
+        while (cs > 1 && H % (16 * cs) != 0) cs >>= 1;
+    a.cs = cs;
+    const int pitch = H / cs + 8;                       // staged row (bf16) of the router slices
+    int ech = E;                                        // experts staged per round (W_r slice rows)
+    while (ech > 128 && (size_t)(16 + ech) * pitch * 2 > 96 * 1024) ech >>= 1;
+    a.ech = ech;
+    const int grid = ((T + 15) / 16) * cs;
+    size_t smem = (size_t)E * 16 * 4 > (size_t)RDEC_CHUNKS * E * 2 ? (size_t)E * 16 * 4 : (size_t)RDEC_CHUNKS * E * 2;
+    if (wr) smem = (size_t)E * 16 * 4 + (size_t)(16 + ech) * pitch * 2;
     if (E <= 128)      launch_rdec<4>(a, grid, smem, st);
     else if (E <= 256) launch_rdec<8>(a, grid, smem, st);
     else               launch_rdec<16>(a, grid, smem, st);

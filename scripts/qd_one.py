@@ -30,11 +30,17 @@ for layer in range(L):
 lg = torch.from_numpy(synth.trace_logits(1, 0, 5, B, E, zipf)).cuda()
 xd = bf16_dev(synth.normal_bf16(1, 0, 5, 0, (B, H)))
 yd = torch.zeros(B, H, dtype=torch.bfloat16, device="cuda")
+kw = dict(logits=lg)
+if os.environ.get("QD_ROUTER"):                 # router mode (the bench's): logits = x W_r^T + b on the device
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    wr = (torch.randn(E, H, device="cuda", generator=gen) / H ** 0.5).to(torch.bfloat16)
+    rb = torch.log(torch.arange(1, E + 1, device="cuda", dtype=torch.float32) ** -max(zipf, 1e-3))
+    kw = dict(router_w=wr, router_bias=rb)
 for i in range(10):
-    pool.dx_moe_forward(i % L, xd, B, yd, logits=lg)
+    pool.dx_moe_forward(i % L, xd, B, yd, **kw)
 pool.dx_profile_enable(1)
 for i in range(reps):
-    pool.dx_moe_forward(i % L, xd, B, yd, logits=lg)
+    pool.dx_moe_forward(i % L, xd, B, yd, **kw)
 pr = pool.dx_profile_read()
 n = pr["forwards"]
 gu, dn = pr["ffn_ms"][0] / n, pr["ffn_ms"][1] / n
