@@ -65,7 +65,7 @@ struct dx_pool_s {
     __nv_bfloat16* Y = nullptr;
     int32_t* err_flag = nullptr;
     int32_t* dev_err = nullptr;             // sticky device-side error (EP routed rows), reported by dx_sync
-    int32_t* gemm_sched = nullptr;      // [phase][ticket counter, CTAs done] of the grouped GEMMs (self-resetting)
+    int32_t* gemm_sched = nullptr;      // [kernel: k_gemm, k_wide][phase][ticket counter, CTAs done] (self-resetting)
     int2* manual_cmds = nullptr;
     int32_t* manual_status = nullptr;
     const uint8_t** hi_img_dev = nullptr;   // [L * E_loc]
@@ -99,6 +99,7 @@ struct dx_pool_s {
     __nv_bfloat16* Xp = nullptr;            // x rows in permuted order (B operand of gate/up)
     std::vector<GemmMaps> gmaps;            // per layer (weights); xb filled per launch
     CUtensorMap xb0[4], xb1[4];             // B operand maps (Xp / act) for tiles of 16, 32, 64, 128 rows
+    CUtensorMap xw0, xw1;                   // the same, 256-row tiles (k_wide)
     CUtensorMap xk0[3], xk1[3];             // 3-D B maps (Xp / act): several K chunks per box (decode int)
     std::vector<DecMaps> dec_maps;          // host: per-layer maps of the decode kernels (k_dec.cu)
     DecBMaps dec_bmaps;
@@ -251,8 +252,11 @@ static dx_status build_maps(dx_pool p) {
         const uint64_t d0[2] = {(uint64_t)H, rows}, s0[1] = {(uint64_t)H * 2};
         const uint64_t d1[2] = {(uint64_t)I, rows}, s1[1] = {(uint64_t)I * 2};
         const uint32_t b[2] = {64, bn};
+        const uint32_t bw[2] = {64, 256};
         if (!make_map(&p->xb0[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->Xp, d0, s0, b, CU_TENSOR_MAP_SWIZZLE_128B) ||
-            !make_map(&p->xb1[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, b, CU_TENSOR_MAP_SWIZZLE_128B)) {
+            !make_map(&p->xb1[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, b, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            (i == 0 && (!make_map(&p->xw0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->Xp, d0, s0, bw, CU_TENSOR_MAP_SWIZZLE_128B) ||
+                        !make_map(&p->xw1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, bw, CU_TENSOR_MAP_SWIZZLE_128B)))) {
             dx_set_error("tensor map encoding failed (activations)");
             return DX_ERR_CUDA;
         }
@@ -650,7 +654,7 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     p->Xp = carve<__nv_bfloat16>(q, n_ent * p->H);
     p->err_flag = carve<int32_t>(q, 1);
     p->dev_err = carve<int32_t>(q, 1);
-    p->gemm_sched = carve<int32_t>(q, 4);
+    p->gemm_sched = carve<int32_t>(q, 8);
     p->manual_cmds = carve<int2>(q, 1024);
     p->manual_status = carve<int32_t>(q, 1024);
     p->corr = carve<uint32_t>(q, (size_t)(L > 1 ? L - 1 : 0) * E * E);
@@ -796,7 +800,7 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         DX_CUDA(cudaMemcpyAsync(c.plan_n, pn.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
         DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(p->dev_err, 0, 4, p->cs));
-        DX_CUDA(cudaMemsetAsync(p->gemm_sched, 0, 16, p->cs));
+        DX_CUDA(cudaMemsetAsync(p->gemm_sched, 0, 32, p->cs));
         DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
         DX_CUDA(cudaMemsetAsync(w.done, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(w.gbar, 0, 8, p->cs));
@@ -1304,13 +1308,20 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         ga.E_loc = E; ga.shared_slot = p->shared_slot;
         static const int dbg = [] { const char* s = getenv("DX_GEMM_DBG"); return s ? atoi(s) : 0; }();
         ga.dbg = dbg;
+        // prefill with a bf16 HIGH tier: those experts' items run as 128 x 256 tiles in k_wide, the rest in k_gemm
+        const bool wide = !dec && p->hi.bits == 16 && wide_enabled();
+        ga.skip_bf16 = wide ? 1 : 0;
         GemmMaps gm = p->gmaps[layer];
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb0[i];
         for (int i = 0; i < 3; ++i) gm.xk[i] = p->xk0[i];
+        gm.xw = p->xw0;
+        if (wide) launch_wide(0, gm, ga, max_act * (p->I / 64), p->cs);
         launch_gemm(0, dec, gm, ga, max_act * (p->I / 64), p->cs);
         if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb1[i];
         for (int i = 0; i < 3; ++i) gm.xk[i] = p->xk1[i];
+        gm.xw = p->xw1;
+        if (wide) launch_wide(1, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
         launch_gemm(1, dec, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
         }
     }

@@ -307,6 +307,7 @@ struct GemmMaps {
     CUtensorMap wlo_gu, wlo_dn;
     // B operands (token rows [rows][K] bf16, 128 B swizzle)
     CUtensorMap xb[4];              // 2-D boxes {64, 16/32/64/128}
+    CUtensorMap xw;                 // 2-D box {64, 256}: the wide prefill tiles of k_wide
     CUtensorMap xk[3];              // 3-D {64, rows, K/64}: boxes {64,16,4}, {64,32,4}, {64,16,8} (decode int stages)
 };
 struct GemmArgs {
@@ -326,6 +327,7 @@ struct GemmArgs {
     __nv_bfloat16* Y;
     int* sched;                     // [phase][ticket counter, CTAs done]: dynamic work-item hand-out, zero
                                     // between launches (the last CTA of a launch resets it)
+    int skip_bf16;                  // prefill k_gemm: the leading bf16 (HIGH, 16-bit) experts are k_wide's
     int dbg;                        // performance experiments only (DX_GEMM_DBG): 4 skip the A-in-TMEM MMAs,
                                     // 5 skip the dequant transform, 6 both, 13 = 6 with plain
                                     // arrivals instead of tcgen05.commit on int stages
@@ -374,6 +376,9 @@ void launch_dec(int phase, const DecMaps& lm, const DecBMaps& bm, const DecArgs&
 void gemm_trap_init();                            // host-mapped watchdog record (once per process)
 int gemm_trap_report(char* buf, size_t n);        // appends the record, if a k_gemm wait timed out
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
+// prefill: the bf16 (HIGH) experts' items as 128 x 256 tiles (k_wide); k_gemm then takes only the others (skip_bf16)
+void launch_wide(int phase, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
+bool wide_enabled();
 
 // k_ctrl.cu
 void launch_fold(const Ctrl& c, int layer, u64 B_tot, cudaStream_t st);

@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         int v = 0;
         if (t < n_act) {
             const int e = a.act_e[t];
-            v = (a.off[e + 1] - a.off[e] + C::NBMAX - 1) / C::NBMAX;
+            const bool bf = a.skip_bf16 && (e >= a.E_loc || a.tier[e]);    // k_wide's (bf16 HIGH) expert
+            v = bf ? 0 : (a.off[e + 1] - a.off[e] + C::NBMAX - 1) / C::NBMAX;
         }
         int x = v;
 #pragma unroll
@@ -699,6 +700,247 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
     }
 }
 
+// ==========================================================================================================
+// k_wide: prefill items of the bf16 (HIGH tier) experts as 128 x 256 tiles (weights M = 128, tokens N <= 256).
+// A 128 x 128 tile reads 32 KB of operands per 64-wide K chunk for 2.1 MFLOP; a 128 x 256 tile reads 48 KB for
+// 4.2 MFLOP, so the operand stream from L2 per flop drops by a quarter and the tensor pipe issues twice the work
+// per barrier round trip.  No dequant warps: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-9 two
+// epilogue teams (team t drains accumulator buffer t: two 256-column fp32 accumulators = all of TMEM), warp 10
+// the scheduler (work items (expert, 256-token tile, row block) over the HIGH experts, through the same global
+// ticket counter protocol as k_gemm).  The epilogues are k_gemm's (SwiGLU pairing of gate/up rows; gate scaling
+// and the scatter to Y for down).
+constexpr int WD_STAGES = 4, WD_B = 256 * 128, WD_STAGE = A_BYTES + WD_B;
+constexpr int WD_W_EPI = 2, WD_TEAMS = 2, WD_W_SCHED = WD_W_EPI + 4 * WD_TEAMS, WD_THREADS = 32 * (WD_W_SCHED + 1);
+constexpr int WD_SMEM = 1024 + WD_STAGES * WD_STAGE + WD_TEAMS * XCH_BYTES + 1024 + RING * 32 + TPRE_BYTES;
+static_assert(WD_SMEM + 2 * 256 * 8 + 128 <= 232448, "k_wide shared memory");
+
+template <int PHASE>
+__global__ void __launch_bounds__(WD_THREADS, 1) k_wide(const __grid_constant__ GemmMaps maps, GemmArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sS = smem;
+    float* xch = reinterpret_cast<float*>(sS + WD_STAGES * WD_STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + WD_TEAMS * XCH_BYTES);
+    uint64_t* full = bars;
+    uint64_t* empty = full + WD_STAGES;
+    uint64_t* tfull = empty + WD_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* tkfull = tempty + 2;
+    uint64_t* tkempty = tkfull + RING;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tkempty + RING);
+    Tick* ring = reinterpret_cast<Tick*>(reinterpret_cast<uint8_t*>(bars) + 1024);
+    int32_t* tpre = reinterpret_cast<int32_t*>(ring + RING);
+    constexpr int NT = 256;
+
+    const int K = PHASE == 0 ? a.H : a.I;
+    const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
+    const int nk = K / KCH;
+    const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < WD_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+        for (int b = 0; b < RING; ++b) { mbar_init(&tkfull[b], 1); mbar_init(&tkempty[b], WD_W_SCHED); }
+        fence_mbar_init();
+        tma_prefetch(&maps.xw);
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    DX_GRID_WAIT();
+    DX_GRID_LAUNCH();
+    const int n_act = a.n_act[0];
+    {
+        // 256-token tiles of the HIGH (bf16) experts, exclusive prefix over the active list (n_act <= 513)
+        __shared__ int32_t wsum[32];
+        int tot = 0;
+        for (int base0 = 0; base0 <= n_act; base0 += WD_THREADS) {
+            const int t = base0 + threadIdx.x;
+            int v = 0;
+            if (t < n_act) {
+                const int e = a.act_e[t];
+                v = (e >= a.E_loc || a.tier[e]) ? (a.off[e + 1] - a.off[e] + NT - 1) / NT : 0;
+            }
+            int x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            int base = tot;
+            for (int w2 = 0; w2 < warp; ++w2) base += wsum[w2];
+            if (t <= n_act) tpre[t] = base + x - v;
+            int all = 0;
+            for (int w2 = 0; w2 < WD_THREADS / 32; ++w2) all += wsum[w2];
+            __syncthreads();
+            tot += all;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const int n_items = tpre[n_act] * nmb;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+    if (warp == 0) {
+        int st = 0;
+        uint32_t ph = 0;
+        Item w;
+        const CUtensorMap* amap = PHASE == 0 ? &maps.a16_gu : &maps.a16_dn;
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
+            const int rb = box_rows(w.m);
+            const CUtensorMap* bmap = rb == 256 ? &maps.xw : &maps.xb[rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : 3];
+            const int arow = PHASE == 0 ? w.mb * 64 : w.mb * 128;
+            for (int kb = 0; kb < nk; ++kb) {
+                gwait(&empty[st], ph ^ 1, 2, 128);
+                if (elect_one()) {
+                    uint8_t* sA = sS + st * WD_STAGE;
+                    mbar_arrive_expect_tx(&full[st], A_BYTES + rb * 128);
+                    if (PHASE == 0) tma_load_4d(sA, amap, &full[st], kb * KCH, arow, 0, w.slot);
+                    else tma_load_3d(sA, amap, &full[st], kb * KCH, arow, w.slot);
+                    tma_load_2d(sA + A_BYTES, bmap, &full[st], kb * KCH, w.r0);
+                }
+                __syncwarp();
+                if (++st == WD_STAGES) { st = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        int st = 0, cc = 0;
+        uint32_t ph = 0;
+        Item w;
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii, ++cc) {
+            const int rb = box_rows(w.m);
+            const uint32_t idesc = idesc_bf16(128, rb);
+            const int buf = cc & 1;
+            gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, DX_EPI_BACK / 2);
+            tc_fence_after();
+            const uint32_t d = tmem + buf * 256;
+            for (int kb = 0; kb < nk; ++kb) {
+                gwait(&full[st], ph, 4, 64);
+                tc_fence_after();
+                const uint32_t sA = smem_u32(sS + st * WD_STAGE);
+                const uint64_t da = umma_desc_sw128(sA), db = umma_desc_sw128(sA + A_BYTES);
+                if (elect_one()) {
+#pragma unroll
+                    for (int s = 0; s < KCH / 16; ++s) mma_bf16(d, da + 2 * s, db + 2 * s, idesc, (kb | s) != 0);
+                    mma_commit(&empty[st]);
+                }
+                __syncwarp();
+                if (++st == WD_STAGES) { st = 0; ph ^= 1; }
+            }
+            if (elect_one()) mma_commit(&tfull[buf]);
+            __syncwarp();
+        }
+    } else if (warp == WD_W_SCHED) {
+        int* ctr = a.sched + 4 + 2 * PHASE;
+        for (int ii = 0;; ++ii) {
+            const int sl = ii % RING;
+            gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11, 256);
+            int item = 0;
+            if (lane == 0) {
+                item = atomicAdd(ctr, 1);
+                ring[sl].v = item >= n_items ? make_int4(0, 0, 0, 0) : decode_tiled(a, tpre, n_act, item, nmb, NT);
+                ring[sl].item = item;
+                mbar_arrive(&tkfull[sl]);
+            }
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= n_items) break;
+        }
+    } else {
+        // epilogue teams (as k_gemm's prefill epilogue)
+        const int team = (warp - WD_W_EPI) >> 2;
+        const int q = warp & 3;
+        const int et = threadIdx.x - 32 * (WD_W_EPI + 4 * team);
+        const uint32_t nbar = 1 + team;
+        float* xch_t = xch + team * (XCH_BYTES / 4);
+        __shared__ int32_t ent_w[2][256];                 // phase 1: the chunk's entry ids / gates, per team
+        __shared__ float gate_w[2][256];
+        int32_t* ent_t = ent_w[team];
+        float* gate_t = gate_w[team];
+        int cc = 0;
+        Item w;
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii, ++cc) {
+            const int buf = cc & 1;
+            if (buf != team) continue;
+            const int nvalid = w.m;
+            if (PHASE == 1) {
+                for (int i = et; i < nvalid; i += 128) {
+                    const int ent = a.perm[w.r0 + i];
+                    ent_t[i] = ent;
+                    gate_t[i] = a.gate[ent];
+                }
+            }
+            gwait(&tfull[buf], (cc >> 1) & 1, 9, DX_EPI_BACK);
+            tc_fence_after();
+            named_bar(nbar, 128);
+            for (int col = 0; col < nvalid; col += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + buf * 256 + ((uint32_t)(32 * q) << 16) + col, v);
+                tmem_ld_wait();
+                if (PHASE == 0) {
+                    float* xu = xch_t;
+                    float* xg = xch_t + 16 * 64;
+                    const int rr = 32 * (q & 1) + lane;
+                    if (q >= 2) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) xu[j * 64 + rr] = __uint_as_float(v[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) xg[j * 64 + rr] = __uint_as_float(v[16 + j]);
+                    }
+                    named_bar(nbar, 128);
+                    const int f = w.mb * 64 + rr;
+                    const int j0 = q < 2 ? 0 : 16;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const int j = j0 + jj;
+                        if (col + j < nvalid) {
+                            const float gv = q < 2 ? __uint_as_float(v[jj]) : xg[jj * 64 + rr];
+                            const float uv = q < 2 ? xu[jj * 64 + rr] : __uint_as_float(v[16 + jj]);
+                            const float sg = __fdividef(gv, 1.0f + __expf(-gv));
+                            a.act[(size_t)(w.r0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
+                        }
+                    }
+                    named_bar(nbar, 128);
+                } else {
+                    const int h = w.mb * 128 + 32 * q + lane;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (col + j < nvalid && h < a.H) {
+                            const int ent = ent_t[col + j];
+                            a.Y[(size_t)ent * a.H + h] = __float2bfloat16_rn(gate_t[col + j] * __uint_as_float(v[j]));
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+            named_bar(nbar, 128);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+    if (threadIdx.x == 0) {
+        int* ctr = a.sched + 4 + 2 * PHASE;
+        __threadfence();
+        if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+            atomicExch(ctr, 0);
+            atomicExch(ctr + 1, 0);
+        }
+    }
+}
+
+template <int PHASE>
+void launch_wide_one(const GemmMaps& maps, const GemmArgs& a, int items, cudaStream_t st) {
+    static unsigned long long attr_mask = 0;
+    if (dx_first_on_device(attr_mask)) cudaFuncSetAttribute(k_wide<PHASE>, cudaFuncAttributeMaxDynamicSharedMemorySize, WD_SMEM);
+    const int grid = items < DX_NUM_SMS ? items : DX_NUM_SMS;
+    dx_launch(k_wide<PHASE>, dim3(grid), dim3(WD_THREADS), WD_SMEM, st, g_dx_pdl, maps, a);
+}
+
 template <int PHASE, bool DEC>
 void launch_one(const GemmMaps& maps, const GemmArgs& a, int items, cudaStream_t st) {
     using C = Cfg<DEC>;
@@ -713,6 +955,16 @@ void launch_one(const GemmMaps& maps, const GemmArgs& a, int items, cudaStream_t
 }  // namespace
 
 bool gemm_decode_cfg(int T) { return T <= 64; }
+
+bool wide_enabled() {
+    static const bool on = [] { const char* e = getenv("DX_WIDE"); return !e || atoi(e) != 0; }();
+    return on;
+}
+void launch_wide(int phase, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st) {
+    if (max_items <= 0) return;
+    if (phase == 0) launch_wide_one<0>(maps, a, max_items, st);
+    else launch_wide_one<1>(maps, a, max_items, st);
+}
 
 static uint32_t* g_trap_host = nullptr;
 void gemm_trap_init() {
