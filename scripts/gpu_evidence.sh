@@ -12,7 +12,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.l
 timeout 900 python bench.py > $O/${T}_bench.json 2> $O/${T}_bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --switch-stress > $O/${T}_c5.json 2> $O/${T}_c5.err; echo "c5 rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/${T}_bench_reference.json 2> $O/${T}_ref.err; echo "ref rc=$?"
-K='regex:k_(router|route|place|gemm|combine|fold|plan|xfer|gather|dec|scan|corr|shared)'
+K='regex:k_(router|route|place|gemm|wide|combine|fold|plan|xfer|gather|dec|scan|corr|shared)'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -s 400 -c 400 --csv --log-file $O/${T}_launches.csv \
   python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e --prefill-tokens 0 --no-batch-sweep --no-q80b --no-teleport --no-prefetch-leg > $O/${T}_ll.log 2>&1
 python scripts/launch_summary.py $O/${T}_launches.csv > $O/${T}_launch_summary.txt; cat $O/${T}_launch_summary.txt
@@ -22,6 +22,6 @@ python scripts/launch_summary.py $O/${T}_prefill_launches.csv > $O/${T}_prefill_
 DX_LOG_BYTES=1 DX_WATCHDOG_S=60 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gemm' -s 400 -c 4 -o $O/${T}_ncu_decode -f \
   python bench.py --layers 8 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --prefill-tokens 0 --no-batch-sweep --no-q80b --no-teleport --no-prefetch-leg > $O/${T}_ncu_decode.log 2>&1
 echo "ncu decode rc=$?"
-DX_WATCHDOG_S=60 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gemm' -s 200 -c 2 -o $O/${T}_ncu_prefill -f \
+DX_WATCHDOG_S=60 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_(gemm|wide)' -s 200 -c 4 -o $O/${T}_ncu_prefill -f \
   python bench.py --batch 4096 --layers 4 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --prefill-tokens 0 --no-batch-sweep --no-q80b --no-teleport --no-prefetch-leg > $O/${T}_ncu_prefill.log 2>&1
 echo "ncu prefill rc=$?"
