@@ -1004,7 +1004,8 @@ void launch_route(const float* logits, int T, int E, int k, int e_lo, const Rout
 }
 
 bool route_dec_ok(int T, int E, int k) {
-    return T >= 1 && T * k <= RDEC_MAX_ENT && E <= 512 && E % 32 == 0 && k <= ROUTE_MAX_K;
+    // T <= 128: at most 8 clusters of 8 CTAs, so the grid barrier's CTAs are always co-resident
+    return T >= 1 && T <= 128 && T * k <= RDEC_MAX_ENT && E <= 512 && E % 32 == 0 && k <= ROUTE_MAX_K;
 }
 
 template <int NVT>
