@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
             gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11, 256);
             int item = 0;
             if (lane == 0) {
-                item = atomicAdd(ctr, 1);
+                item = ii == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(ctr, 1);   // first item static: no atomic round trip
                 ring[sl].v = item >= n_items ? make_int4(0, 0, 0, 0)
                            : DEC ? decode_raw(a, etab, item, nmb) : decode_tiled(a, tpre, n_act, item, nmb, C::NBMAX);
                 ring[sl].item = item;
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(WD_THREADS, 1) k_wide(const __grid_constant__ 
             gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11, 256);
             int item = 0;
             if (lane == 0) {
-                item = atomicAdd(ctr, 1);
+                item = ii == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(ctr, 1);   // first item static: no atomic round trip
                 ring[sl].v = item >= n_items ? make_int4(0, 0, 0, 0) : decode_tiled(a, tpre, n_act, item, nmb, NT);
                 ring[sl].item = item;
                 mbar_arrive(&tkfull[sl]);

@@ -523,7 +523,8 @@ __global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
     if (a.wr && CS > 1) cluster_barrier();               // the cluster's partials are no longer read
     RDEC_T(3)
     for (int i = threadIdx.x; i < RDEC_CHUNKS * E; i += blockDim.x) chist[i] = 0;
-    grid_sync(a.ws.gbar);
+    if ((int)gridDim.x == CS && CS > 1) cluster_barrier();  // T <= 16: the grid is one cluster
+    else grid_sync(a.ws.gbar);
     RDEC_T(4)
     DX_GRID_LAUNCH();                       // every CTA is resident and past the barrier
     // ---------------- C: histograms, offsets, active list (every CTA, identical results)
