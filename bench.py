@@ -438,6 +438,11 @@ def run_ours(a, rank, world, local_rank):
     ffn_ms = prof["ffn_ms"]
     ach0 = wb[0] / (ffn_ms[0] / 1e3) / 1e9 if ffn_ms[0] > 0 else 0.0
     ach_all = (wb[0] + wb[1]) / ((ffn_ms[0] + ffn_ms[1]) / 1e3) / 1e9
+    fused = prof.get("ffn_fused", 0) > 0     # decode FFN as ONE launch: the roofline kernel covers both phases
+    rf_kernel = ("k_gemm<2,1> fused decode FFN: gate/up + SwiGLU, then down + gate scaling, one persistent launch "
+                 "(tcgen05)") if fused else "k_gemm<0> decode gate/up + SwiGLU (tcgen05)"
+    rf_ach = ach_all if fused else ach0
+    rf_bytes = (wb[0] + wb[1]) if fused else wb[0]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ffn_traffic.json")
     if os.path.exists(tpath):
@@ -456,14 +461,14 @@ def run_ours(a, rank, world, local_rank):
                    "global_batch": B * world,
                    "parallelism": f"ep{G}" if ep_mode else (f"replicas x{world}" if world > 1 else "single"),
                    "l2": "no flush: each step streams >=48 distinct layers of weights (> 126 MB L2)"},
-        "roofline": {"bound": "hbm", "kernel": "k_gemm<0> decode gate/up + SwiGLU (tcgen05)", "achieved": ach0, "peak": peak,
-                     "unit": "GB/s", "frac": ach0 / peak, "traffic": traffic, "peak_source": peak_src,
+        "roofline": {"bound": "hbm", "kernel": rf_kernel, "achieved": rf_ach, "peak": peak,
+                     "unit": "GB/s", "frac": rf_ach / peak, "traffic": None if fused else traffic, "peak_source": peak_src,
                      "ffn_both_phases_gbs": ach_all, "ffn_both_frac": ach_all / peak,
                      # the whole layer (routing, both GEMMs, combine, fold, plan periods, switching): every touched
                      # expert's algorithmic weight bytes over the device time of the whole timed stack
                      "layer_achieved": (wb[0] + wb[1]) / max(prof["forwards"], 1) * L * a.steps / (ms / 1e3) / 1e9,
                      "layer_frac": (wb[0] + wb[1]) / max(prof["forwards"], 1) * L * a.steps / (ms / 1e3) / 1e9 / peak,
-                     "algorithmic_bytes_per_launch": wb[0] / max(prof["forwards"], 1)},
+                     "algorithmic_bytes_per_launch": rf_bytes / max(prof["forwards"], 1)},
         "gpu_launches": launches,
         "e2e": e2e,
         "extra": {"ffn_ms_share": (ffn_ms[0] + ffn_ms[1]) * scale / ms if ms > 0 else None,
@@ -905,10 +910,11 @@ def tier_brackets(a, cfg0, ptrs, L, E, H, B, dev, stream, peak, wr_arr, bias_arr
         pool.close()
         wb = prof["weight_bytes"][0] + prof["weight_bytes"][1]
         ffn_s = (prof["ffn_ms"][0] + prof["ffn_ms"][1]) / 1e3
-        g0 = prof["weight_bytes"][0] / (prof["ffn_ms"][0] / 1e3) / 1e9 if prof["ffn_ms"][0] > 0 else 0.0
+        g0 = (prof["weight_bytes"][0] / (prof["ffn_ms"][0] / 1e3) / 1e9
+              if prof["ffn_ms"][0] > 0 and not prof.get("ffn_fused", 0) else None)
         gbs = wb / ffn_s / 1e9 if ffn_s > 0 else 0.0
         out[name] = {"n_hot": n_hot, "value": B * L * n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / n,
-                     "weight_bytes_per_layer": wb / max(prof["forwards"], 1), "gateup_gbs": g0, "gateup_frac": g0 / peak,
+                     "weight_bytes_per_layer": wb / max(prof["forwards"], 1), "gateup_gbs": g0, "gateup_frac": g0 / peak if g0 is not None else None,
                      "ffn_weight_gbs": gbs, "ffn_hbm_frac": gbs / peak}
     return out
 

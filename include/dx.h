@@ -303,6 +303,8 @@ typedef struct {
     uint64_t ssd_bytes;
     double   ssd_read_ms;       /* host time spent in those reads */
     int64_t  dram_cache_hits;   /* HIGH images served by the DRAM cache */
+    int64_t  ffn_fused;         /* profiled forwards whose FFN was ONE fused decode launch (gate/up then down):
+                                   their whole FFN time is in ffn_ms[0] and ffn_ms[1] is ~0 */
 } dx_profile_t;
 /* f-1 cross-layer correlation prefetch.  fanout f in [0, 8] (0 = off), lead d in
  * [1, Tp - L].  With f > 0 every dx_moe_forward / dx_moe_step of layer l (the stack called layer by layer on the

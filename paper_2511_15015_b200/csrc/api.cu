@@ -65,6 +65,8 @@ struct dx_pool_s {
     __nv_bfloat16* Y = nullptr;
     int32_t* err_flag = nullptr;
     int32_t* dev_err = nullptr;             // sticky device-side error (EP routed rows), reported by dx_sync
+    int32_t* dn_done = nullptr;         // fused decode FFN: gate/up items done per active expert (self-resetting)
+    int64_t prof_fused = 0;             // profiled forwards whose FFN ran as one fused launch
     int32_t* gemm_sched = nullptr;      // [kernel: k_gemm, k_wide][phase][ticket counter, CTAs done] (self-resetting)
     int2* manual_cmds = nullptr;
     int32_t* manual_status = nullptr;
@@ -654,7 +656,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     p->Xp = carve<__nv_bfloat16>(q, n_ent * p->H);
     p->err_flag = carve<int32_t>(q, 1);
     p->dev_err = carve<int32_t>(q, 1);
-    p->gemm_sched = carve<int32_t>(q, 8);
+    p->gemm_sched = carve<int32_t>(q, 12);
+    p->dn_done = carve<int32_t>(q, (size_t)p->E_loc + 64);
     p->manual_cmds = carve<int2>(q, 1024);
     p->manual_status = carve<int32_t>(q, 1024);
     p->corr = carve<uint32_t>(q, (size_t)(L > 1 ? L - 1 : 0) * E * E);
@@ -800,7 +803,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         DX_CUDA(cudaMemcpyAsync(c.plan_n, pn.data(), L * 4, cudaMemcpyHostToDevice, p->cs));
         DX_CUDA(cudaMemsetAsync(p->err_flag, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(p->dev_err, 0, 4, p->cs));
-        DX_CUDA(cudaMemsetAsync(p->gemm_sched, 0, 32, p->cs));
+        DX_CUDA(cudaMemsetAsync(p->gemm_sched, 0, 48, p->cs));
+        DX_CUDA(cudaMemsetAsync(p->dn_done, 0, ((size_t)p->E_loc + 64) * 4, p->cs));
         DX_CUDA(cudaMemsetAsync(w.stats, 0, 4 * 8, p->cs));
         DX_CUDA(cudaMemsetAsync(w.done, 0, 4, p->cs));
         DX_CUDA(cudaMemsetAsync(w.gbar, 0, 8, p->cs));
@@ -1083,6 +1087,8 @@ extern "C" dx_status dx_profile_read(dx_pool p, dx_profile_t* out) {
     p->prof_xfer_ev.clear();
     out->forwards = p->prof_fwd;
     p->prof_fwd = 0;
+    out->ffn_fused = p->prof_fused;
+    p->prof_fused = 0;
     u64 st[4];
     DX_CUDA(cudaMemcpy(st, p->ws.stats, sizeof(st), cudaMemcpyDeviceToHost));
     DX_CUDA(cudaMemset(p->ws.stats, 0, sizeof(st)));
@@ -1311,10 +1317,22 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         // prefill with a bf16 HIGH tier: those experts' items run as 128 x 256 tiles in k_wide, the rest in k_gemm
         const bool wide = !dec && p->hi.bits == 16 && wide_enabled();
         ga.skip_bf16 = wide ? 1 : 0;
+        ga.dn_done = p->dn_done;
         GemmMaps gm = p->gmaps[layer];
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb0[i];
         for (int i = 0; i < 3; ++i) gm.xk[i] = p->xk0[i];
         gm.xw = p->xw0;
+        static const bool fuse_on = [] { const char* e = getenv("DX_FUSE"); return !e || atoi(e) != 0; }();
+        if (dec && fuse_on) {
+            // decode: gate/up + SwiGLU and down + gate scaling in ONE launch (down items wait per expert)
+            for (int i = 0; i < 4; ++i) gm.xb1[i] = p->xb1[i];
+            for (int i = 0; i < 3; ++i) gm.xk1[i] = p->xk1[i];
+            launch_gemm(2, true, gm, ga, max_act * (p->I / 64 + (p->H + 127) / 128), p->cs);
+            if (ev[2]) {
+                DX_CUDA(cudaEventRecord(ev[2], p->cs));
+                ++p->prof_fused;
+            }
+        } else {
         if (wide) launch_wide(0, gm, ga, max_act * (p->I / 64), p->cs);
         launch_gemm(0, dec, gm, ga, max_act * (p->I / 64), p->cs);
         if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
@@ -1323,6 +1341,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         gm.xw = p->xw1;
         if (wide) launch_wide(1, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
         launch_gemm(1, dec, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
+        }
         }
     }
     if (ev[3]) DX_CUDA(cudaEventRecord(ev[3], p->cs));

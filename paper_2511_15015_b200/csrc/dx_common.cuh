@@ -308,6 +308,7 @@ struct GemmMaps {
     // B operands (token rows [rows][K] bf16, 128 B swizzle)
     CUtensorMap xb[4];              // 2-D boxes {64, 16/32/64/128}
     CUtensorMap xw;                 // 2-D box {64, 256}: the wide prefill tiles of k_wide
+    CUtensorMap xb1[4], xk1[3];     // fused decode launch: the down phase's B maps (act rows)
     CUtensorMap xk[3];              // 3-D {64, rows, K/64}: boxes {64,16,4}, {64,32,4}, {64,16,8} (decode int stages)
 };
 struct GemmArgs {
@@ -328,6 +329,7 @@ struct GemmArgs {
     int* sched;                     // [phase][ticket counter, CTAs done]: dynamic work-item hand-out, zero
                                     // between launches (the last CTA of a launch resets it)
     int skip_bf16;                  // prefill k_gemm: the leading bf16 (HIGH, 16-bit) experts are k_wide's
+    int* dn_done;                   // fused decode launch: gate/up items finished per active expert (self-resetting)
     int dbg;                        // performance experiments only (DX_GEMM_DBG): 4 skip the A-in-TMEM MMAs,
                                     // 5 skip the dequant transform, 6 both, 13 = 6 with plain
                                     // arrivals instead of tcgen05.commit on int stages

@@ -176,9 +176,15 @@ __device__ __forceinline__ void gwait(uint64_t* bar, uint32_t parity, uint32_t t
     gwait_slow(a, parity, tag, backoff_ns);
 }
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 // Decoded work item: 128-row block mb of an active expert, its token rows [r0, r0+m), tier / slot / bits.
 struct Item {
     int mb, r0, m, ti, slot, bits;
+    int ph, ae;            // phase (fused decode launch) and active-expert index of the item
 };
 // Prefill work items are (expert, N tile of NT token rows, row block): the N tiles of every active expert
 // are numbered by the prefix tpre[] (so a hot expert's thousands of rows spread over many SMs instead of
@@ -211,7 +217,7 @@ struct Tick {
 // The ii-th item of this CTA, from the ring (every field warp-uniform: read by lane 0, broadcast).  The
 // warp then releases the ring entry.  Returns false after the last item.
 __device__ __forceinline__ bool take_item(const GemmArgs& a, const Tick* ring, uint64_t* tkfull, uint64_t* tkempty,
-                                          int ii, int n_items, int nmb, Item& it) {
+                                          int ii, int n_items, int nmb, Item& it, int n0 = -1, int nmb1 = 1) {
     const int sl = ii % RING;
     gwait(&tkfull[sl], (ii / RING) & 1, 10, 128);
     int4 v = ring[sl].v;
@@ -224,7 +230,15 @@ __device__ __forceinline__ bool take_item(const GemmArgs& a, const Tick* ring, u
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&tkempty[sl]);
     if (item >= n_items) return false;
-    it.mb = item % nmb;
+    if (n0 >= 0 && item >= n0) {                       // fused decode launch: down items follow the gate/up items
+        it.ph = 1;
+        it.mb = (item - n0) % nmb1;
+        it.ae = (item - n0) / nmb1;
+    } else {
+        it.ph = 0;
+        it.mb = item % nmb;
+        it.ae = item / nmb;
+    }
     it.r0 = v.x;
     it.m = v.y;
     it.slot = v.z;
@@ -266,11 +280,16 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
     int32_t* tpre = reinterpret_cast<int32_t*>(tabs + 2 * TAB_BYTES); // [n_act + 1] prefill N-tile prefix
     int4* etab = reinterpret_cast<int4*>(tabs + 2 * TAB_BYTES);       // decode: [EMAX] the active experts' items
 
-    const int K = PHASE == 0 ? a.H : a.I;
-    const int nmb = PHASE == 0 ? a.I / 64 : (a.H + 127) / 128;
-    const int nk = K / KCH;
-    const int G = K / a.g;                                // quantisation groups per weight row
-    const bool tab_ok = G <= GTAB;                        // per-item scale/zero tables staged by TMA
+    // PHASE 2 (decode only): ONE launch runs the gate/up items and then the down items of every active expert; a
+    // down item is handed out only after all gate/up items of its expert have written their act rows (per-expert
+    // completion counters), so the down work of early experts overlaps the gate/up tail of late ones.
+    constexpr bool FUSED = PHASE == 2;
+    static_assert(!FUSED || DEC, "the fused launch is the decode configuration");
+    const int nmb0 = a.I / 64, nmb1 = (a.H + 127) / 128;
+    const int nmb = PHASE == 1 ? nmb1 : nmb0;             // (fused: of the first n0 items)
+    const int nk_[2] = {a.H / KCH, a.I / KCH};
+    const int G_[2] = {a.H / a.g, a.I / a.g};             // quantisation groups per weight row
+    const bool tab_ok_[2] = {G_[0] <= GTAB, G_[1] <= GTAB};   // per-item scale/zero tables staged by TMA
     // warp index made provably warp-uniform: role branches are uniform and the single-thread issue paths
     // keep their operands in uniform registers
     const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
@@ -292,6 +311,8 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
     DX_GRID_LAUNCH();
     const int n_act = a.n_act[0];
     int n_items = n_act * nmb;
+    const int n0 = FUSED ? n_act * nmb0 : -1;              // fused: items [0, n0) gate/up, [n0, n_items) down
+    if (FUSED) n_items = n_act * (nmb0 + nmb1);
     if (!DEC) {
         // N tiles per active expert, exclusive prefix over the active list (n_act <= 512 < blockDim)
         __shared__ int32_t wsum[32];
@@ -336,8 +357,12 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         int st = 0, tc = 0;
         uint32_t ph = 0;
         Item w;
-        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w, n0, nmb1); ++ii) {
+            const int iph = FUSED ? w.ph : PHASE;
+            const int nk = nk_[iph], G = G_[iph];
+            const bool tab_ok = tab_ok_[iph];
             const bool qt = w.bits != 16;
+            if (FUSED && iph == 1) asm volatile("fence.proxy.async.global;" ::: "memory");   // act rows: generic -> TMA
             if (qt && tab_ok) {
                 // this item's scales / zeros: contiguous row spans of the slot's [rows][G] tables
                 const int tb = tc & 1;
@@ -348,7 +373,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                     const uint8_t* sb = a.layer + (w.ti ? a.hi_base + (int64_t)w.slot * a.hi.bytes : (int64_t)w.slot * a.lo.bytes);
                     uint8_t* ts = tabs + tb * TAB_BYTES;
                     uint8_t* tz = ts + 128 * GTAB * 2;
-                    if (PHASE == 0) {
+                    if (iph == 0) {
                         const uint32_t sbytes = 64 * G * 2, zbytes = 64 * G;
                         mbar_arrive_expect_tx(&tabfull[tb], 2 * (sbytes + zbytes));
                         for (int m = 0; m < 2; ++m) {        // gate rows -> table rows 0-63, up rows -> 64-127
@@ -369,26 +394,28 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                 __syncwarp();
             }
             const CUtensorMap* amap =
-                PHASE == 0 ? (!qt ? &maps.a16_gu : DEC ? (w.ti ? &maps.whi_gu : &maps.wlo_gu) : (w.ti ? &maps.ahi_gu : &maps.alo_gu))
+                iph == 0 ? (!qt ? &maps.a16_gu : DEC ? (w.ti ? &maps.whi_gu : &maps.wlo_gu) : (w.ti ? &maps.ahi_gu : &maps.alo_gu))
                            : (!qt ? &maps.a16_dn : DEC ? (w.ti ? &maps.whi_dn : &maps.wlo_dn) : (w.ti ? &maps.ahi_dn : &maps.alo_dn));
             const int nb = C::nb(w.bits), ks = C::ks(w.bits);
-            const int arow = PHASE == 0 ? w.mb * 64 : w.mb * 128;
+            const int arow = iph == 0 ? w.mb * 64 : w.mb * 128;
+            const CUtensorMap* xbm = (FUSED && iph == 1) ? maps.xb1 : maps.xb;
+            const CUtensorMap* xkm = (FUSED && iph == 1) ? maps.xk1 : maps.xk;
             const int kunit = qt ? KCH * w.bits / 8 : KCH;     // A inner coordinate per chunk (bytes / elements)
-            for (int n0 = 0; n0 < w.m; n0 += nb) {
-                const int rb = box_rows(min(nb, w.m - n0));
+            for (int c0 = 0; c0 < w.m; c0 += nb) {
+                const int rb = box_rows(min(nb, w.m - c0));
                 const int ri = rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : 3;
                 const bool multi = DEC && qt;                   // one B box carries the stage's ks chunks
-                const CUtensorMap* bmap = multi ? &maps.xk[w.bits == 2 ? 2 : ri] : &maps.xb[ri];
+                const CUtensorMap* bmap = multi ? &xkm[w.bits == 2 ? 2 : ri] : &xbm[ri];
                 const uint32_t bytes = multi ? A_BYTES + ks * rb * 128 : (qt ? 128 * kunit : A_BYTES) + rb * 128;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
                     gwait(&empty[st], ph ^ 1, 2, 128);
                     if (elect_one()) {
                         uint8_t* sA = sS + st * STAGE_BYTES;
                         mbar_arrive_expect_tx(&full[st], bytes);
-                        if (PHASE == 0) tma_load_4d(sA, amap, &full[st], kb0 * kunit, arow, 0, w.slot);
+                        if (iph == 0) tma_load_4d(sA, amap, &full[st], kb0 * kunit, arow, 0, w.slot);
                         else tma_load_3d(sA, amap, &full[st], kb0 * kunit, arow, w.slot);
-                        if (multi) tma_load_3d(sA + A_BYTES, bmap, &full[st], 0, w.r0 + n0, kb0);
-                        else tma_load_2d(sA + A_BYTES, bmap, &full[st], kb0 * KCH, w.r0 + n0);
+                        if (multi) tma_load_3d(sA + A_BYTES, bmap, &full[st], 0, w.r0 + c0, kb0);
+                        else tma_load_2d(sA + A_BYTES, bmap, &full[st], kb0 * KCH, w.r0 + c0);
                     }
                     __syncwarp();
                     if (++st == STAGES) { st = 0; ph ^= 1; }
@@ -401,10 +428,11 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         int st = 0, ab = 0, cc = 0;
         uint32_t ph = 0, aph = 0;
         Item w;
-        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w, n0, nmb1); ++ii) {
+            const int nk = nk_[FUSED ? w.ph : PHASE];
             const int nb = C::nb(w.bits), ks = C::ks(w.bits);
-            for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
-                const int rb = box_rows(min(nb, w.m - n0));
+            for (int c0 = 0; c0 < w.m; c0 += nb, ++cc) {
+                const int rb = box_rows(min(nb, w.m - c0));
                 const uint32_t idesc = idesc_bf16(128, rb);
                 const int buf = cc & 1;
                 gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, DX_EPI_BACK / 2);
@@ -474,7 +502,6 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         const int qa = warp & 3;
         const int r = 32 * qa + lane;
         const uint32_t rsw = r & 7;                        // 128 B swizzle phase of this row
-        const int mat_rows = PHASE == 0 ? a.I : a.H;
         const uint32_t lane_base = tmem_a + ((uint32_t)(32 * qa) << 16);
         const uint32_t stages_u32 = smem_u32(sS);
         const int gsh = 31 - __clz(a.g);                  // g is a power of two (checked at pool creation)
@@ -483,7 +510,11 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         int st = 0, ab = 0, tc = 0, nbuf = 0;
         uint32_t ph = 0, aph = 0;
         Item w;
-        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w, n0, nmb1); ++ii) {
+            const int iph = FUSED ? w.ph : PHASE;
+            const int nk = nk_[iph], G = G_[iph];
+            const bool tab_ok = tab_ok_[iph];
+            const int mat_rows = iph == 0 ? a.I : a.H;
             if (w.bits == 16) {                           // bf16 stages need no transform: observe their phases
                 const int nst = ((w.m + C::nb(16) - 1) / C::nb(16)) * nk;
                 for (int s = 0; s < nst; ++s) {
@@ -495,8 +526,8 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                 continue;
             }
             // row r of the item's A block: matrix mat (gate 0 / up 1 / down 2), row mrow of it
-            const int mat = PHASE == 0 ? (r >> 6) : 2;
-            const int mrow = PHASE == 0 ? w.mb * 64 + (r & 63) : w.mb * 128 + r;
+            const int mat = iph == 0 ? (r >> 6) : 2;
+            const int mrow = iph == 0 ? w.mb * 64 + (r & 63) : w.mb * 128 + r;
             const bool valid = mrow < mat_rows;
             const SlotLayout& L = w.ti ? a.hi : a.lo;
             const uint8_t* slot_base =
@@ -520,7 +551,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                 constexpr int KS = DEC ? 16 / BITS : 1;     // K chunks per stage
                 constexpr int ROWB = KCH * BITS / 8;        // code bytes per row per chunk
                 constexpr int NBB = DEC ? (BITS == 4 ? 32 : 16) : 128;
-                for (int n0 = 0; n0 < w.m; n0 += NBB) {
+                for (int c0 = 0; c0 < w.m; c0 += NBB) {
                     for (int kb0 = 0; kb0 < nk; kb0 += KS) {
                         // every transform thread observes every phase of full[] (no phase aliasing)
                         gwait(&full[st], ph, 7, DX_TBACK);
@@ -589,15 +620,23 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
     } else if (warp == W_SCHED) {
         // ------------------------------------------------ scheduler: claim a ticket, decode it, publish it
         // (the ring is only RING deep, so a CTA never hoards work another SM could start sooner)
-        int* ctr = a.sched + 2 * PHASE;
+        int* ctr = a.sched + (FUSED ? 8 : 2 * PHASE);
         for (int ii = 0;; ++ii) {
             const int sl = ii % RING;
             gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11, 256);
             int item = 0;
             if (lane == 0) {
                 item = ii == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(ctr, 1);   // first item static: no atomic round trip
+                if (FUSED && item >= n0 && item < n_items) {
+                    // a down item: wait until every gate/up item of its expert has published its act rows
+                    const unsigned* dd = reinterpret_cast<const unsigned*>(a.dn_done) + (item - n0) / nmb1;
+                    const long long t0 = clock64();
+                    while ((int)ld_acquire_u32(dd) < nmb0)
+                        if (clock64() - t0 > 8000000000ll) gemm_trap(12, 0);
+                }
                 ring[sl].v = item >= n_items ? make_int4(0, 0, 0, 0)
-                           : DEC ? decode_raw(a, etab, item, nmb) : decode_tiled(a, tpre, n_act, item, nmb, C::NBMAX);
+                           : DEC ? (FUSED && item >= n0 ? decode_raw(a, etab, item - n0, nmb1) : decode_raw(a, etab, item, nmb))
+                                 : decode_tiled(a, tpre, n_act, item, nmb, C::NBMAX);
                 ring[sl].item = item;
                 mbar_arrive(&tkfull[sl]);
             }
@@ -618,15 +657,16 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         float* gate_t = team == 0 ? gate_s : xch_t + 128;
         int cc = 0;
         Item w;
-        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w); ++ii) {
+        for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w, n0, nmb1); ++ii) {
+            const int iph = FUSED ? w.ph : PHASE;
             const int nb = C::nb(w.bits);
-            for (int n0 = 0; n0 < w.m; n0 += nb, ++cc) {
+            for (int c0 = 0; c0 < w.m; c0 += nb, ++cc) {
                 const int buf = cc & 1;
                 if (EPI_TEAMS == 2 && buf != team) continue;   // the other team's chunk
-                const int nvalid = min(nb, w.m - n0);
-                if (PHASE == 1) {                       // entry ids and gates of this chunk's tokens -> smem
+                const int nvalid = min(nb, w.m - c0);
+                if (iph == 1) {                         // entry ids and gates of this chunk's tokens -> smem
                     for (int i = et; i < nvalid; i += 128) {
-                        const int ent = a.perm[w.r0 + n0 + i];
+                        const int ent = a.perm[w.r0 + c0 + i];
                         ent_t[i] = ent;
                         gate_t[i] = a.gate[ent];
                     }
@@ -638,7 +678,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                     uint32_t v[32];
                     tmem_ld32(tmem + buf * C::NBMAX + ((uint32_t)(32 * q) << 16) + col, v);
                     tmem_ld_wait();
-                    if (PHASE == 0) {
+                    if (iph == 0) {
                         // gate rows 0-63 (warps q < 2) meet their up rows 64-127 (q >= 2) through smem, and all
                         // four warps share the SwiGLU: the gate warps take token columns 0-15 of the block (up
                         // values from smem), the up warps columns 16-31 (gate values from smem).
@@ -663,7 +703,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                                 const float gv = q < 2 ? __uint_as_float(v[jj]) : xg[jj * 64 + rr];
                                 const float uv = q < 2 ? xu[jj * 64 + rr] : __uint_as_float(v[16 + jj]);
                                 const float sg = __fdividef(gv, 1.0f + __expf(-gv));
-                                a.act[(size_t)(w.r0 + n0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
+                                a.act[(size_t)(w.r0 + c0 + col + j) * a.I + f] = __float2bfloat16_rn(sg * uv);
                             }
                         }
                         named_bar(nbar, 128);
@@ -683,6 +723,14 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                 if (lane == 0) mbar_arrive(&tempty[buf]);
                 named_bar(nbar, 128);                      // ent_s / gate_s / xch reused by the next chunk
             }
+            if (FUSED && iph == 0) {                        // this gate/up item's act rows are written: count it
+                __threadfence();
+                named_bar(nbar, 128);
+                if (et == 0) {
+                    __threadfence();
+                    atomicAdd(a.dn_done + w.ae, 1);
+                }
+            }
         }
     }
     __syncthreads();
@@ -691,11 +739,13 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         tmem_dealloc<512>(tmem);
     }
     if (threadIdx.x == 0) {                           // the last CTA out resets the ticket counter for the
-        int* ctr = a.sched + 2 * PHASE;                // next launch (which reads it only after griddepcontrol.wait)
+        int* ctr = a.sched + (FUSED ? 8 : 2 * PHASE);  // next launch (which reads it only after griddepcontrol.wait)
         __threadfence();
         if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
             atomicExch(ctr, 0);
             atomicExch(ctr + 1, 0);
+            if (FUSED)
+                for (int i = 0; i < n_act; ++i) a.dn_done[i] = 0;   // every item is done: counters back to zero
         }
     }
 }
@@ -985,16 +1035,20 @@ void gemm_trap_init() {
 static const char* const k_trap_names[] = {"?", "tabempty (producer)", "empty (producer)", "tempty (MMA)", "full (MMA)",
                                            "aready (MMA)", "tabfull (transform)", "full (transform)",
                                            "aempty (transform)", "tfull (epilogue)", "tkfull (item ring)",
-                                           "tkempty (scheduler)"};
+                                           "tkempty (scheduler)", "gate/up completion (fused scheduler)"};
 int gemm_trap_report(char* buf, size_t n) {
     if (!g_trap_host || (g_trap_host[0] >> 16) != 0xDEADu) return 0;
     const uint32_t tag = g_trap_host[0] & 0xFFFFu;
     return snprintf(buf, n, " [k_gemm watchdog: wait on %s, parity %u, block %u, thread %u]",
-                    tag < 12 ? k_trap_names[tag] : "?", g_trap_host[1], g_trap_host[2], g_trap_host[3]);
+                    tag < 13 ? k_trap_names[tag] : "?", g_trap_host[1], g_trap_host[2], g_trap_host[3]);
 }
 
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st) {
     if (max_items <= 0) return;
+    if (phase == 2) {                                  // fused decode FFN (gate/up then down, one launch)
+        launch_one<2, true>(maps, a, max_items, st);
+        return;
+    }
     if (phase == 0) {
         if (dec) launch_one<0, true>(maps, a, max_items, st);
         else launch_one<0, false>(maps, a, max_items, st);

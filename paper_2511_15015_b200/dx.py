@@ -70,7 +70,7 @@ class dx_profile_t(ctypes.Structure):
                 ("promotions", ctypes.c_int64), ("demotions", ctypes.c_int64), ("copy_ms", ctypes.c_double),
                 ("copy_bytes", ctypes.c_uint64), ("prefetch_issued", ctypes.c_int64), ("prefetch_hits", ctypes.c_int64),
                 ("ssd_reads", ctypes.c_int64), ("ssd_bytes", ctypes.c_uint64), ("ssd_read_ms", ctypes.c_double),
-                ("dram_cache_hits", ctypes.c_int64)]
+                ("dram_cache_hits", ctypes.c_int64), ("ffn_fused", ctypes.c_int64)]
 
 
 class dx_plan(ctypes.Structure):
@@ -397,4 +397,4 @@ class Pool:
                     promotions=pr.promotions, demotions=pr.demotions, copy_ms=pr.copy_ms,
                     copy_bytes=int(pr.copy_bytes), prefetch_issued=pr.prefetch_issued, prefetch_hits=pr.prefetch_hits,
                     ssd_reads=pr.ssd_reads, ssd_bytes=int(pr.ssd_bytes), ssd_read_ms=pr.ssd_read_ms,
-                    dram_cache_hits=pr.dram_cache_hits)
+                    dram_cache_hits=pr.dram_cache_hits, ffn_fused=pr.ffn_fused)
