@@ -143,6 +143,9 @@ __device__ __noinline__ void gemm_trap(uint32_t tag, uint32_t parity) {
     }
     __trap();
 }
+#ifndef DX_STATIC_FIRST
+#define DX_STATIC_FIRST 0      // 1: each CTA's first work item is blockIdx.x (measured: slower whenever side-stream transfer blocks share SMs: C2 490 K vs 503 K layer-tok/s, exposed switch 7.1 vs 4.5 %)
+#endif
 #ifndef DX_EPI_BACK
 #define DX_EPI_BACK 256        // backoff (ns) of the epilogue's accumulator wait (MMA's drain wait: half)
 #endif
@@ -626,7 +629,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
             gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11, 256);
             int item = 0;
             if (lane == 0) {
-                item = ii == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(ctr, 1);   // first item static: no atomic round trip
+                item = (DX_STATIC_FIRST && ii == 0) ? (int)blockIdx.x : (DX_STATIC_FIRST ? (int)gridDim.x : 0) + atomicAdd(ctr, 1);   // first item static: no atomic round trip
                 if (FUSED && item >= n0 && item < n_items) {
                     // a down item: wait until every gate/up item of its expert has published its act rows
                     const unsigned* dd = reinterpret_cast<const unsigned*>(a.dn_done) + (item - n0) / nmb1;
@@ -887,7 +890,7 @@ __global__ void __launch_bounds__(WD_THREADS, 1) k_wide(const __grid_constant__ 
             gwait(&tkempty[sl], ((ii / RING) & 1) ^ 1, 11, 256);
             int item = 0;
             if (lane == 0) {
-                item = ii == 0 ? (int)blockIdx.x : (int)gridDim.x + atomicAdd(ctr, 1);   // first item static: no atomic round trip
+                item = (DX_STATIC_FIRST && ii == 0) ? (int)blockIdx.x : (DX_STATIC_FIRST ? (int)gridDim.x : 0) + atomicAdd(ctr, 1);   // first item static: no atomic round trip
                 ring[sl].v = item >= n_items ? make_int4(0, 0, 0, 0) : decode_tiled(a, tpre, n_act, item, nmb, NT);
                 ring[sl].item = item;
                 mbar_arrive(&tkfull[sl]);
