@@ -34,7 +34,6 @@ void dx_set_error(const char* fmt, ...) {
     size_t len = strlen(g_err);
     gemm_trap_report(g_err + len, sizeof(g_err) - len);
     len = strlen(g_err);
-    dec_trap_report(g_err + len, sizeof(g_err) - len);
 }
 extern "C" const char* dx_last_error(void) { return g_err; }
 extern "C" const char* dx_version(void) { return "dynaexq-b200 0.1 (sm_100a)"; }
@@ -103,8 +102,6 @@ struct dx_pool_s {
     CUtensorMap xb0[4], xb1[4];             // B operand maps (Xp / act) for tiles of 16, 32, 64, 128 rows
     CUtensorMap xw0, xw1;                   // the same, 256-row tiles (k_wide)
     CUtensorMap xk0[3], xk1[3];             // 3-D B maps (Xp / act): several K chunks per box (decode int)
-    std::vector<DecMaps> dec_maps;          // host: per-layer maps of the decode kernels (k_dec.cu)
-    DecBMaps dec_bmaps;
     // expert parallelism over NCCL (ep_nccl.cu): library-owned communicator and exchange buffers
     void* comm = nullptr;
     __nv_bfloat16 *ep_send_rows = nullptr, *ep_recv_rows = nullptr, *ep_y_rows = nullptr, *ep_back_rows = nullptr;
@@ -174,7 +171,6 @@ struct dx_pool_s {
     std::vector<cudaEvent_t> ev_planh;      // plan copied to the host
     std::vector<int> xfer_pending;          // per layer: plan made, transfers not yet issued
     int n_pending = 0;
-    bool use_kdec = false;                  // DX_DEC=1: the k_dec.cu decode kernels instead of k_gemm's decode
                                             // configuration (A/B runs; measured slower on the int tiers)
 };
 
@@ -261,53 +257,6 @@ static dx_status build_maps(dx_pool p) {
                         !make_map(&p->xw1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, bw, CU_TENSOR_MAP_SWIZZLE_128B)))) {
             dx_set_error("tensor map encoding failed (activations)");
             return DX_ERR_CUDA;
-        }
-    }
-    // decode kernels (k_dec.cu): per-layer A maps and the pool's B maps, copied to device memory
-    {
-        std::vector<DecMaps>& dm = p->dec_maps;
-        dm.assign(p->L, DecMaps{});
-        memset(dm.data(), 0, dm.size() * sizeof(DecMaps));
-        for (int l = 0; l < p->L; ++l) {
-            DecMaps& d = dm[l];
-            d.a16[0] = p->gmaps[l].a16_gu;
-            d.a16[1] = p->gmaps[l].a16_dn;
-            const uint8_t* lb = p->weights + (size_t)l * p->layer_bytes;
-            bool ok = true;
-            for (int t = 0; t < 2; ++t) {
-                const SlotLayout& Ls = t ? p->hi : p->lo;
-                if (Ls.bits == 16) continue;
-                const uint8_t* base = lb + (t ? p->hi_base : 0);
-                const uint64_t slots = t ? (uint64_t)p->hi_slots : (uint64_t)(E + s);
-                const uint64_t rb0 = (uint64_t)H * Ls.bits / 8, rb1 = (uint64_t)I * Ls.bits / 8;
-                const uint64_t d0[4] = {rb0, (uint64_t)I, 2, slots}, s0[3] = {rb0, (uint64_t)Ls.codes_stride, (uint64_t)Ls.bytes};
-                const uint64_t d1[3] = {rb1, (uint64_t)H, slots}, s1[2] = {rb1, (uint64_t)Ls.bytes};
-                for (int wi = 0; wi < 3; ++wi) {
-                    const uint32_t W = 128u >> wi;
-                    const CUtensorMapSwizzle sw = wi == 0 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                                : wi == 1 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-                    const uint32_t b0[4] = {W, 64, 2, 1}, b1[3] = {W, 128, 1};
-                    ok &= make_map(&d.cq[t][0][wi], CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, d0, s0, b0, sw);
-                    ok &= make_map(&d.cq[t][1][wi], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base + 2 * Ls.codes_stride, d1, s1,
-                                   b1, sw);
-                }
-            }
-            if (!ok) { dx_set_error("decode tensor map encoding failed (layer %d)", l); return DX_ERR_CUDA; }
-        }
-        DecBMaps& bmh = p->dec_bmaps;
-        memset(&bmh, 0, sizeof(bmh));
-        for (int ph = 0; ph < 2; ++ph) {
-            const uint64_t K = ph == 0 ? (uint64_t)H : (uint64_t)I;
-            const uint64_t dd[3] = {64, (uint64_t)p->n_ent, K / 64}, ss[2] = {K * 2, 128};
-            for (int ri = 0; ri < 3; ++ri)
-                for (int ki = 0; ki < 4; ++ki) {
-                    const uint32_t b[3] = {64, 16u << ri, 1u << ki};
-                    if (!make_map(&bmh.b[ph][ri][ki], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ph == 0 ? (void*)p->Xp : (void*)p->act,
-                                  dd, ss, b, CU_TENSOR_MAP_SWIZZLE_128B)) {
-                        dx_set_error("decode tensor map encoding failed (activations)");
-                        return DX_ERR_CUDA;
-                    }
-                }
         }
     }
     for (int i = 0; i < 3; ++i) {                           // {rows, chunks}: {16, 4}, {32, 4}, {16, 8}
@@ -885,11 +834,6 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     inf.export_bytes_hi = cfg->high_bits == 16 ? n3 * 2 : n3 + n3 / p->g * 3;
     inf.export_bytes_lo = n3 + n3 / p->g * 3;
     gemm_trap_init();
-    dec_trap_init();
-    {
-        const char* e = getenv("DX_DEC");
-        p->use_kdec = e && e[0] == '1';
-    }
     st = build_maps(p);
     if (st != DX_OK) return fail(st);
     *out = p;
@@ -1292,20 +1236,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         // tcgen05 grouped GEMMs (k_gemm.cu) over the rows placed in Xp: gate/up + SwiGLU, then down.
         // m_e <= T for top-k routing; the owner side (k = 1) sees m_e <= T rows as well.
         const bool dec = gemm_decode_cfg(m_max >= 0 ? m_max : T);
-        if (dec && p->use_kdec) {
-            // decode configuration: k_dec.cu (every weight tile read and dequantised once)
-            DecArgs da;
-            da.layer = a.arena_layer; da.hi_base = p->hi_base; da.hi = p->hi; da.lo = p->lo;
-            da.tier = a.tier; da.slot = a.slot; da.off = ws.off; da.act_e = ws.act_e; da.n_act = ws.n_act;
-            da.perm = ws.perm; da.gate = ws.gate; da.H = p->H; da.I = p->I; da.g = p->g; da.k = k;
-            da.act = p->act; da.Y = p->Y; da.sched = p->gemm_sched;
-            da.E_loc = E; da.shared_slot = p->shared_slot;
-            static const int dbg = [] { const char* s = getenv("DX_GEMM_DBG"); return s ? atoi(s) : 0; }();
-            da.dbg = dbg;
-            launch_dec(0, p->dec_maps[layer], p->dec_bmaps, da, max_act * (p->I / 64), p->cs);
-            if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
-            launch_dec(1, p->dec_maps[layer], p->dec_bmaps, da, max_act * ((p->H + 127) / 128), p->cs);
-        } else {
+        {
         GemmArgs ga;
         ga.layer = a.arena_layer; ga.hi_base = p->hi_base; ga.hi = p->hi; ga.lo = p->lo;
         ga.tier = a.tier; ga.slot = a.slot; ga.off = ws.off; ga.act_e = ws.act_e; ga.n_act = ws.n_act;

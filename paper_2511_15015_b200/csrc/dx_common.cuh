@@ -336,45 +336,6 @@ struct GemmArgs {
 };
 bool gemm_decode_cfg(int T);
 
-// k_dec.cu (decode configuration, T <= 64): the host keeps one DecMaps per layer and one DecBMaps per pool
-// and passes one phase's maps by value (DecPhaseMaps, a __grid_constant__ kernel parameter).  Maps in
-// global memory would need a tensormap-proxy acquire on every use: the TMA unit caches descriptors by
-// address, and a later pool reusing the address would otherwise read another pool's stale maps.
-struct DecMaps {
-    CUtensorMap a16[2];             // [phase] bf16 HIGH weights: gate/up {K, rows, mat, slot} box {64, 64, 2, 1};
-                                    // down {K, rows, slot} box {64, 128, 1}; 128 B swizzle
-    CUtensorMap cq[2][2][3];        // [tier 0 LOW / 1 HIGH][phase][box width 128 / 64 / 32 B] raw codes,
-                                    // matching 128 / 64 / 32 B swizzle
-};
-struct DecBMaps {
-    CUtensorMap b[2][3][4];         // [phase: Xp / act][N rows 16 / 32 / 64][K chunks per box 1 / 2 / 4 / 8]
-};
-struct DecArgs {
-    const uint8_t* layer;
-    i64 hi_base;
-    SlotLayout hi, lo;
-    const int32_t* tier;
-    const int32_t* slot;
-    const int32_t* off;
-    const int32_t* act_e;
-    const int32_t* n_act;
-    const int32_t* perm;
-    const float* gate;
-    int H, I, g, k;
-    int E_loc, shared_slot;         // f-3 (as GemmArgs)
-    __nv_bfloat16* act;
-    __nv_bfloat16* Y;
-    int* sched;
-    int dbg;
-};
-void dec_trap_init();
-int dec_trap_report(char* buf, size_t n);
-struct DecPhaseMaps {
-    CUtensorMap a16;                // DecMaps::a16[phase]
-    CUtensorMap cq[2][3];           // DecMaps::cq[tier][phase][width]
-    CUtensorMap b[3][4];            // DecBMaps::b[phase]
-};
-void launch_dec(int phase, const DecMaps& lm, const DecBMaps& bm, const DecArgs& a, int max_items, cudaStream_t st);
 void gemm_trap_init();                            // host-mapped watchdog record (once per process)
 int gemm_trap_report(char* buf, size_t n);        // appends the record, if a k_gemm wait timed out
 void launch_gemm(int phase, bool dec, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st);
