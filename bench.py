@@ -446,8 +446,8 @@ def run_ours(a, rank, world, local_rank):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ffn_traffic.json")
     if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get("gateup_dram_bytes_per_launch")
+        with open(tpath) as f:     # measured DRAM bytes per launch of the same kernel (one ncu --set full capture)
+            traffic = json.load(f).get("fused_dram_bytes_per_launch" if fused else "gateup_dram_bytes_per_launch")
     out = {
         "metric": METRIC, "value": world * B * L * a.steps / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
@@ -462,7 +462,7 @@ def run_ours(a, rank, world, local_rank):
                    "parallelism": f"ep{G}" if ep_mode else (f"replicas x{world}" if world > 1 else "single"),
                    "l2": "no flush: each step streams >=48 distinct layers of weights (> 126 MB L2)"},
         "roofline": {"bound": "hbm", "kernel": rf_kernel, "achieved": rf_ach, "peak": peak,
-                     "unit": "GB/s", "frac": rf_ach / peak, "traffic": None if fused else traffic, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": rf_ach / peak, "traffic": traffic, "peak_source": peak_src,
                      "ffn_both_phases_gbs": ach_all, "ffn_both_frac": ach_all / peak,
                      # the whole layer (routing, both GEMMs, combine, fold, plan periods, switching): every touched
                      # expert's algorithmic weight bytes over the device time of the whole timed stack

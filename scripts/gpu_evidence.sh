@@ -19,7 +19,7 @@ python scripts/launch_summary.py $O/${T}_launches.csv > $O/${T}_launch_summary.t
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -s 300 -c 200 --csv --log-file $O/${T}_prefill_launches.csv \
   python bench.py --batch 4096 --layers 4 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --prefill-tokens 0 --no-batch-sweep --no-q80b --no-teleport --no-prefetch-leg > $O/${T}_pll.log 2>&1
 python scripts/launch_summary.py $O/${T}_prefill_launches.csv > $O/${T}_prefill_launch_summary.txt; cat $O/${T}_prefill_launch_summary.txt
-DX_LOG_BYTES=1 DX_WATCHDOG_S=60 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gemm' -s 400 -c 4 -o $O/${T}_ncu_decode -f \
+DX_LOG_BYTES=1 DX_WATCHDOG_S=60 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gemm' -s 200 -c 4 -o $O/${T}_ncu_decode -f \
   python bench.py --layers 8 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --prefill-tokens 0 --no-batch-sweep --no-q80b --no-teleport --no-prefetch-leg > $O/${T}_ncu_decode.log 2>&1
 echo "ncu decode rc=$?"
 DX_WATCHDOG_S=60 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_(gemm|wide)' -s 200 -c 4 -o $O/${T}_ncu_prefill -f \
