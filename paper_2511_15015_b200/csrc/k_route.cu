@@ -413,6 +413,8 @@ __global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
     }
     DX_GRID_WAIT();
     RDEC_T(1)
+    // this thread's expert's published tier (phase C's HIGH-first active list): read now, used after the barrier
+    const int tier_e = ((int)threadIdx.x < E && a.rs.tier) ? __ldcg(a.rs.tier + threadIdx.x) : 0;
     if (a.wr) {
         // ---------------- A: partial router logits over this CTA's K slice (router in full precision).
         // The slice of the tile's 16 x rows and of W_r (ECH experts per round) is staged in shared memory by bulk
@@ -547,11 +549,14 @@ __global__ void __launch_bounds__(512) k_route_dec(const RouteDecArgs a) {
 #pragma unroll
         for (int c2 = 0; c2 < RDEC_CHUNKS; ++c2) c += (uint32_t)chist[c2 * E + e];
     }
-    const int32_t o = block_excl_scan<int32_t>((int32_t)c, tmp, &total_s);
-    const int32_t ac = block_excl_scan<int32_t>(c > 0 ? 1 : 0, tmp, &na_s);
-    // active list HIGH tier first (the grouped GEMMs hand out work items in this order, heaviest first)
-    const int32_t hi = (e < E && c && a.rs.tier && a.rs.tier[e]) ? 1 : 0;
-    const int32_t ah = block_excl_scan<int32_t>(hi, tmp, &nhi_s);
+    // one block scan of three packed 10-bit counts (every sum <= 512): rows, active experts, active HIGH experts;
+    // the active list puts the HIGH tier first (the grouped GEMMs hand out work items in this order, heaviest first)
+    const int32_t hi = (c && tier_e) ? 1 : 0;
+    int32_t ptot;
+    const int32_t pk = block_excl_scan<int32_t>((int32_t)c | ((c > 0 ? 1 : 0) << 10) | (hi << 20), tmp, &ptot);
+    const int32_t o = pk & 1023, ac = (pk >> 10) & 1023, ah = (pk >> 20) & 1023;
+    if (threadIdx.x == 0) { total_s = ptot & 1023; na_s = (ptot >> 10) & 1023; nhi_s = (ptot >> 20) & 1023; }
+    __syncthreads();
     if (e < E) {
         if (blockIdx.x == 0) {
             a.ws.off[e] = o;
