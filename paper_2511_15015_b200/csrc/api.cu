@@ -169,6 +169,7 @@ struct dx_pool_s {
     int4* plan_host = nullptr;              // pinned [L][E_loc] copy of the device plan list
     int32_t* plan_n_host = nullptr;         // pinned [L]
     std::vector<cudaEvent_t> ev_planh;      // plan copied to the host
+    std::vector<cudaEvent_t> ev_plandone;   // plan kernel done (compute stream): the side stream copies the plan out
     std::vector<int> xfer_pending;          // per layer: plan made, transfers not yet issued
     int n_pending = 0;
                                             // configuration (A/B runs; measured slower on the int tiers)
@@ -419,6 +420,11 @@ static void io_worker(dx_pool p) {
         }
         dx_status st = DX_OK;
         for (auto& c : job.copies) {
+            if (p->ssd_fd < 0) {             // DRAM tier: the pinned HIGH image straight to its block
+                if (cudaMemcpyAsync(c.second, p->hi_img_host[c.first], p->img_bytes, cudaMemcpyHostToDevice, p->ss) !=
+                    cudaSuccess) { st = DX_ERR_CUDA; break; }
+                continue;
+            }
             std::lock_guard<std::mutex> lk(p->io_mu);
             const uint8_t* img;
             int sl;
@@ -443,7 +449,7 @@ static void io_worker(dx_pool p) {
 
 // the I/O worker finished the layer's hand-over (or, layer < 0, every hand-over); its first error, if any
 static dx_status io_wait(dx_pool p, int layer) {
-    if (p->ssd_fd < 0 || !p->io_thread.joinable()) return DX_OK;
+    if (!p->io_thread.joinable()) return DX_OK;
     std::unique_lock<std::mutex> lk(p->io_mu);
     p->io_cv.wait(lk, [&] { return layer >= 0 ? p->io_pending[layer] == 0 : p->io_inflight == 0; });
     const dx_status e = p->io_err;
@@ -644,6 +650,8 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
     for (int l = 0; l < L; ++l) cudaEventCreateWithFlags(&p->ev_side[l], cudaEventDisableTiming);
     p->ev_planh.resize(L);
     for (int l = 0; l < L; ++l) cudaEventCreateWithFlags(&p->ev_planh[l], cudaEventDisableTiming);
+    p->ev_plandone.resize(L);
+    for (int l = 0; l < L; ++l) cudaEventCreateWithFlags(&p->ev_plandone[l], cudaEventDisableTiming);
     p->xfer_pending.assign(L, 0);
     p->t.assign(L, 0);
     p->publish_at.assign(L, -1);
@@ -815,9 +823,16 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         const int fd2 = open(ssd_path, O_RDONLY | O_DIRECT);
         if (fd2 >= 0 && p->img_bytes % 4096 == 0) { close(p->ssd_fd); p->ssd_fd = fd2; p->ssd_direct = true; }
         else if (fd2 >= 0) close(fd2);
-        cudaGetDevice(&p->device);
-        p->io_pending.assign(L, 0);
-        p->io_thread = std::thread(io_worker, p);
+    }
+    {
+        // the transfer thread: issues the runtime plans' promotion copies (and SSD reads) off the forward-issuing
+        // host thread (DX_XFER_THREAD=0: inline on the calling thread, as for EP pools)
+        static const bool xt = [] { const char* e = getenv("DX_XFER_THREAD"); return !e || atoi(e) != 0; }();
+        if (ssd || (xt && !nccl_id && !ep_group)) {
+            cudaGetDevice(&p->device);
+            p->io_pending.assign(L, 0);
+            p->io_thread = std::thread(io_worker, p);
+        }
     }
 
     dx_info& inf = p->info;
@@ -889,6 +904,7 @@ extern "C" dx_status dx_pool_destroy(dx_pool p) {
     if (p->comm) ep_nccl_destroy(p->comm);
     if (p->ep_pairs_host) cudaFreeHost(p->ep_pairs_host);
     for (auto ev : p->ev_planh) cudaEventDestroy(ev);
+    for (auto ev : p->ev_plandone) cudaEventDestroy(ev);
     for (auto ev : p->ev_pf) cudaEventDestroy(ev);
     for (auto ev : p->cache_ev) cudaEventDestroy(ev);
     if (p->ssd_cache) cudaFreeHost(p->ssd_cache);
@@ -1635,7 +1651,10 @@ static dx_status fold_prepare(dx_pool p, int layer, FoldReq* req) {
             p->prof_wait_ev.push_back(e1);
             DX_CUDA(cudaEventRecord(e0, p->cs));
         }
-        DX_CUDA(cudaStreamWaitEvent(p->cs, p->ev_side[layer], 0));
+        // a side stream that already finished needs no cross-stream dependency (which would break the PDL chain)
+        const cudaError_t q = cudaEventQuery(p->ev_side[layer]);
+        if (q == cudaErrorNotReady) DX_CUDA(cudaStreamWaitEvent(p->cs, p->ev_side[layer], 0));
+        else DX_CHECK(q == cudaSuccess, DX_ERR_CUDA, "side-stream event: %s", cudaGetErrorString(q));
         if (e1) DX_CUDA(cudaEventRecord(e1, p->cs));
         p->publish_at[layer] = -1;
     }
@@ -1726,7 +1745,9 @@ static dx_status issue_transfers(dx_pool p, int layer) {
     const int n = p->plan_n_host[layer];
     int nd = 0;
     for (int i = 0; i < n; ++i) nd += p->plan_host[layer * E + i].y == -1;
-    if (nd > 0) {                    // demotions: device quantisation on the second side stream, beside the copies
+    // TIMING ATTRIBUTION ONLY (results wrong): DX_XFER_SKIP=1 skips the demotions' quantisation, =2 the promotions' copies
+    static const int xfer_skip = [] { const char* e = getenv("DX_XFER_SKIP"); return e ? atoi(e) : 0; }();
+    if (nd > 0 && xfer_skip != 1) {  // demotions: device quantisation on the second side stream, beside the copies
         DX_CUDA(cudaStreamWaitEvent(p->ss2, p->ev_planh[layer], 0));
         launch_transitions(p->ctrl, layer, xfer_args(p, layer), n, 3, p->ss2);
         DX_CUDA(cudaEventRecord(p->ev_dem, p->ss2));
@@ -1735,8 +1756,9 @@ static dx_status issue_transfers(dx_pool p, int layer) {
     const size_t bytes = p->hi.bits == 16 ? (size_t)3 * p->I * p->H * 2 : (size_t)p->hi.bytes;
     uint8_t* hi_region = p->weights + (size_t)layer * p->layer_bytes + p->hi_base;
     u64 np = 0;
-    if (p->ssd_fd >= 0 && p->io_thread.joinable()) {
-        // f-4: hand the SSD reads and their copies to the I/O thread; it records ev_side when they are issued
+    if (p->io_thread.joinable()) {
+        // hand the promotions' copies (f-4: and the SSD reads) to the transfer thread; it records ev_side when they
+        // are issued, so the host thread issuing the forwards never spends its time on them
         dx_pool_s::IoJob job{layer, {}, nd > 0, nullptr, nullptr};
         for (int i = 0; i < n; ++i) {
             const int4 cmd = p->plan_host[layer * E + i];
@@ -1774,6 +1796,7 @@ static dx_status issue_transfers(dx_pool p, int layer) {
         bool hit = false;                          // staged by the prefetch into this very block already
         for (const int2& sg : p->staged[layer]) hit |= sg.x == cmd.x && sg.y == cmd.z;
         if (hit) { ++p->pf_hits; continue; }
+        if (xfer_skip == 2) continue;
         dx_status rc = copy_high_image(p, layer * E + cmd.x, hi_region + (size_t)cmd.z * p->hi.bytes, p->ss);
         if (rc != DX_OK) return rc;
         ++np;
@@ -1785,7 +1808,7 @@ static dx_status issue_transfers(dx_pool p, int layer) {
         p->prof_copy_ev.push_back(xc);
         p->prof_copy_bytes.push_back(np * bytes);
     }
-    if (nd > 0) DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_dem, 0));
+    if (nd > 0 && xfer_skip != 1) DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_dem, 0));
     if (x0) {
         cudaEvent_t x1 = prof_event(p);
         p->prof_xfer_ev.push_back(x1);
@@ -1872,13 +1895,16 @@ extern "C" dx_status dx_plan_precision(dx_pool p, int32_t layer, dx_plan* out) {
     if (p->teleport) {
         DX_CUDA(cudaEventRecord(p->ev_side[layer], p->cs));
     } else {
-        // the plan to pinned host memory; the transfers are issued once the host sees it (issue_transfers)
+        // the plan to pinned host memory, copied on the side stream (copies on the compute stream would break the
+        // programmatic-dependent-launch chain of the forwards); the transfers are issued once the host sees it
         const size_t E = (size_t)p->E_loc;
+        DX_CUDA(cudaEventRecord(p->ev_plandone[layer], p->cs));
+        DX_CUDA(cudaStreamWaitEvent(p->ss, p->ev_plandone[layer], 0));
         DX_CUDA(cudaMemcpyAsync(p->plan_n_host + layer, p->ctrl.plan_n + layer, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                p->cs));
+                                p->ss));
         DX_CUDA(cudaMemcpyAsync(p->plan_host + layer * E, p->ctrl.plan_cmd + layer * E, E * sizeof(int4),
-                                cudaMemcpyDeviceToHost, p->cs));
-        DX_CUDA(cudaEventRecord(p->ev_planh[layer], p->cs));
+                                cudaMemcpyDeviceToHost, p->ss));
+        DX_CUDA(cudaEventRecord(p->ev_planh[layer], p->ss));
         p->xfer_pending[layer] = 1;
         p->n_pending += 1;
     }
