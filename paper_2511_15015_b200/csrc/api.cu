@@ -825,9 +825,10 @@ static dx_status pool_create(const dx_config* cfg, const void* const* master, vo
         else if (fd2 >= 0) close(fd2);
     }
     {
-        // the transfer thread: issues the runtime plans' promotion copies (and SSD reads) off the forward-issuing
-        // host thread (DX_XFER_THREAD=0: inline on the calling thread, as for EP pools)
-        static const bool xt = [] { const char* e = getenv("DX_XFER_THREAD"); return !e || atoi(e) != 0; }();
+        // the transfer thread: issues the SSD tier's reads and copies off the forward-issuing host thread.  For DRAM
+        // pools it is opt-in (DX_XFER_THREAD=1): measured, it did not lower the exposed switch time and the hand-over
+        // at publication cost the end-to-end loop (host copy + sync every step) ~6 %
+        static const bool xt = [] { const char* e = getenv("DX_XFER_THREAD"); return e && atoi(e) != 0; }();
         if (ssd || (xt && !nccl_id && !ep_group)) {
             cudaGetDevice(&p->device);
             p->io_pending.assign(L, 0);
