@@ -1246,6 +1246,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
     a.H = p->H; a.I = p->I; a.g = p->g; a.k = k;
     if (ev[1]) DX_CUDA(cudaEventRecord(ev[1], p->cs));
     const int ns = k == p->k ? p->cfg.n_shared : 0;            // the owner-side (k = 1) EP path has no shared rows
+    int ffn_launches = 2;                                       // kernels launched for a6/a7 (counted below)
     const int max_act = (T * k < E ? T * k : E) + ns;
     if (p->ffn_path == 1) {
         launch_expert_ffn(a, (const __nv_bfloat16*)x, ws.gate, ws, T, E, p->act, p->Y, p->cs, ev[2]);
@@ -1276,12 +1277,14 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
             for (int i = 0; i < 4; ++i) gm.xb1[i] = p->xb1[i];
             for (int i = 0; i < 3; ++i) gm.xk1[i] = p->xk1[i];
             launch_gemm(2, true, gm, ga, max_act * (p->I / 64 + (p->H + 127) / 128), p->cs);
+            ffn_launches = 1;
             if (ev[2]) {
                 DX_CUDA(cudaEventRecord(ev[2], p->cs));
                 ++p->prof_fused;
             }
         } else {
         if (wide) launch_wide(0, gm, ga, max_act * (p->I / 64), p->cs);
+        if (wide) ffn_launches = 4;
         launch_gemm(0, dec, gm, ga, max_act * (p->I / 64), p->cs);
         if (ev[2]) DX_CUDA(cudaEventRecord(ev[2], p->cs));
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb1[i];
@@ -1302,7 +1305,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
     } else {
         launch_combine(p->Y, T, k, p->H, (__nv_bfloat16*)y, p->cs, nullptr, nullptr, nullptr, ns ? T * k : -1);
     }
-    p->launches += 3;
+    p->launches += ffn_launches + 1;                            // + the combine
     cudaError_t ce = cudaGetLastError();
     DX_CHECK(ce == cudaSuccess, DX_ERR_CUDA, "launch failed: %s", cudaGetErrorString(ce));
     static const bool log_bytes = getenv("DX_LOG_BYTES") != nullptr;
