@@ -101,6 +101,7 @@ struct dx_pool_s {
     std::vector<GemmMaps> gmaps;            // per layer (weights); xb filled per launch
     CUtensorMap xb0[4], xb1[4];             // B operand maps (Xp / act) for tiles of 16, 32, 64, 128 rows
     CUtensorMap xw0, xw1;                   // the same, 256-row tiles (k_wide)
+    CUtensorMap xp0, xp1;                   // the same, 192-row tiles (k_gemm prefill)
     CUtensorMap xk0[3], xk1[3];             // 3-D B maps (Xp / act): several K chunks per box (decode int)
     // expert parallelism over NCCL (ep_nccl.cu): library-owned communicator and exchange buffers
     void* comm = nullptr;
@@ -251,11 +252,13 @@ static dx_status build_maps(dx_pool p) {
         const uint64_t d0[2] = {(uint64_t)H, rows}, s0[1] = {(uint64_t)H * 2};
         const uint64_t d1[2] = {(uint64_t)I, rows}, s1[1] = {(uint64_t)I * 2};
         const uint32_t b[2] = {64, bn};
-        const uint32_t bw[2] = {64, 256};
+        const uint32_t bw[2] = {64, 256}, bp[2] = {64, 192};
         if (!make_map(&p->xb0[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->Xp, d0, s0, b, CU_TENSOR_MAP_SWIZZLE_128B) ||
             !make_map(&p->xb1[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, b, CU_TENSOR_MAP_SWIZZLE_128B) ||
             (i == 0 && (!make_map(&p->xw0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->Xp, d0, s0, bw, CU_TENSOR_MAP_SWIZZLE_128B) ||
-                        !make_map(&p->xw1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, bw, CU_TENSOR_MAP_SWIZZLE_128B)))) {
+                        !make_map(&p->xw1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, bw, CU_TENSOR_MAP_SWIZZLE_128B) ||
+                        !make_map(&p->xp0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->Xp, d0, s0, bp, CU_TENSOR_MAP_SWIZZLE_128B) ||
+                        !make_map(&p->xp1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p->act, d1, s1, bp, CU_TENSOR_MAP_SWIZZLE_128B)))) {
             dx_set_error("tensor map encoding failed (activations)");
             return DX_ERR_CUDA;
         }
@@ -1271,6 +1274,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb0[i];
         for (int i = 0; i < 3; ++i) gm.xk[i] = p->xk0[i];
         gm.xw = p->xw0;
+        gm.xb192 = p->xp0;
         static const bool fuse_on = [] { const char* e = getenv("DX_FUSE"); return !e || atoi(e) != 0; }();
         if (dec && fuse_on) {
             // decode: gate/up + SwiGLU and down + gate scaling in ONE launch (down items wait per expert)
@@ -1290,6 +1294,7 @@ static dx_status expert_ffn(dx_pool p, int layer, const RouteWs& ws, const void*
         for (int i = 0; i < 4; ++i) gm.xb[i] = p->xb1[i];
         for (int i = 0; i < 3; ++i) gm.xk[i] = p->xk1[i];
         gm.xw = p->xw1;
+        gm.xb192 = p->xp1;
         if (wide) launch_wide(1, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
         launch_gemm(1, dec, gm, ga, max_act * ((p->H + 127) / 128), p->cs);
         }

@@ -308,6 +308,7 @@ struct GemmMaps {
     // B operands (token rows [rows][K] bf16, 128 B swizzle)
     CUtensorMap xb[4];              // 2-D boxes {64, 16/32/64/128}
     CUtensorMap xw;                 // 2-D box {64, 256}: the wide prefill tiles of k_wide
+    CUtensorMap xb192;              // 2-D box {64, 192}: k_gemm's prefill tiles
     CUtensorMap xb1[4], xk1[3];     // fused decode launch: the down phase's B maps (act rows)
     CUtensorMap xk[3];              // 3-D {64, rows, K/64}: boxes {64,16,4}, {64,32,4}, {64,16,8} (decode int stages)
 };

@@ -67,12 +67,16 @@ constexpr int TAB_BYTES = 128 * GTAB * 3;     // one item's table: [128 rows][G]
 // quantised stage; otherwise (prefill) N <= 128 and one chunk per stage for every tier.
 template <bool DEC>
 struct Cfg {
-    static constexpr int NBMAX = DEC ? 64 : 128;
+    // prefill: N tiles of 192 tokens (an int item's dequantised chunk feeds 1.5x the MMAs of a 128 tile; the two
+    // 192-column accumulators leave 4 TMEM A buffers, one per dequant group), 4 stages of 16 KB A + 24 KB B
+    static constexpr int NBMAX = DEC ? 64 : 192;
+    static constexpr int STG = DEC ? STAGES : 4;
+    static constexpr int SBYTES = DEC ? STAGE_BYTES : A_BYTES + 192 * 128;
     static constexpr int ACH = DEC ? 4 : 1;                    // K chunks per TMEM A buffer (32 columns each)
     static constexpr int NA = (512 - 2 * NBMAX) / (32 * ACH);  // TMEM A buffers: 3 (decode) / 8 (prefill)
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + Roles<DEC>::EPI_TEAMS * XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES +
+    static constexpr int SMEM = 1024 + STG * SBYTES + Roles<DEC>::EPI_TEAMS * XCH_BYTES + 2048 + RING * 32 + 2 * TAB_BYTES +
                                 (DEC ? ETAB_BYTES : TPRE_BYTES);
-    __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : 128; }
+    __device__ static int nb(int bits) { return DEC ? (bits == 16 ? 64 : (bits == 4 ? 32 : 16)) : NBMAX; }
     __device__ static int ks(int bits) { return (DEC && bits != 16) ? 16 / bits : 1; }   // int4: 4, int2: 8
 };
 
@@ -255,6 +259,9 @@ __device__ __forceinline__ int box_rows(int nvalid) {        // B tile rows: pow
     while (r < nvalid) r <<= 1;
     return r;
 }
+__device__ __forceinline__ int box_rows_p(int nvalid) {      // k_gemm prefill: 16 .. 128, then 192
+    return nvalid <= 128 ? box_rows(nvalid) : 192;
+}
 
 template <int PHASE, bool DEC>
 __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
@@ -262,12 +269,12 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
     using C = Cfg<DEC>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sS = smem;                                   // [STAGES][A 16 KB | B 16 KB]
-    float* xch = reinterpret_cast<float*>(sS + STAGES * STAGE_BYTES);            // [32 cols][64 rows]
+    uint8_t* sS = smem;                                   // [C::STG][A 16 KB | B 16 KB]
+    float* xch = reinterpret_cast<float*>(sS + C::STG * C::SBYTES);            // [32 cols][64 rows]
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + EPI_TEAMS * XCH_BYTES);
-    uint64_t* full = bars;                                // [STAGES] TMA landed (A or raw, and B)
-    uint64_t* empty = full + STAGES;                      // [STAGES] MMA finished with the stage
-    uint64_t* aready = empty + STAGES;                    // [NA] transform wrote TMEM A buffer
+    uint64_t* full = bars;                                // [C::STG] TMA landed (A or raw, and B)
+    uint64_t* empty = full + C::STG;                      // [C::STG] MMA finished with the stage
+    uint64_t* aready = empty + C::STG;                    // [NA] transform wrote TMEM A buffer
     uint64_t* aempty = aready + C::NA;                    // [NA] MMA finished with TMEM A buffer
     uint64_t* tfull = aempty + C::NA;                     // [2] accumulator ready
     uint64_t* tempty = tfull + 2;                         // [2] accumulator drained
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
 
     // prologue independent of the predecessor kernels (overlaps their tail under PDL)
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1 + NTW); }
+        for (int s = 0; s < C::STG; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1 + NTW); }
         for (int b = 0; b < C::NA; ++b) { mbar_init(&aready[b], DEC ? NTW : 4); mbar_init(&aempty[b], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4);
@@ -405,15 +412,15 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
             const CUtensorMap* xkm = (FUSED && iph == 1) ? maps.xk1 : maps.xk;
             const int kunit = qt ? KCH * w.bits / 8 : KCH;     // A inner coordinate per chunk (bytes / elements)
             for (int c0 = 0; c0 < w.m; c0 += nb) {
-                const int rb = box_rows(min(nb, w.m - c0));
+                const int rb = DEC ? box_rows(min(nb, w.m - c0)) : box_rows_p(min(nb, w.m - c0));
                 const int ri = rb == 16 ? 0 : rb == 32 ? 1 : rb == 64 ? 2 : 3;
                 const bool multi = DEC && qt;                   // one B box carries the stage's ks chunks
-                const CUtensorMap* bmap = multi ? &xkm[w.bits == 2 ? 2 : ri] : &xbm[ri];
+                const CUtensorMap* bmap = multi ? &xkm[w.bits == 2 ? 2 : ri] : rb == 192 ? &maps.xb192 : &xbm[ri];
                 const uint32_t bytes = multi ? A_BYTES + ks * rb * 128 : (qt ? 128 * kunit : A_BYTES) + rb * 128;
                 for (int kb0 = 0; kb0 < nk; kb0 += ks) {
                     gwait(&empty[st], ph ^ 1, 2, 128);
                     if (elect_one()) {
-                        uint8_t* sA = sS + st * STAGE_BYTES;
+                        uint8_t* sA = sS + st * C::SBYTES;
                         mbar_arrive_expect_tx(&full[st], bytes);
                         if (iph == 0) tma_load_4d(sA, amap, &full[st], kb0 * kunit, arow, 0, w.slot);
                         else tma_load_3d(sA, amap, &full[st], kb0 * kunit, arow, w.slot);
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                         else tma_load_2d(sA + A_BYTES, bmap, &full[st], kb0 * KCH, w.r0 + c0);
                     }
                     __syncwarp();
-                    if (++st == STAGES) { st = 0; ph ^= 1; }
+                    if (++st == C::STG) { st = 0; ph ^= 1; }
                 }
             }
         }
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
             const int nk = nk_[FUSED ? w.ph : PHASE];
             const int nb = C::nb(w.bits), ks = C::ks(w.bits);
             for (int c0 = 0; c0 < w.m; c0 += nb, ++cc) {
-                const int rb = box_rows(min(nb, w.m - c0));
+                const int rb = DEC ? box_rows(min(nb, w.m - c0)) : box_rows_p(min(nb, w.m - c0));
                 const uint32_t idesc = idesc_bf16(128, rb);
                 const int buf = cc & 1;
                 gwait(&tempty[buf], ((cc >> 1) & 1) ^ 1, 3, DX_EPI_BACK / 2);
@@ -445,7 +452,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                     const int kc = min(ks, nk - kb0);
                     gwait(&full[st], ph, 4, 64);
                     tc_fence_after();
-                    const uint32_t sA = smem_u32(sS + st * STAGE_BYTES), sB = sA + A_BYTES;
+                    const uint32_t sA = smem_u32(sS + st * C::SBYTES), sB = sA + A_BYTES;
                     if (w.bits == 16) {
                         const uint64_t da = umma_desc_sw128(sA), db = umma_desc_sw128(sB);
                         if (elect_one()) {
@@ -489,7 +496,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                         else mma_commit(&empty[st]);
                     }
                     __syncwarp();
-                    if (++st == STAGES) { st = 0; ph ^= 1; }
+                    if (++st == C::STG) { st = 0; ph ^= 1; }
                 }
                 if (elect_one()) mma_commit(&tfull[buf]);
                 __syncwarp();
@@ -524,7 +531,7 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                     gwait(&full[st], ph, 7, 64);         // idle: poll gently
                     __syncwarp();                        // released by every transform warp too, so the
                     if (lane == 0) mbar_arrive(&empty[st]);   // producer can never lap an observer
-                    if (++st == STAGES) { st = 0; ph ^= 1; }
+                    if (++st == C::STG) { st = 0; ph ^= 1; }
                 }
                 continue;
             }
@@ -553,14 +560,14 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                 constexpr int BITS = decltype(bits_c)::value;
                 constexpr int KS = DEC ? 16 / BITS : 1;     // K chunks per stage
                 constexpr int ROWB = KCH * BITS / 8;        // code bytes per row per chunk
-                constexpr int NBB = DEC ? (BITS == 4 ? 32 : 16) : 128;
+                constexpr int NBB = DEC ? (BITS == 4 ? 32 : 16) : C::NBMAX;
                 for (int c0 = 0; c0 < w.m; c0 += NBB) {
                     for (int kb0 = 0; kb0 < nk; kb0 += KS) {
                         // every transform thread observes every phase of full[] (no phase aliasing)
                         gwait(&full[st], ph, 7, DX_TBACK);
                         const int cst = st;
-                        const uint32_t stage = stages_u32 + st * STAGE_BYTES;
-                        if (++st == STAGES) { st = 0; ph ^= 1; }
+                        const uint32_t stage = stages_u32 + st * C::SBYTES;
+                        if (++st == C::STG) { st = 0; ph ^= 1; }
                         const int kc = min(KS, nk - kb0);
                         for (int j0 = 0; j0 < kc; j0 += C::ACH, ++nbuf) {
                             const int cab = ab;
@@ -656,8 +663,10 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
         const int et = threadIdx.x - 32 * (W_EPI + 4 * team);   // 0..127
         const uint32_t nbar = 1 + team;
         float* xch_t = xch + team * (XCH_BYTES / 4);
-        int32_t* ent_t = team == 0 ? ent_s : reinterpret_cast<int32_t*>(xch_t);
-        float* gate_t = team == 0 ? gate_s : xch_t + 128;
+        // phase 1: the chunk's entry ids / gates (decode: <= 64 in the barrier block; prefill: <= 192 in the team's
+        // exchange buffer, which phase 1 does not otherwise use)
+        int32_t* ent_t = DEC ? ent_s : reinterpret_cast<int32_t*>(xch_t);
+        float* gate_t = DEC ? gate_s : xch_t + 256;
         int cc = 0;
         Item w;
         for (int ii = 0; take_item(a, ring, tkfull, tkempty, ii, n_items, nmb, w, n0, nmb1); ++ii) {
@@ -1010,7 +1019,8 @@ void launch_one(const GemmMaps& maps, const GemmArgs& a, int items, cudaStream_t
 bool gemm_decode_cfg(int T) { return T <= 64; }
 
 bool wide_enabled() {
-    static const bool on = [] { const char* e = getenv("DX_WIDE"); return !e || atoi(e) != 0; }();
+    // opt-in (DX_WIDE=1): with k_gemm's 192-token prefill tiles the single launch is faster (C3 602 vs 571 TFLOP/s)
+    static const bool on = [] { const char* e = getenv("DX_WIDE"); return e && atoi(e) != 0; }();
     return on;
 }
 void launch_wide(int phase, const GemmMaps& maps, const GemmArgs& a, int max_items, cudaStream_t st) {
