@@ -77,11 +77,13 @@ __global__ void __launch_bounds__(512) k_router(const __nv_bfloat16* __restrict_
 }
 
 // Router for larger T (prefill): a tiled tensor-core GEMM logits[T][E] = x[T][H] W_r[E][H]^T (+ b).  Block tile
-// 64 tokens x 128 experts, K in chunks of 64 staged through shared memory by cp.async (double-buffered; 16-byte
-// units XOR-swizzled by row so the ldmatrix row groups hit distinct banks), 8 warps
-// of 32 tokens x 32 experts (2 x 4 mma.sync m16n8k16 tiles, fragments by ldmatrix).  Each logit is one warp's
-// fp32 accumulation in K order: deterministic.  x is read once, W_r once per 64-token tile (from L2).
-constexpr int RT_M = 64, RT_N = 128, RT_K = 64, RT_LD = RT_K;   // rows of 8 16-byte units, unit c at c ^ (row & 7)
+// 32 tokens x 128 experts (T = 4096: 128 CTAs; 64-token tiles left 84 SMs idle: 34.8 -> 27.3 us), K in chunks of 64
+// staged through shared memory by cp.async (double-buffered; 16-byte units XOR-swizzled by row so the ldmatrix row
+// groups hit distinct banks), 8 warps of 16 tokens x 32 experts (1 x 4 mma.sync m16n8k16 tiles, fragments by
+// ldmatrix).  Each logit is one warp's fp32 accumulation in K order: deterministic.  x is read once, W_r once per
+// token tile (from L2).
+constexpr int RT_M = 32, RT_N = 128, RT_K = 64, RT_LD = RT_K;   // rows of 8 16-byte units, unit c at c ^ (row & 7)
+constexpr int RT_MI = RT_M / 32;               // 16-row m tiles per warp (8 warps: 2 along tokens x 4 along experts)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(pred ? 16 : 0));
 }
@@ -94,9 +96,9 @@ __global__ void __launch_bounds__(256) k_router_tiled(const __nv_bfloat16* __res
     DX_GRID_LAUNCH();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t0 = blockIdx.x * RT_M, e0 = blockIdx.y * RT_N;
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;        // warp tile origin in the block tile
+    const int wm = (warp & 1) * (RT_M / 2), wn = (warp >> 1) * 32;   // warp tile origin in the block tile
     auto stage = [&](int buf, int k0) {
-        // x: 64 rows x 8 16-byte units; W_r: 128 rows x 8 units -> 1536 units over 256 threads
+        // x: RT_M rows x 8 16-byte units; W_r: 128 rows x 8 units, over 256 threads
         for (int u = tid; u < (RT_M + RT_N) * 8; u += 256) {
             const int row = u >> 3, c = u & 7;
             if (row < RT_M) {
@@ -112,9 +114,9 @@ __global__ void __launch_bounds__(256) k_router_tiled(const __nv_bfloat16* __res
         }
         asm volatile("cp.async.commit_group;");
     };
-    float acc[2][4][4];
+    float acc[RT_MI][4][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < RT_MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -132,9 +134,9 @@ __global__ void __launch_bounds__(256) k_router_tiled(const __nv_bfloat16* __res
         __syncthreads();
 #pragma unroll
         for (int ks = 0; ks < RT_K; ks += 16) {
-            uint32_t a[2][4], b[4][2];
+            uint32_t a[RT_MI][4], b[4][2];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {                   // A 16x16: rows wm+16i.., ldmatrix.x4
+            for (int i = 0; i < RT_MI; ++i) {               // A 16x16: rows wm+16i.., ldmatrix.x4
                 const int r = wm + 16 * i + (lane & 15), cu = (ks >> 3) + (lane >> 4);
                 const uint32_t ad = (uint32_t)__cvta_generic_to_shared(&xs[buf][r][(cu ^ (r & 7)) * 8]);
                 asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(256) k_router_tiled(const __nv_bfloat16* __res
                 asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(b[j][0]), "=r"(b[j][1]) : "r"(ad));
             }
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < RT_MI; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) mma16816(acc[i][j], a[i][0], a[i][1], a[i][2], a[i][3], b[j][0], b[j][1]);
         }
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(256) k_router_tiled(const __nv_bfloat16* __res
     }
     const int g = lane >> 2, q = lane & 3;
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < RT_MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
