@@ -585,10 +585,10 @@ __global__ void __launch_bounds__(Roles<DEC>::THREADS, 1) k_gemm(const __grid_co
                                         uint32_t zz[2], ss[2];
                                         const uint32_t v0 = group_sz(k0 >> gsh);
                                         const uint32_t v1 = a.g >= 64 ? v0 : group_sz((k0 + 32) >> gsh);
-                                        zz[0] = (v0 >> 16) * 0x10001u;
-                                        ss[0] = (v0 & 0xFFFFu) * 0x10001u;
-                                        zz[1] = (v1 >> 16) * 0x10001u;
-                                        ss[1] = (v1 & 0xFFFFu) * 0x10001u;
+                                        zz[0] = __byte_perm(v0, 0u, 0x3232);   // bf16(128 + z) in both halves
+                                        ss[0] = __byte_perm(v0, 0u, 0x1010);   // bf16 s in both halves
+                                        zz[1] = __byte_perm(v1, 0u, 0x3232);
+                                        ss[1] = __byte_perm(v1, 0u, 0x1010);
                                         // raw codes of (row r, chunk j): decode stages hold one 128 B-swizzled
                                         // row of KS chunks (16 B unit c of row r at unit c ^ (r & 7)); prefill
                                         // stages one chunk
